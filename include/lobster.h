@@ -1,0 +1,168 @@
+/*
+ * lobster.h — C ABI of the B200-native semi-naive fixpoint engine.
+ *
+ * The engine evaluates a stratified Datalog program over semiring-tagged
+ * relations by semi-naive fixpoint iteration on one CUDA device (sm_100a).
+ * The four calls follow the paper's statement of the problem:
+ *   - a stratified program of rules          PAPER.md:383-410 (§3.1, Fig. 6)
+ *   - an input database of tagged facts      PAPER.md:285-287 (§2), 413-422
+ *   - batched samples (sample-id register)   PAPER.md:681-691 (§4.3)
+ *   - fixpoint evaluation                    PAPER.md:599-611 (§3.4), 1366-1392 (Alg. 1)
+ *   - outputs read back per sample with tags and gradients
+ *                                            PAPER.md:685 (§4.3), 292 (§2)
+ * Readings of silent / ambiguous passages: SURVEY.md §8(c), restated in
+ * DESIGN.md ("Readings").
+ *
+ * Conventions
+ *   - Every call returns lobster_status; no C++ exception crosses the ABI.
+ *   - All device work is ordered on lobster_options.cuda_stream (NULL = the
+ *     legacy default stream).  Calls are blocking with respect to the host
+ *     unless stated otherwise.
+ *   - One context per host thread; a context is not shareable.
+ *   - Call order: program_load -> facts_push* -> run -> output_get*.  The
+ *     first facts_push after a completed run starts a new database: every
+ *     relation's facts, every output and the fact-id counter are reset.
+ *   - There is no CPU fallback: if the CUDA device is unavailable every call
+ *     that needs it fails with LOBSTER_E_CUDA.
+ */
+#ifndef LOBSTER_H
+#define LOBSTER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lobster_ctx lobster_ctx; /* opaque; owns all device and output memory */
+
+typedef enum {
+  LOBSTER_OK = 0,
+  LOBSTER_E_INVALID_ARG = 1, /* NULL pointer, bad enum, unknown relation name in output_get */
+  LOBSTER_E_PARSE = 2,       /* program text error; message "line:col: msg"          */
+  LOBSTER_E_SCHEMA = 3,      /* unknown input relation / arity mismatch / batched w/o samples */
+  LOBSTER_E_RANGE = 4,       /* prob NaN or outside [0,1]; sample id out of range; key or
+                                witness wider than 64 / 32 bits                               */
+  LOBSTER_E_STATE = 5,       /* call out of order (push before load, get before run, ...)    */
+  LOBSTER_E_OOM = 6,         /* device allocation failed                                      */
+  LOBSTER_E_ITER_CAP = 7,    /* max_iters rounds reached in a stratum (state readable)        */
+  LOBSTER_E_CUDA = 8,        /* CUDA error; sticky: the context must be destroyed             */
+  LOBSTER_E_NCCL = 9         /* collective failure (reserved for the multi-GPU layer)         */
+} lobster_status;
+
+/* Provenance semirings (PAPER.md:445-456 Fig. 7b; :616-617 §3.5).
+ *   UNIT               : Bool {⊥,⊤}, ∨, ∧.  No tag is stored.
+ *   MAX_MIN_PROB       : [0,1], 0, 1, max, min                         (Fig. 7b)
+ *   ADD_MULT_PROB      : [0,∞) unclamped, 0, 1, +, ×; ⊕ within a round accumulates
+ *                        in fp64 and rounds once to fp32                 (reading 6, 9)
+ *   DIFF_MAX_MULT_PROB : [0,1] × witness, 0, 1, max (strict improvement; ties keep
+ *                        the existing tag, same-round ties pick the smallest
+ *                        (rule, non-head variables)), fp32 ×.  Gradients flow to
+ *                        the input facts of the winning derivation      (reading 7, 8) */
+typedef enum {
+  LOBSTER_UNIT = 0,
+  LOBSTER_MAX_MIN_PROB = 1,
+  LOBSTER_ADD_MULT_PROB = 2,
+  LOBSTER_DIFF_MAX_MULT_PROB = 3
+} lobster_semiring;
+
+typedef struct {
+  int32_t device;       /* CUDA device ordinal                                              */
+  void* cuda_stream;    /* cudaStream_t all work is ordered on (NULL = default stream)     */
+  int32_t batch_size;   /* samples per database (>= 1; 0 is treated as 1)                   */
+  int32_t max_iters;    /* per-stratum round cap; 0 = default 100000                        */
+  int64_t arena_bytes;  /* initial per-round scratch arena; 0 = auto (grows on demand)      */
+  int32_t micro_batch;  /* reserved (0 = whole batch in one fixpoint)                       */
+  int32_t rank;         /* this process's rank (informational; collectives live above)      */
+  int32_t world_size;   /* number of ranks (informational)                                   */
+  void* nccl_comm;      /* reserved                                                          */
+} lobster_options;
+
+/* Create a context on options->device.  options may be NULL (device 0, default
+ * stream, batch 1).  Errors: CUDA (no device), OOM. */
+lobster_status lobster_create(const lobster_options* options, lobster_ctx** out);
+void lobster_destroy(lobster_ctx* ctx);
+/* Message of the last failed call on ctx; valid until the next call on ctx. */
+const char* lobster_last_error(const lobster_ctx* ctx);
+
+/* Load a program (subset of Fig. 3c syntax):
+ *     type Cell = u32                                  -- alias, ignored (columns are int32)
+ *     type edge(x: Cell, y: Cell)                      -- batched input relation
+ *     shared type composition(a: i32, b: i32, c: i32)  -- input without a sample column
+ *     rel path(x, y) :- edge(x, y) or (path(x, z) and edge(z, y)).
+ *     rel endpoints_connected() :- is_endpoint(x), is_endpoint(y), path(x, y), x != y.
+ *     output endpoints_connected                       -- gradients are produced for outputs
+ * Bodies are conjunctions (',' or 'and') and disjunctions ('or', split into one
+ * rule per disjunct, left to right) of atoms and comparisons `a != b`, `a == b`
+ * between variables or integer constants.  Atom arguments are variables or
+ * integer constants.  Every rule needs at least one batched body atom.
+ * Stratification: SCCs of the predicate dependency graph in topological order
+ * (PAPER.md:383-389).  Errors: PARSE ("line:col: msg"; unbound head variable,
+ * unknown relation, arity mismatch); INVALID_ARG (bad semiring); STATE (called
+ * twice).  No device work. */
+lobster_status lobster_program_load(lobster_ctx* ctx, const char* program_text, lobster_semiring semiring);
+
+/* Append n facts to input relation `relation`.
+ *   columns    : `arity` pointers, each to n int32 values (host or device memory,
+ *                detected per pointer); may be NULL when arity == 0
+ *   sample_ids : n int32 in [0, batch_size) (host or device); NULL for a shared relation
+ *   probs      : n float in [0,1] (host or device); NULL = 1.0; ignored under UNIT
+ * Fact ids are dense in push order: [*first_fact_id, *first_fact_id + n).
+ * The data is copied before return; the caller keeps ownership of its buffers.
+ * Duplicate tuples within a sample are ⊕-merged at run (reading 16).
+ * Errors: SCHEMA (unknown input relation, missing sample ids), RANGE (prob NaN
+ * or outside [0,1]; sample id out of range), STATE (before program_load). */
+lobster_status lobster_facts_push(lobster_ctx* ctx, const char* relation, int64_t n,
+                                  const int32_t* const* columns, const int32_t* sample_ids,
+                                  const float* probs, int64_t* first_fact_id);
+
+typedef struct {
+  int32_t strata, rounds_total;   /* strata evaluated; rounds summed over strata           */
+  int64_t tuples_derived;         /* Σ final IDB tuples                                   */
+  int64_t candidates;             /* Σ join outputs (|C|) over all rounds                 */
+  double ms_total, ms_join, ms_sort, ms_reduce, ms_merge, ms_grad, ms_comm;
+  int64_t bytes_algorithmic;      /* SURVEY §8(d) B_alg summed over rounds               */
+} lobster_run_stats;
+
+/* Evaluate every stratum to fixpoint (termination: no new tuple and no tag whose
+ * fp32 bits changed, reading 1), then — under DIFF_MAX_MULT_PROB — walk the
+ * witnesses of every `output` relation and build its per-tuple gradients.
+ * Blocking on the context stream.  stats may be NULL.
+ * Errors: STATE (no program), OOM, ITER_CAP (state of the last round is
+ * readable), RANGE (packed key > 64 bits or witness > 32 bits), CUDA. */
+lobster_status lobster_run(lobster_ctx* ctx, lobster_run_stats* stats);
+
+typedef struct {
+  int64_t n;                      /* rows                                                  */
+  int32_t arity;
+  int32_t on_device;              /* 1: pointers are device pointers                        */
+  const int32_t* sample_ids;      /* n (sample of each row)                                 */
+  const int32_t* const* columns;  /* arity pointers to n int32; rows sorted by (sample, cols) */
+  const float* probs;             /* n; NULL under UNIT; add-mult is unclamped      */
+  const int64_t* sample_offsets;  /* batch_size+1: rows of sample s are [off[s], off[s+1])  */
+  const int64_t* grad_offsets;    /* n+1, DIFF_MAX_MULT_PROB output relations only, else NULL */
+  const int64_t* grad_fact_ids;   /* grad_offsets[n] ids, ascending within each row         */
+  const float* grad_values;       /* ∂probs[row] / ∂p(fact), fp64-accumulated, rounded to fp32 */
+} lobster_output;
+
+/* Views of relation `relation` (any IDB relation; gradients only for relations
+ * marked `output`).  where: 0 = host copies, 1 = device pointers.  Views are
+ * owned by ctx and valid until the next push / run / program_load / destroy.
+ * Errors: INVALID_ARG (unknown relation or bad `where`), STATE (no successful run). */
+lobster_status lobster_output_get(lobster_ctx* ctx, const char* relation, int32_t where, lobster_output* out);
+
+/* Optional: dense input-fact gradient of Σ_rows upstream[row] · probs[row] for an
+ * `output` relation: grad_facts[f] = Σ_rows upstream[row] · ∂probs[row]/∂p_f,
+ * a deterministic segmented sum (no atomics).  upstream: n floats, grad_facts:
+ * (number of pushed facts) floats; both device pointers.  Errors: STATE,
+ * INVALID_ARG (not an output relation / not DIFF_MAX_MULT_PROB). */
+lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation,
+                                       const float* upstream, float* grad_facts);
+
+/* Number of facts pushed into the current database (size of grad_facts). */
+int64_t lobster_num_facts(const lobster_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOBSTER_H */

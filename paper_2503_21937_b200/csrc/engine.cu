@@ -1,0 +1,1416 @@
+// engine.cu — host driver of the semi-naive fixpoint (B1-B4 of SURVEY §1.2):
+// relation store, ingest, planner, per-round loop, witness walk, outputs, and
+// the extern "C" boundary of include/lobster.h.
+//
+// Per stratum (Alg. 1; §3.4):
+//   round 1 ("seed", reading 3): rules whose body atoms are all external
+//   round r>1: for each rule with local atoms and each local position j:
+//              B_1^new ⋈ .. ⋈ Δ_j ⋈ .. ⋈ B_k^old      (Fig. 10 Join)
+//   every round: C -> radix sort -> segmented ⊕ = U -> diff against F ->
+//              Δ' (increments), F ⊕= changed, F ∪= new    (Fig. 10 Stratum)
+//   stop when Σ|Δ'| = 0 (reading 1).
+// Device work is all in the kernels of k_*.cu; this file only plans and
+// launches.  There is no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "devmem.hpp"
+#include "kernels.cuh"
+#include "lobster.h"
+#include "program.hpp"
+
+namespace lob {
+
+static int bits_for(uint64_t range) { return range == 0 ? 0 : 64 - __builtin_clzll(range); }
+
+constexpr int MAXARITY = 8;
+
+struct Layout {
+  bool has_sample = false;
+  int sbits = 0, sshift = 0;
+  std::vector<int> bits, shift;
+  std::vector<int32_t> mins;
+  int total = 0;
+};
+
+struct Staged {
+  DBuf<int32_t> cols[MAXARITY];
+  DBuf<int32_t> sid;
+  DBuf<float> p;
+  DBuf<int32_t> fid;
+  int64_t n = 0;
+};
+
+struct RelState {
+  Layout L;
+  DBuf<uint64_t> key, key2;
+  DBuf<float> p, p2;
+  DBuf<uint32_t> w, w2;
+  DBuf<int32_t> fid;
+  int64_t n = 0;
+  DBuf<uint64_t> dkey;
+  DBuf<float> dp;
+  DBuf<uint32_t> dw;
+  int64_t nd = 0;
+  DBuf<uint64_t> okey;
+  DBuf<float> op;
+  DBuf<uint32_t> ow;
+  int64_t no = 0;
+  bool need_old = false;
+  DBuf<uint64_t> ckey, ckey2, cv64, cv64b;
+  DBuf<uint32_t> cv32, cv32b;
+  int64_t nc = 0;
+  Staged in;
+  // outputs
+  bool out_dev_ready = false, out_host_ready = false;
+  DBuf<int32_t> o_sid, o_cols;
+  DBuf<int64_t> o_soff;
+  std::vector<int32_t> h_sid, h_cols;
+  std::vector<float> h_p;
+  std::vector<int64_t> h_soff, h_goff, h_gfid;
+  std::vector<float> h_gval;
+  std::vector<const int32_t*> col_ptrs;
+  bool has_grad = false;
+  DBuf<int64_t> goff, gfid;
+  DBuf<float> gval;
+  int64_t ng = 0;
+
+  void bind(cudaStream_t st) {
+    for (auto* b : {&key, &key2, &dkey, &okey, &ckey, &ckey2, &cv64, &cv64b}) b->bind(st);
+    for (auto* b : {&p, &p2, &dp, &op, &gval}) b->bind(st);
+    for (auto* b : {&w, &w2, &dw, &ow, &cv32, &cv32b}) b->bind(st);
+    for (auto* b : {&fid, &o_sid, &o_cols}) b->bind(st);
+    for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
+    for (auto& c : in.cols) c.bind(st);
+    in.sid.bind(st);
+    in.p.bind(st);
+    in.fid.bind(st);
+  }
+};
+
+// Sorted index over one relation version: key = [sample][order...], prefix =
+// sample + the first nbound columns of `order`.
+struct Index {
+  const uint64_t* key = nullptr;
+  const float* p = nullptr;
+  int64_t n = 0;
+  DBuf<uint64_t> own_key, tmp_key;
+  DBuf<float> own_p, tmp_p;
+  DBuf<int64_t> off;
+  const int64_t* offp = nullptr;
+  int64_t nprefix = 0;
+  int free_bits = 0, prefix_bits = 0;
+  bool has_sample = false;
+  int sshift = 0, sbits = 0;
+  std::vector<int> col_shift, col_bits;
+};
+
+struct Table {  // probe side of a join step
+  const uint64_t* key = nullptr;
+  int64_t n = 0;
+  std::vector<const float*> tags;
+  std::vector<int> tag_atom;
+  bool has_sample = true;
+  int sshift = 0, sbits = 0;
+  std::vector<int> vshift, vbits;  // per var id, -1 unbound
+};
+
+enum Version { V_EXT = 0, V_NEW = 1, V_OLD = 2, V_DELTA = 3 };
+
+struct Ctx {
+  lobster_options opt{};
+  cudaStream_t st = nullptr;
+  std::string err;
+  bool sticky = false;
+  bool loaded = false, ran = false, dirty = false;
+  int semi = 0;
+  Program prog;
+  std::vector<std::unique_ptr<RelState>> rels;
+  int64_t next_fact = 0;
+  Arena arena;
+  int64_t* hbuf = nullptr;  // pinned
+  std::map<std::pair<int, std::vector<int>>, std::unique_ptr<Index>> static_idx;
+  std::vector<int64_t> class_min, class_max;
+  std::vector<int> rule_bits;
+  std::vector<std::vector<int>> wshift, wbits;  // per rule, per nonhead var
+  DBuf<float> fact_p;
+  lobster_run_stats stats{};
+  int max_iters = 100000;
+  int64_t num_facts_db = 0;
+  // timing
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  size_t ev_used = 0;
+  std::vector<cudaEvent_t> ev_pool;
+
+  // ------------------------------------------------------------------ util
+  void sync() { cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"); }
+  void kcheck(const char* what) { cuda_check(cudaGetLastError(), what); }
+  template <typename T>
+  T read_dev(const T* d) {
+    cuda_check(cudaMemcpyAsync(hbuf, d, sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
+    sync();
+    T v;
+    std::memcpy(&v, hbuf, sizeof(T));
+    return v;
+  }
+  cudaEvent_t get_event() {
+    if (ev_used < ev_pool.size()) return ev_pool[ev_used++];
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    ev_pool.push_back(e);
+    ev_used++;
+    return e;
+  }
+  struct Phase {
+    Ctx* c;
+    int id;
+    cudaEvent_t a;
+    Phase(Ctx* cc, int i) : c(cc), id(i) {
+      a = c->get_event();
+      cudaEventRecord(a, c->st);
+    }
+    ~Phase() {
+      cudaEvent_t b = c->get_event();
+      cudaEventRecord(b, c->st);
+      c->ev.push_back({id, {a, b}});
+    }
+  };
+
+  ~Ctx() {
+    for (auto& r : rels) r.reset();
+    static_idx.clear();
+    arena.free_all();
+    fact_p.release();
+    if (st) cudaStreamSynchronize(st);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (hbuf) cudaFreeHost(hbuf);
+  }
+
+  // --------------------------------------------------------------- create
+  void create(const lobster_options* o) {
+    if (o) opt = *o;
+    if (opt.batch_size < 1) opt.batch_size = 1;
+    max_iters = opt.max_iters > 0 ? opt.max_iters : 100000;
+    int ndev = 0;
+    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (opt.device < 0 || opt.device >= ndev) throw Failure(LOBSTER_E_CUDA, "no such CUDA device");
+    cuda_check(cudaSetDevice(opt.device), "cudaSetDevice");
+    st = reinterpret_cast<cudaStream_t>(opt.cuda_stream);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, opt.device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cuda_check(cudaMallocHost(&hbuf, 64), "cudaMallocHost");
+    arena.bind(st);
+    fact_p.bind(st);
+    if (opt.arena_bytes > 0) arena.reserve_initial((size_t)opt.arena_bytes);
+  }
+
+  // ---------------------------------------------------------- program load
+  void load(const char* text, int semiring) {
+    if (loaded) throw Failure(LOBSTER_E_STATE, "program already loaded");
+    if (semiring < 0 || semiring > 3) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
+    if (!text) throw Failure(LOBSTER_E_INVALID_ARG, "program text is NULL");
+    prog = parse_program(text);
+    semi = semiring;
+    for (auto& r : prog.rels)
+      if (r.arity > MAXARITY) throw Failure(LOBSTER_E_PARSE, "relation " + r.name + ": arity above 8 is unsupported");
+    for (auto& R : prog.rules) {
+      if ((int)R.body.size() > MAXT) throw Failure(LOBSTER_E_PARSE, "rule with more than 6 body atoms is unsupported");
+      if (R.var_names.size() > 9) throw Failure(LOBSTER_E_PARSE, "rule with more than 9 variables is unsupported");
+    }
+    rels.clear();
+    for (size_t i = 0; i < prog.rels.size(); ++i) {
+      rels.emplace_back(new RelState());
+      rels.back()->bind(st);
+    }
+    // relations that need an "old" version: local atoms placed after another
+    // local atom of the same stratum in some rule body (B_k^old)
+    for (auto& R : prog.rules) {
+      int s = prog.rels[R.head_rel].stratum;
+      int seen = 0;
+      for (auto& a : R.body) {
+        if (!prog.rels[a.rel].input && prog.rels[a.rel].stratum == s) {
+          if (seen) rels[a.rel]->need_old = true;
+          seen++;
+        }
+      }
+    }
+    rule_bits.assign(prog.rels.size(), 0);
+    for (size_t r = 0; r < prog.rels.size(); ++r)
+      rule_bits[r] = prog.rels[r].nrules > 1 ? bits_for((uint64_t)prog.rels[r].nrules - 1) : 0;
+    loaded = true;
+  }
+
+  // ------------------------------------------------------------ facts push
+  void new_database() {
+    for (auto& r : rels) {
+      r->in.n = 0;
+      r->n = r->nd = r->no = r->nc = 0;
+      r->out_dev_ready = r->out_host_ready = false;
+      r->has_grad = false;
+    }
+    static_idx.clear();
+    next_fact = 0;
+    ran = false;
+  }
+
+  void push(const char* relname, int64_t n, const int32_t* const* columns, const int32_t* sample_ids,
+            const float* probs, int64_t* first) {
+    if (!loaded) throw Failure(LOBSTER_E_STATE, "facts_push before program_load");
+    if (!relname) throw Failure(LOBSTER_E_INVALID_ARG, "relation name is NULL");
+    auto it = prog.rel_id.find(relname);
+    if (it == prog.rel_id.end() || !prog.rels[it->second].input)
+      throw Failure(LOBSTER_E_SCHEMA, std::string("unknown input relation ") + relname);
+    if (n < 0) throw Failure(LOBSTER_E_INVALID_ARG, "negative row count");
+    const Relation& R = prog.rels[it->second];
+    if (R.arity > 0 && n > 0 && !columns) throw Failure(LOBSTER_E_INVALID_ARG, "columns is NULL");
+    if (!R.shared && n > 0 && !sample_ids)
+      throw Failure(LOBSTER_E_SCHEMA, std::string("relation ") + relname + " is batched: sample ids required");
+    if (ran) new_database();
+    RelState& S = *rels[it->second];
+    const int64_t base = S.in.n;
+    if (next_fact + n > INT32_MAX) throw Failure(LOBSTER_E_RANGE, "more than 2^31 facts");
+    for (int c = 0; c < R.arity; ++c) {
+      if (!columns[c] && n > 0) throw Failure(LOBSTER_E_INVALID_ARG, "column pointer is NULL");
+      S.in.cols[c].reserve(base + n, base);
+    }
+    S.in.sid.reserve(base + n, base);
+    S.in.p.reserve(base + n, base);
+    S.in.fid.reserve(base + n, base);
+    if (n > 0) {
+      for (int c = 0; c < R.arity; ++c)
+        cuda_check(cudaMemcpyAsync(S.in.cols[c].ptr() + base, columns[c], n * sizeof(int32_t), cudaMemcpyDefault, st),
+                   "push columns");
+      if (!R.shared)
+        cuda_check(cudaMemcpyAsync(S.in.sid.ptr() + base, sample_ids, n * sizeof(int32_t), cudaMemcpyDefault, st),
+                   "push sample ids");
+      if (probs && semi != S_UNIT)
+        cuda_check(cudaMemcpyAsync(S.in.p.ptr() + base, probs, n * sizeof(float), cudaMemcpyDefault, st), "push probs");
+      else
+        launch_fill_f32(S.in.p.ptr() + base, n, 1.0f, st);
+      launch_iota_i32(S.in.fid.ptr() + base, n, (int32_t)next_fact, st);
+      // validation (reading: S:46 range errors)
+      uint32_t* flags = reinterpret_cast<uint32_t*>(hbuf);
+      uint32_t* dflag = arena.get<uint32_t>(1);
+      cuda_check(cudaMemsetAsync(dflag, 0, 4, st), "memset");
+      launch_validate((probs && semi != S_UNIT) ? S.in.p.ptr() + base : nullptr,
+                      R.shared ? nullptr : S.in.sid.ptr() + base, n, opt.batch_size, dflag, st);
+      kcheck("validate");
+      cuda_check(cudaMemcpyAsync(flags, dflag, 4, cudaMemcpyDeviceToHost, st), "D2H");
+      sync();
+      arena.reset();
+      if (*flags & 1u) throw Failure(LOBSTER_E_RANGE, std::string("relation ") + relname + ": probability NaN or outside [0,1]");
+      if (*flags & 2u) throw Failure(LOBSTER_E_RANGE, std::string("relation ") + relname + ": sample id out of range");
+    }
+    S.in.n = base + n;
+    *first = next_fact;
+    next_fact += n;
+    dirty = true;
+  }
+
+  // ---------------------------------------------------------------- layout
+  Layout make_layout(int r) {
+    const Relation& R = prog.rels[r];
+    Layout L;
+    L.has_sample = !R.shared;
+    L.sbits = L.has_sample ? bits_for((uint64_t)opt.batch_size - 1) : 0;
+    int pos = 0;
+    L.bits.assign(R.arity, 0);
+    L.shift.assign(R.arity, 0);
+    L.mins.assign(R.arity, 0);
+    for (int c = R.arity - 1; c >= 0; --c) {
+      int cl = R.col_class[c];
+      L.bits[c] = bits_for((uint64_t)(class_max[cl] - class_min[cl]));
+      L.mins[c] = (int32_t)class_min[cl];
+      L.shift[c] = pos;
+      pos += L.bits[c];
+    }
+    L.sshift = pos;
+    L.total = pos + L.sbits;
+    if (L.total > 63)
+      throw Failure(LOBSTER_E_RANGE, "packed key of relation " + R.name + " needs " + std::to_string(L.total) +
+                                         " bits (> 63)");
+    return L;
+  }
+
+  // ----------------------------------------------------------------- ingest
+  void ingest() {
+    const int nr = (int)prog.rels.size();
+    // A0: per-column min/max of every input relation -> domain classes
+    std::vector<std::pair<int, int>> cols;
+    for (int r = 0; r < nr; ++r)
+      if (prog.rels[r].input)
+        for (int c = 0; c < prog.rels[r].arity; ++c) cols.push_back({r, c});
+    std::vector<int32_t> mm(cols.size() * 2);
+    int32_t* dmm = arena.get<int32_t>((int64_t)mm.size() + 2);
+    for (size_t i = 0; i < cols.size(); ++i) {
+      mm[2 * i] = INT32_MAX;
+      mm[2 * i + 1] = INT32_MIN;
+    }
+    if (!mm.empty()) {
+      cuda_check(cudaMemcpyAsync(dmm, mm.data(), mm.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+      for (size_t i = 0; i < cols.size(); ++i) {
+        RelState& S = *rels[cols[i].first];
+        launch_minmax(S.in.cols[cols[i].second].ptr(), S.in.n, dmm + 2 * i, st);
+      }
+      kcheck("minmax");
+      cuda_check(cudaMemcpyAsync(mm.data(), dmm, mm.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      sync();
+    }
+    class_min.assign(prog.nclasses, INT64_MAX);
+    class_max.assign(prog.nclasses, INT64_MIN);
+    for (size_t i = 0; i < cols.size(); ++i) {
+      if (rels[cols[i].first]->in.n == 0) continue;
+      int cl = prog.rels[cols[i].first].col_class[cols[i].second];
+      class_min[cl] = std::min<int64_t>(class_min[cl], mm[2 * i]);
+      class_max[cl] = std::max<int64_t>(class_max[cl], mm[2 * i + 1]);
+    }
+    for (int cl = 0; cl < prog.nclasses; ++cl) {
+      if (prog.class_has_const[cl]) {
+        class_min[cl] = std::min(class_min[cl], prog.class_cmin[cl]);
+        class_max[cl] = std::max(class_max[cl], prog.class_cmax[cl]);
+      }
+      if (class_min[cl] > class_max[cl]) class_min[cl] = class_max[cl] = 0;
+    }
+    for (int r = 0; r < nr; ++r) rels[r]->L = make_layout(r);
+    // witness layouts (diff-max-mult): rule index in the top bits, non-head
+    // variables below, first variable most significant (tie order, reading 8b)
+    wshift.assign(prog.rules.size(), {});
+    wbits.assign(prog.rules.size(), {});
+    for (size_t ri = 0; ri < prog.rules.size(); ++ri) {
+      const Rule& R = prog.rules[ri];
+      int tot = 0;
+      for (int v : R.nonhead) {
+        int cl = R.var_class[v];
+        int b = bits_for((uint64_t)(class_max[cl] - class_min[cl]));
+        wbits[ri].push_back(b);
+        tot += b;
+      }
+      if (semi == S_MAXMULT && tot > 32 - rule_bits[R.head_rel])
+        throw Failure(LOBSTER_E_RANGE, "witness of a rule for " + prog.rels[R.head_rel].name + " needs " +
+                                           std::to_string(tot + rule_bits[R.head_rel]) + " bits (> 32)");
+      int pos = tot;
+      for (size_t i = 0; i < R.nonhead.size(); ++i) {
+        pos -= wbits[ri][i];
+        wshift[ri].push_back(pos);
+      }
+    }
+    // pack + sort + ⊕-merge duplicates of every input relation (A0)
+    for (int r = 0; r < nr; ++r) {
+      if (!prog.rels[r].input) continue;
+      RelState& S = *rels[r];
+      const int64_t n = S.in.n;
+      S.n = 0;
+      if (n == 0) continue;
+      PackPlan pp{};
+      pp.ncols = prog.rels[r].arity;
+      for (int c = 0; c < pp.ncols; ++c) {
+        pp.col[c] = S.in.cols[c].ptr();
+        pp.min[c] = S.L.mins[c];
+        pp.shift[c] = (uint8_t)S.L.shift[c];
+      }
+      pp.sample = S.L.has_sample ? S.in.sid.ptr() : nullptr;
+      pp.sshift = (uint8_t)S.L.sshift;
+      uint64_t* k0 = arena.get<uint64_t>(n);
+      uint64_t* k1 = arena.get<uint64_t>(n);
+      uint32_t* r0 = arena.get<uint32_t>(n);
+      uint32_t* r1 = arena.get<uint32_t>(n);
+      void* stmp = arena.alloc(sort_tmp_bytes(n));
+      launch_pack(pp, n, k0, r0, st);
+      int which = radix_sort<uint32_t>(k0, r0, k1, r1, n, S.L.total, stmp, st);
+      uint64_t* ks = which ? k1 : k0;
+      uint32_t* rs = which ? r1 : r0;
+      float* ps = arena.get<float>(n);
+      int32_t* fs = arena.get<int32_t>(n);
+      launch_gather_f32(S.in.p.ptr(), rs, ps, n, st);
+      launch_gather_i32(S.in.fid.ptr(), rs, fs, n, st);
+      uint32_t* fl = arena.get<uint32_t>(n);
+      uint32_t* pos = arena.get<uint32_t>(n);
+      uint32_t* tot = arena.get<uint32_t>(1);
+      launch_heads(ks, n, fl, st);
+      exclusive_scan<uint32_t>(fl, pos, n, tot, arena.alloc(scan_tmp_bytes<uint32_t>(n)), st);
+      kcheck("ingest");
+      const int64_t nu = read_dev(tot);
+      S.key.reserve(nu);
+      S.p.reserve(nu);
+      S.fid.reserve(nu);
+      launch_edb_reduce(ks, ps, fs, pos, n, semi, S.key.ptr(), S.p.ptr(), S.fid.ptr(), st);
+      kcheck("edb reduce");
+      S.n = nu;
+      arena.reset();
+    }
+    num_facts_db = next_fact;
+    if (semi == S_MAXMULT) {
+      fact_p.reserve(next_fact + 1);
+      for (int r = 0; r < nr; ++r) {
+        if (!prog.rels[r].input || rels[r]->in.n == 0) continue;
+        RelState& S = *rels[r];
+        // facts of one relation carry ids in push order: scatter p by id
+        scatter_fact_p(S.in.fid.ptr(), S.in.p.ptr(), S.in.n);
+      }
+    }
+  }
+
+  void scatter_fact_p(const int32_t* fid, const float* p, int64_t n);
+
+  // ------------------------------------------------------------------ index
+  // Build (or alias) an index of relation r's version (key, p, n) with column
+  // order `order`, prefix = sample + first nbound columns.
+  void layout_index(Index& ix, const Layout& L, const std::vector<int>& order, int nbound) {
+    ix.has_sample = L.has_sample;
+    ix.sbits = L.sbits;
+    ix.col_shift.assign(L.bits.size(), 0);
+    ix.col_bits = L.bits;
+    int pos = 0;
+    for (int i = (int)order.size() - 1; i >= 0; --i) {
+      ix.col_shift[order[i]] = pos;
+      pos += L.bits[order[i]];
+      if (i == nbound) ix.free_bits = pos;
+    }
+    if (nbound == (int)order.size()) ix.free_bits = 0;
+    ix.sshift = pos;
+    ix.prefix_bits = pos - ix.free_bits + ix.sbits;
+  }
+
+  static bool is_natural(const std::vector<int>& order) {
+    for (size_t i = 0; i < order.size(); ++i)
+      if (order[i] != (int)i) return false;
+    return true;
+  }
+
+  // build into ix from a version's data; persistent=true uses ix.own_* buffers
+  void build_index(Index& ix, const Layout& L, const std::vector<int>& order, int nbound, const uint64_t* key,
+                   const float* p, int64_t n, bool persistent, bool want_offsets) {
+    layout_index(ix, L, order, nbound);
+    ix.n = n;
+    if (is_natural(order)) {
+      ix.key = key;
+      ix.p = p;
+    } else {
+      std::vector<Move> mv;
+      if (L.has_sample && L.sbits) mv.push_back({0, (uint8_t)L.sshift, (uint8_t)L.sbits, (uint8_t)ix.sshift});
+      for (size_t c = 0; c < L.bits.size(); ++c)
+        if (L.bits[c]) mv.push_back({0, (uint8_t)L.shift[c], (uint8_t)L.bits[c], (uint8_t)ix.col_shift[c]});
+      uint64_t *k0, *k1;
+      float *p0 = nullptr, *p1 = nullptr;
+      if (persistent) {
+        ix.own_key.bind(st); ix.tmp_key.bind(st); ix.own_p.bind(st); ix.tmp_p.bind(st);
+        ix.own_key.reserve(n); ix.tmp_key.reserve(n);
+        k0 = ix.own_key.ptr(); k1 = ix.tmp_key.ptr();
+        if (p) { ix.own_p.reserve(n); ix.tmp_p.reserve(n); p0 = ix.own_p.ptr(); p1 = ix.tmp_p.ptr(); }
+      } else {
+        k0 = arena.get<uint64_t>(n); k1 = arena.get<uint64_t>(n);
+        if (p) { p0 = arena.get<float>(n); p1 = arena.get<float>(n); }
+      }
+      launch_rekey(key, n, mv.data(), (int)mv.size(), k0, st);
+      if (p) cuda_check(cudaMemcpyAsync(p0, p, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "index p");
+      void* stmp = arena.alloc(sort_tmp_bytes(n));
+      int which;
+      if (p) which = radix_sort<uint32_t>(k0, (uint32_t*)p0, k1, (uint32_t*)p1, n, L.total, stmp, st);
+      else which = radix_sort<void>(k0, nullptr, k1, nullptr, n, L.total, stmp, st);
+      ix.key = which ? k1 : k0;
+      ix.p = p ? (which ? p1 : p0) : nullptr;
+      kcheck("index build");
+    }
+    ix.offp = nullptr;
+    if (want_offsets && ix.prefix_bits <= 26 && ((int64_t)1 << ix.prefix_bits) <= 4 * n + 4096) {
+      ix.nprefix = (int64_t)1 << ix.prefix_bits;
+      int64_t* off;
+      if (persistent) {
+        ix.off.bind(st);
+        ix.off.reserve(ix.nprefix + 1);
+        off = ix.off.ptr();
+      } else {
+        off = arena.get<int64_t>(ix.nprefix + 1);
+      }
+      launch_build_offsets(ix.key, n, ix.free_bits, ix.nprefix, off, st);
+      kcheck("offsets");
+      ix.offp = off;
+    }
+  }
+
+  Index* static_index(int r, const std::vector<int>& order, int nbound) {
+    auto key = std::make_pair(r, order);
+    key.second.push_back(1000 + nbound);
+    auto it = static_idx.find(key);
+    if (it != static_idx.end()) return it->second.get();
+    std::unique_ptr<Index> ix(new Index());
+    RelState& S = *rels[r];
+    build_index(*ix, S.L, order, nbound, S.key.ptr(), semi == S_UNIT ? nullptr : S.p.ptr(), S.n, true, true);
+    Index* raw = ix.get();
+    static_idx[key] = std::move(ix);
+    return raw;
+  }
+
+  // ------------------------------------------------------------ rule eval
+  struct VerData {
+    const uint64_t* key;
+    const float* p;
+    int64_t n;
+  };
+  VerData version_data(int rel, Version v) {
+    RelState& S = *rels[rel];
+    const bool tag = semi != S_UNIT;
+    switch (v) {
+      case V_DELTA: return {S.dkey.ptr(), tag ? S.dp.ptr() : nullptr, S.nd};
+      case V_OLD: return {S.okey.ptr(), tag ? S.op.ptr() : nullptr, S.no};
+      default: return {S.key.ptr(), tag ? S.p.ptr() : nullptr, S.n};
+    }
+  }
+
+  int32_t class_base(int cl) const { return (int32_t)class_min[cl]; }
+
+  // Evaluate one rule (variant) and append its candidates to the head's buffer.
+  void eval_rule(const Rule& R, const std::vector<Version>& ver, int start) {
+    const int na = (int)R.body.size();
+    const int nv = (int)R.var_names.size();
+    RelState& H = *rels[R.head_rel];
+    // join order: start atom, then most bound columns, natural prefix, size
+    std::vector<int> order{start};
+    std::vector<char> bound(nv, 0), used(na, 0);
+    used[start] = 1;
+    for (auto& t : R.body[start].args) if (t.is_var()) bound[t.var] = 1;
+    for (int s = 1; s < na; ++s) {
+      int best = -1;
+      std::tuple<int, int, int64_t, int> bkey{};
+      for (int a = 0; a < na; ++a) {
+        if (used[a]) continue;
+        int nb = 0;
+        std::vector<char> isb;
+        for (auto& t : R.body[a].args) {
+          bool b = !t.is_var() || bound[t.var];
+          isb.push_back(b);
+          nb += b;
+        }
+        int natural = 1;
+        for (int c = 0; c < (int)isb.size(); ++c) if ((c < nb) != (bool)isb[c]) natural = 0;
+        int64_t sz = version_data(R.body[a].rel, ver[a]).n;
+        auto k = std::make_tuple(nb, natural, -sz, -a);
+        if (best < 0 || k > bkey) { best = a; bkey = k; }
+      }
+      order.push_back(best);
+      used[best] = 1;
+      for (auto& t : R.body[best].args) if (t.is_var()) bound[t.var] = 1;
+    }
+    // probe table = start atom
+    Table T;
+    const BodyAtom& A0 = R.body[start];
+    const Layout& L0 = rels[A0.rel]->L;
+    VerData d0 = version_data(A0.rel, ver[start]);
+    if (d0.n == 0) return;
+    T.key = d0.key;
+    T.n = d0.n;
+    if (semi != S_UNIT) { T.tags.push_back(d0.p); T.tag_atom.push_back(start); }
+    T.has_sample = L0.has_sample;
+    T.sshift = L0.sshift;
+    T.sbits = L0.sbits;
+    T.vshift.assign(nv, -1);
+    T.vbits.assign(nv, 0);
+    std::vector<Cmp> pending_start;  // constants / repeated vars of the start atom
+    for (int c = 0; c < (int)A0.args.size(); ++c) {
+      const Term& t = A0.args[c];
+      Operand f{0, (uint8_t)L0.shift[c], (uint8_t)L0.bits[c], L0.mins[c]};
+      if (!t.is_var()) {
+        Operand k{2, 0, 0, t.cst};
+        pending_start.push_back({f, k, 0});
+      } else if (T.vshift[t.var] >= 0) {
+        Operand g{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
+        pending_start.push_back({f, g, 0});
+      } else {
+        T.vshift[t.var] = L0.shift[c];
+        T.vbits[t.var] = L0.bits[c];
+      }
+    }
+    if (!T.has_sample) throw Failure(LOBSTER_E_STATE, "internal: join must start from a batched atom");
+    std::vector<char> cmp_done(R.cmps.size(), 0);
+    auto var_bound = [&](const Term& t, const std::vector<int>& vs) { return !t.is_var() || vs[t.var] >= 0; };
+
+    if (na == 1) {  // projection
+      ProjectPlan pp{};
+      pp.key = T.key;
+      pp.tag = semi != S_UNIT ? T.tags[0] : nullptr;
+      pp.n = T.n;
+      for (auto& c : pending_start) pp.cmp[pp.ncmp++] = c;
+      for (size_t i = 0; i < R.cmps.size(); ++i) {
+        const Compare& cm = R.cmps[i];
+        auto op = [&](const Term& t) -> Operand {
+          if (!t.is_var()) return Operand{2, 0, 0, t.cst};
+          return Operand{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
+        };
+        if (pp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
+        pp.cmp[pp.ncmp++] = Cmp{op(cm.a), op(cm.b), (int8_t)cm.neq};
+      }
+      head_moves(R, H, T, nullptr, pp.om, pp.nom, pp.cout);
+      pp.semi = semi;
+      witness_moves(R, T, nullptr, pp.wm, pp.nwm, pp.wconst);
+      reserve_candidates(H, H.nc + T.n);
+      pp.okey = H.ckey.ptr() + H.nc;
+      pp.oval32 = H.cv32.ptr() ? H.cv32.ptr() + H.nc : nullptr;
+      pp.oval64 = H.cv64.ptr() ? H.cv64.ptr() + H.nc : nullptr;
+      launch_project(pp, st);
+      kcheck("project");
+      H.nc += T.n;
+      stats.candidates += T.n;
+      return;
+    }
+
+    for (int s = 1; s < na; ++s) {
+      const int ai = order[s];
+      const BodyAtom& A = R.body[ai];
+      const Relation& AR = prog.rels[A.rel];
+      RelState& AS = *rels[A.rel];
+      const Layout& L = AS.L;
+      // bound / free columns
+      std::vector<int> bcols, fcols;
+      for (int c = 0; c < (int)A.args.size(); ++c) {
+        if (var_bound(A.args[c], T.vshift)) bcols.push_back(c); else fcols.push_back(c);
+      }
+      std::vector<int> iorder = bcols;
+      iorder.insert(iorder.end(), fcols.begin(), fcols.end());
+      const int nbound = (int)bcols.size();
+      Index* ix;
+      Index local_ix;
+      if (ver[ai] == V_EXT) {
+        ix = static_index(A.rel, iorder, nbound);
+      } else {
+        VerData vd = version_data(A.rel, ver[ai]);
+        build_index(local_ix, L, iorder, nbound, vd.key, vd.p, vd.n, false, false);
+        ix = &local_ix;
+      }
+      if (ix->n == 0) return;
+      JoinPlan jp{};
+      jp.pkey = T.key;
+      jp.np = T.n;
+      jp.npt = (int)T.tags.size();
+      for (int k = 0; k < jp.npt; ++k) jp.ptag[k] = T.tags[k];
+      // prefix moves (probe -> prefix coordinates)
+      bool impossible = false;
+      if (L.has_sample && L.sbits)
+        jp.prem[jp.nprem++] = Move{0, (uint8_t)T.sshift, (uint8_t)T.sbits, (uint8_t)(ix->sshift - ix->free_bits)};
+      for (int c : bcols) {
+        const Term& t = A.args[c];
+        const int dsh = ix->col_shift[c] - ix->free_bits;
+        if (!t.is_var()) {
+          int64_t f = (int64_t)t.cst - L.mins[c];
+          if (f < 0 || f >= ((int64_t)1 << L.bits[c])) impossible = true;
+          else jp.cprefix |= (uint64_t)f << dsh;
+        } else if (L.bits[c]) {
+          jp.prem[jp.nprem++] = Move{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], (uint8_t)dsh};
+        }
+      }
+      if (impossible) return;
+      jp.bkey = ix->key;
+      jp.btag = semi != S_UNIT ? ix->p : nullptr;
+      jp.nb = ix->n;
+      jp.boff = ix->offp;
+      jp.nprefix = ix->nprefix;
+      jp.free_bits = ix->free_bits;
+      // new variables from free columns; repeated free vars -> equality
+      std::vector<int> nshift(nv, -1), nbits(nv, 0);  // build-side fields of new vars
+      for (int c : fcols) {
+        const Term& t = A.args[c];
+        if (nshift[t.var] >= 0) {
+          if (jp.nfeq >= 2) throw Failure(LOBSTER_E_PARSE, "too many repeated variables in one atom");
+          jp.feq[jp.nfeq++] = Move{1, (uint8_t)ix->col_shift[c], (uint8_t)L.bits[c], (uint8_t)nshift[t.var]};
+        } else {
+          nshift[t.var] = ix->col_shift[c];
+          nbits[t.var] = L.bits[c];
+        }
+      }
+      // comparisons whose variables are all bound after this step
+      auto operand = [&](const Term& t) -> Operand {
+        if (!t.is_var()) return Operand{2, 0, 0, t.cst};
+        if (T.vshift[t.var] >= 0)
+          return Operand{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
+        return Operand{1, (uint8_t)nshift[t.var], (uint8_t)nbits[t.var], class_base(R.var_class[t.var])};
+      };
+      auto avail = [&](const Term& t) { return !t.is_var() || T.vshift[t.var] >= 0 || nshift[t.var] >= 0; };
+      if (s == 1)
+        for (auto& c : pending_start) jp.cmp[jp.ncmp++] = c;
+      for (size_t i = 0; i < R.cmps.size(); ++i) {
+        if (cmp_done[i] || !avail(R.cmps[i].a) || !avail(R.cmps[i].b)) continue;
+        if (jp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
+        jp.cmp[jp.ncmp++] = Cmp{operand(R.cmps[i].a), operand(R.cmps[i].b), (int8_t)R.cmps[i].neq};
+        cmp_done[i] = 1;
+      }
+      jp.semi = semi;
+      const bool last = s == na - 1;
+      jp.final_step = last ? 1 : 0;
+      // count + scan (A3-A4)
+      int64_t* count = arena.get<int64_t>(T.n);
+      int64_t* start_ = arena.get<int64_t>(T.n);
+      int64_t* offs = arena.get<int64_t>(T.n);
+      int64_t* tot = arena.get<int64_t>(1);
+      {
+        Phase ph(this, 0);
+        launch_join_count(jp, count, start_, st);
+        exclusive_scan<int64_t>(count, offs, T.n, tot, arena.alloc(scan_tmp_bytes<int64_t>(T.n)), st);
+        kcheck("join count");
+      }
+      const int64_t total = read_dev(tot);
+      if (total == 0) return;
+      Table N;  // next probe table (intermediate)
+      if (last) {
+        Table view = T;
+        head_moves(R, H, T, &nshift, jp.om, jp.nom, jp.cout, &nbits);
+        witness_moves(R, T, &nshift, jp.wm, jp.nwm, jp.wconst, &nbits);
+        // ⊗ order: T = [probe tags..., build tag]
+        if (semi != S_UNIT) {
+          jp.ntag = na;
+          for (int k = 0; k < na; ++k) {
+            int idx = -1;
+            for (size_t q = 0; q < T.tag_atom.size(); ++q) if (T.tag_atom[q] == k) idx = (int)q;
+            if (k == ai) idx = jp.npt;
+            jp.tag_order[k] = (int8_t)idx;
+          }
+        }
+        reserve_candidates(H, H.nc + total);
+        jp.okey = H.ckey.ptr() + H.nc;
+        jp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
+        jp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
+      } else {
+        // intermediate layout: sample + all bound vars (var id order)
+        N.has_sample = true;
+        N.vshift.assign(nv, -1);
+        N.vbits.assign(nv, 0);
+        int pos = 0;
+        for (int v = nv - 1; v >= 0; --v) {
+          int b = T.vshift[v] >= 0 ? T.vbits[v] : (nshift[v] >= 0 ? nbits[v] : -1);
+          if (b < 0) continue;
+          N.vshift[v] = pos;
+          N.vbits[v] = b;
+          pos += b;
+        }
+        N.sshift = pos;
+        N.sbits = T.sbits;
+        if (pos + N.sbits > 63) throw Failure(LOBSTER_E_RANGE, "intermediate join key wider than 63 bits");
+        if (T.sbits) jp.om[jp.nom++] = Move{0, (uint8_t)T.sshift, (uint8_t)T.sbits, (uint8_t)N.sshift};
+        for (int v = 0; v < nv; ++v) {
+          if (N.vshift[v] < 0 || N.vbits[v] == 0) continue;
+          if (jp.nom >= MAXM) throw Failure(LOBSTER_E_PARSE, "too many variables in one rule");
+          if (T.vshift[v] >= 0) jp.om[jp.nom++] = Move{0, (uint8_t)T.vshift[v], (uint8_t)T.vbits[v], (uint8_t)N.vshift[v]};
+          else jp.om[jp.nom++] = Move{1, (uint8_t)nshift[v], (uint8_t)nbits[v], (uint8_t)N.vshift[v]};
+        }
+        N.key = arena.get<uint64_t>(total);
+        N.n = total;
+        jp.okey = const_cast<uint64_t*>(N.key);
+        if (semi != S_UNIT) {
+          for (int k = 0; k <= jp.npt; ++k) {
+            float* t = arena.get<float>(total);
+            jp.otag[k] = t;
+            N.tags.push_back(t);
+          }
+          N.tag_atom = T.tag_atom;
+          N.tag_atom.push_back(ai);
+        }
+      }
+      {
+        Phase ph(this, 0);
+        launch_join_write(jp, offs, start_, total, st);
+        kcheck("join write");
+      }
+      if (last) {
+        H.nc += total;
+        stats.candidates += total;
+      } else {
+        T = N;
+      }
+      (void)AR;
+    }
+  }
+
+  // head key moves (src 0 = probe table T, src 1 = build fields given by nshift)
+  void head_moves(const Rule& R, RelState& H, const Table& T, const std::vector<int>* nshift, Move* om, int& nom,
+                  uint64_t& cout, const std::vector<int>* nbits = nullptr) {
+    const Layout& HL = H.L;
+    nom = 0;
+    cout = 0;
+    if (HL.has_sample && HL.sbits) om[nom++] = Move{0, (uint8_t)T.sshift, (uint8_t)T.sbits, (uint8_t)HL.sshift};
+    for (size_t c = 0; c < R.head.size(); ++c) {
+      const Term& t = R.head[c];
+      if (!t.is_var()) {
+        cout |= (uint64_t)((int64_t)t.cst - HL.mins[c]) << HL.shift[c];
+        continue;
+      }
+      if (HL.bits[c] == 0) continue;
+      if (nom >= MAXM) throw Failure(LOBSTER_E_PARSE, "head too wide");
+      if (T.vshift[t.var] >= 0) om[nom++] = Move{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], (uint8_t)HL.shift[c]};
+      else om[nom++] = Move{1, (uint8_t)(*nshift)[t.var], (uint8_t)(*nbits)[t.var], (uint8_t)HL.shift[c]};
+    }
+  }
+
+  void witness_moves(const Rule& R, const Table& T, const std::vector<int>* nshift, Move* wm, int& nwm,
+                     uint32_t& wconst, const std::vector<int>* nbits = nullptr) {
+    nwm = 0;
+    wconst = 0;
+    if (semi != S_MAXMULT) return;
+    const int rb = rule_bits[R.head_rel];
+    if (rb) wconst = (uint32_t)R.local_index << (32 - rb);
+    const size_t ri = (size_t)R.global_index;
+    for (size_t i = 0; i < R.nonhead.size(); ++i) {
+      const int v = R.nonhead[i];
+      if (wbits[ri][i] == 0) continue;
+      if (nwm >= MAXM) throw Failure(LOBSTER_E_PARSE, "too many non-head variables");
+      if (T.vshift[v] >= 0) wm[nwm++] = Move{0, (uint8_t)T.vshift[v], (uint8_t)T.vbits[v], (uint8_t)wshift[ri][i]};
+      else wm[nwm++] = Move{1, (uint8_t)(*nshift)[v], (uint8_t)(*nbits)[v], (uint8_t)wshift[ri][i]};
+    }
+  }
+
+  void reserve_candidates(RelState& H, int64_t n) {
+    H.ckey.reserve(n, H.nc);
+    if (semi == S_MAXMIN || semi == S_ADDMULT) H.cv32.reserve(n, H.nc);
+    if (semi == S_MAXMULT) H.cv64.reserve(n, H.nc);
+  }
+
+  // -------------------------------------------------- per-relation epilogue
+  // sort + segmented ⊕ (A6-A7), diff + apply + merge (A8); returns |Δ'|
+  int64_t settle(int r) {
+    RelState& S = *rels[r];
+    if (S.need_old) {  // OLD = F before this round's update (B^old of the next round)
+      S.okey.reserve(S.n);
+      if (S.n) cuda_check(cudaMemcpyAsync(S.okey.ptr(), S.key.ptr(), S.n * 8, cudaMemcpyDeviceToDevice, st), "old");
+      if (semi != S_UNIT) {
+        S.op.reserve(S.n);
+        if (S.n) cuda_check(cudaMemcpyAsync(S.op.ptr(), S.p.ptr(), S.n * 4, cudaMemcpyDeviceToDevice, st), "old");
+      }
+      S.no = S.n;
+    }
+    const int64_t nc = S.nc;
+    S.nc = 0;
+    if (nc == 0) { S.nd = 0; return 0; }
+    const int tb = S.L.total + 1;  // +1 bit: KEY_DEAD sorts after every key
+    S.ckey2.reserve(nc);
+    uint64_t* ks;
+    const void* vs;
+    {
+      Phase ph(this, 1);
+      void* stmp = arena.alloc(sort_tmp_bytes(nc));
+      int which;
+      if (semi == S_MAXMULT) {
+        S.cv64b.reserve(nc);
+        which = radix_sort<uint64_t>(S.ckey.ptr(), S.cv64.ptr(), S.ckey2.ptr(), S.cv64b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv64b.ptr() : S.cv64.ptr();
+      } else if (semi == S_UNIT) {
+        which = radix_sort<void>(S.ckey.ptr(), nullptr, S.ckey2.ptr(), nullptr, nc, tb, stmp, st);
+        vs = nullptr;
+      } else {
+        S.cv32b.reserve(nc);
+        which = radix_sort<uint32_t>(S.ckey.ptr(), S.cv32.ptr(), S.ckey2.ptr(), S.cv32b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv32b.ptr() : S.cv32.ptr();
+      }
+      ks = which ? S.ckey2.ptr() : S.ckey.ptr();
+      kcheck("sort");
+    }
+    uint32_t* fl = arena.get<uint32_t>(nc);
+    uint32_t* pos = arena.get<uint32_t>(nc);
+    uint32_t* tot = arena.get<uint32_t>(1);
+    {
+      Phase ph(this, 2);
+      launch_heads(ks, nc, fl, st);
+      exclusive_scan<uint32_t>(fl, pos, nc, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nc)), st);
+      kcheck("heads");
+    }
+    const int64_t nu = read_dev(tot);
+    uint64_t* ukey = arena.get<uint64_t>(nu);
+    float* up = semi != S_UNIT ? arena.get<float>(nu) : nullptr;
+    uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
+    {
+      Phase ph(this, 2);
+      launch_seg_reduce(ks, vs, pos, nc, semi, ukey, up, uw, st);
+      kcheck("seg reduce");
+    }
+    uint64_t* flags = arena.get<uint64_t>(nu);
+    uint64_t* offs = arena.get<uint64_t>(nu);
+    int64_t* fpos = arena.get<int64_t>(nu);
+    uint64_t* t2 = arena.get<uint64_t>(1);
+    {
+      Phase ph(this, 3);
+      launch_diff(ukey, up, uw, nu, S.key.ptr(), semi != S_UNIT ? S.p.ptr() : nullptr, S.n, semi, flags, fpos, st);
+      exclusive_scan<uint64_t>(flags, offs, nu, t2, arena.alloc(scan_tmp_bytes<uint64_t>(nu)), st);
+      kcheck("diff");
+    }
+    const uint64_t tt = read_dev(t2);
+    const int64_t nd = (int64_t)(tt & 0xffffffffull), nnew = (int64_t)(tt >> 32);
+    stats.bytes_algorithmic += bytes_round(nc, nu, nd);
+    S.nd = nd;
+    if (nd == 0) return 0;
+    Phase ph(this, 3);
+    S.dkey.reserve(nd);
+    if (semi != S_UNIT) S.dp.reserve(nd);
+    if (semi == S_MAXMULT) S.dw.reserve(nd);
+    uint64_t* nkey = arena.get<uint64_t>(nnew);
+    float* np_ = semi != S_UNIT ? arena.get<float>(nnew) : nullptr;
+    uint32_t* nw = semi == S_MAXMULT ? arena.get<uint32_t>(nnew) : nullptr;
+    launch_apply(ukey, up, uw, nu, flags, offs, fpos, semi, semi != S_UNIT ? S.p.ptr() : nullptr,
+                 semi == S_MAXMULT ? S.w.ptr() : nullptr, S.dkey.ptr(), semi != S_UNIT ? S.dp.ptr() : nullptr,
+                 semi == S_MAXMULT ? S.dw.ptr() : nullptr, nkey, np_, nw, st);
+    kcheck("apply");
+    if (nnew > 0) {
+      const int64_t nn = S.n + nnew;
+      S.key2.reserve(nn);
+      if (semi != S_UNIT) S.p2.reserve(nn);
+      if (semi == S_MAXMULT) S.w2.reserve(nn);
+      launch_merge(S.key.ptr(), semi != S_UNIT ? S.p.ptr() : nullptr, semi == S_MAXMULT ? S.w.ptr() : nullptr, S.n,
+                   nkey, np_, nw, nnew, S.key2.ptr(), semi != S_UNIT ? S.p2.ptr() : nullptr,
+                   semi == S_MAXMULT ? S.w2.ptr() : nullptr, st);
+      kcheck("merge");
+      S.key.swap(S.key2);
+      S.p.swap(S.p2);
+      S.w.swap(S.w2);
+      S.n = nn;
+    }
+    return nd;
+  }
+
+  int64_t bytes_round(int64_t nc, int64_t nu, int64_t nd) const {
+    const int64_t rt = semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4);
+    const int64_t rC = 8 + rt, rF = 8 + rt;
+    return 2 * nc * rC + nu * rF + nd * 2 * rF;
+  }
+
+  // ------------------------------------------------------------------- run
+  void run(lobster_run_stats* out) {
+    if (!loaded) throw Failure(LOBSTER_E_STATE, "run before program_load");
+    if (sticky) throw Failure(LOBSTER_E_CUDA, "context is in a failed state");
+    stats = lobster_run_stats{};
+    ev.clear();
+    ev_used = 0;
+    cudaEvent_t t0 = get_event(), t1;
+    cudaEventRecord(t0, st);
+    for (auto& r : rels) {
+      r->out_dev_ready = r->out_host_ready = false;
+      r->has_grad = false;
+    }
+    static_idx.clear();
+    arena.reset();
+    ingest();
+    int64_t round_cap_hit = 0;
+    for (size_t si = 0; si < prog.strata.size(); ++si) {
+      const std::vector<int>& strat = prog.strata[si];
+      std::set<int> local(strat.begin(), strat.end());
+      for (int r : strat) {
+        RelState& S = *rels[r];
+        S.n = S.nd = S.no = S.nc = 0;
+        S.key.reserve(1);
+        if (semi != S_UNIT) S.p.reserve(1);
+        if (semi == S_MAXMULT) S.w.reserve(1);
+      }
+      int rounds = 0;
+      bool first = true;
+      for (;;) {
+        if (rounds >= max_iters) { round_cap_hit = 1; break; }
+        rounds++;
+        arena.reset();
+        for (const Rule& R : prog.rules) {
+          if (!local.count(R.head_rel)) continue;
+          std::vector<int> lpos;
+          for (int k = 0; k < (int)R.body.size(); ++k)
+            if (local.count(R.body[k].rel)) lpos.push_back(k);
+          if (lpos.empty()) {
+            if (!first) continue;
+            std::vector<Version> ver(R.body.size(), V_EXT);
+            // start: smallest batched atom (ties: body order)
+            int start = -1;
+            int64_t best = INT64_MAX;
+            for (int k = 0; k < (int)R.body.size(); ++k) {
+              if (prog.rels[R.body[k].rel].shared) continue;
+              int64_t n = rels[R.body[k].rel]->n;
+              if (n < best) { best = n; start = k; }
+            }
+            eval_rule(R, ver, start);
+            continue;
+          }
+          if (first) continue;
+          for (size_t j = 0; j < lpos.size(); ++j) {
+            std::vector<Version> ver(R.body.size(), V_EXT);
+            for (size_t q = 0; q < lpos.size(); ++q)
+              ver[lpos[q]] = q == j ? V_DELTA : (q < j ? V_NEW : V_OLD);
+            eval_rule(R, ver, lpos[j]);
+          }
+        }
+        first = false;
+        int64_t changed = 0;
+        for (int r : strat) changed += settle(r);
+        if (changed == 0) break;
+      }
+      stats.rounds_total += rounds;
+      stats.strata++;
+      if (round_cap_hit) break;
+    }
+    for (size_t r = 0; r < prog.rels.size(); ++r)
+      if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
+    if (!round_cap_hit && semi == S_MAXMULT) {
+      Phase ph(this, 4);
+      gradients();
+    }
+    t1 = get_event();
+    cudaEventRecord(t1, st);
+    sync();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    stats.ms_total = ms;
+    for (auto& e : ev) {
+      float m = 0;
+      cudaEventElapsedTime(&m, e.second.first, e.second.second);
+      switch (e.first) {
+        case 0: stats.ms_join += m; break;
+        case 1: stats.ms_sort += m; break;
+        case 2: stats.ms_reduce += m; break;
+        case 3: stats.ms_merge += m; break;
+        default: stats.ms_grad += m; break;
+      }
+    }
+    ran = true;
+    arena.reset();
+    if (out) *out = stats;
+    if (round_cap_hit) throw Failure(LOBSTER_E_ITER_CAP, "max_iters rounds reached");
+  }
+
+  // --------------------------------------------------------- gradients (A11)
+  void gradients() {
+    const int nr = (int)prog.rels.size();
+    std::vector<WalkRel> wr(nr);
+    for (int r = 0; r < nr; ++r) {
+      RelState& S = *rels[r];
+      WalkRel& w = wr[r];
+      std::memset(&w, 0, sizeof(w));
+      w.key = S.key.ptr();
+      w.p = S.p.ptr();
+      w.w = S.w.ptr();
+      w.fid = S.fid.ptr();
+      w.n = S.n;
+      w.input = prog.rels[r].input ? 1 : 0;
+      w.has_sample = S.L.has_sample ? 1 : 0;
+      w.sshift = (uint8_t)S.L.sshift;
+      w.ncols = prog.rels[r].arity;
+      for (int c = 0; c < w.ncols; ++c) {
+        w.shift[c] = (uint8_t)S.L.shift[c];
+        w.bits[c] = (uint8_t)S.L.bits[c];
+        w.min[c] = S.L.mins[c];
+      }
+    }
+    std::vector<WalkRule> rules(prog.rules.size());
+    std::vector<int> base(nr, 0);
+    {
+      std::vector<int> cnt(nr, 0);
+      for (auto& R : prog.rules) cnt[R.head_rel]++;
+      int acc = 0;
+      for (int r = 0; r < nr; ++r) { base[r] = acc; acc += cnt[r]; }
+    }
+    std::vector<WalkRule> ordered(prog.rules.size());
+    for (auto& R : prog.rules) {
+      WalkRule wrl;
+      std::memset(&wrl, 0, sizeof(wrl));
+      wrl.natoms = (int)R.body.size();
+      for (int a = 0; a < wrl.natoms; ++a) {
+        wrl.atom[a].rel = R.body[a].rel;
+        wrl.atom[a].ncols = (int)R.body[a].args.size();
+        for (int c = 0; c < wrl.atom[a].ncols; ++c) {
+          wrl.atom[a].var[c] = (int8_t)R.body[a].args[c].var;
+          wrl.atom[a].cst[c] = R.body[a].args[c].cst;
+        }
+      }
+      wrl.nvars = (int)R.var_names.size();
+      for (int v = 0; v < 16; ++v) { wrl.head_col[v] = -1; wrl.wfield[v] = -1; }
+      for (size_t c = 0; c < R.head.size(); ++c)
+        if (R.head[c].is_var() && wrl.head_col[R.head[c].var] < 0) wrl.head_col[R.head[c].var] = (int8_t)c;
+      for (size_t i = 0; i < R.nonhead.size(); ++i) {
+        int v = R.nonhead[i];
+        wrl.wfield[v] = (int8_t)i;
+        wrl.wshift[v] = (uint8_t)wshift[R.global_index][i];
+        wrl.wbits[v] = (uint8_t)wbits[R.global_index][i];
+        wrl.wmin[v] = (int32_t)class_min[R.var_class[v]];
+      }
+      ordered[base[R.head_rel] + R.local_index] = wrl;
+    }
+    WalkRel* d_rels = arena.get<WalkRel>(nr);
+    WalkRule* d_rules = arena.get<WalkRule>((int64_t)ordered.size());
+    int* d_base = arena.get<int>(nr);
+    int* d_rb = arena.get<int>(nr);
+    int* d_err = arena.get<int>(1);
+    cuda_check(cudaMemcpyAsync(d_rels, wr.data(), nr * sizeof(WalkRel), cudaMemcpyHostToDevice, st), "H2D");
+    if (!ordered.empty())
+      cuda_check(cudaMemcpyAsync(d_rules, ordered.data(), ordered.size() * sizeof(WalkRule), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_base, base.data(), nr * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_rb, rule_bits.data(), nr * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemsetAsync(d_err, 0, sizeof(int), st), "memset");
+    WalkTables T{d_rels, d_rules, d_base, d_rb, nr};
+    for (int r = 0; r < nr; ++r) {
+      if (!prog.rels[r].output || prog.rels[r].input) continue;
+      RelState& S = *rels[r];
+      const int64_t n = S.n;
+      S.goff.reserve(n + 1);
+      if (n == 0) {
+        cuda_check(cudaMemsetAsync(S.goff.ptr(), 0, 8, st), "memset");
+        S.ng = 0;
+        S.has_grad = true;
+        continue;
+      }
+      int64_t* cnt = arena.get<int64_t>(n);
+      int64_t* loff = arena.get<int64_t>(n + 1);
+      launch_walk(T, r, n, 0, nullptr, cnt, nullptr, d_err, st);
+      exclusive_scan<int64_t>(cnt, loff, n, loff + n, arena.alloc(scan_tmp_bytes<int64_t>(n)), st);
+      kcheck("walk");
+      const int64_t nleaf = read_dev(loff + n);
+      const int e = read_dev(d_err);
+      if (e) throw Failure(LOBSTER_E_CUDA, "witness walk failed (code " + std::to_string(e) + ")");
+      uint64_t* k0 = arena.get<uint64_t>(nleaf);
+      uint64_t* k1 = arena.get<uint64_t>(nleaf);
+      launch_walk(T, r, n, 1, loff, nullptr, reinterpret_cast<int64_t*>(k0), d_err, st);
+      // leaf keys: tuple << 32 | fact, sorted -> unique (tuple, fact) runs
+      tag_leaves(k0, loff, n, nleaf);
+      const int tbits = 32 + bits_for((uint64_t)n);
+      int which = radix_sort<void>(k0, nullptr, k1, nullptr, nleaf, tbits, arena.alloc(sort_tmp_bytes(nleaf)), st);
+      uint64_t* ks = which ? k1 : k0;
+      uint32_t* fl = arena.get<uint32_t>(nleaf);
+      uint32_t* pos = arena.get<uint32_t>(nleaf);
+      uint32_t* tot = arena.get<uint32_t>(1);
+      launch_leaf_heads(ks, nleaf, fl, st);
+      exclusive_scan<uint32_t>(fl, pos, nleaf, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nleaf)), st);
+      kcheck("leaf heads");
+      const int64_t nuniq = read_dev(tot);
+      S.gfid.reserve(nuniq);
+      S.gval.reserve(nuniq);
+      double* scratch = arena.get<double>(nuniq);
+      launch_grad(ks, pos, nleaf, nuniq, fact_p.ptr(), n, loff, S.goff.ptr(), S.gfid.ptr(), S.gval.ptr(), scratch, st);
+      kcheck("grad");
+      S.ng = nuniq;
+      S.has_grad = true;
+    }
+  }
+
+  void tag_leaves(uint64_t* k, const int64_t* loff, int64_t n, int64_t nleaf);
+
+  // ------------------------------------------------------------- outputs
+  void output_get(const char* relname, int where, lobster_output* out) {
+    if (!relname || !out) throw Failure(LOBSTER_E_INVALID_ARG, "NULL argument");
+    if (where != 0 && where != 1) throw Failure(LOBSTER_E_INVALID_ARG, "where must be 0 (host) or 1 (device)");
+    auto it = prog.rel_id.find(relname);
+    if (it == prog.rel_id.end()) throw Failure(LOBSTER_E_INVALID_ARG, std::string("unknown relation ") + relname);
+    if (!ran) throw Failure(LOBSTER_E_STATE, "output_get before a successful run");
+    const int r = it->second;
+    RelState& S = *rels[r];
+    const int ar = prog.rels[r].arity;
+    const int64_t n = S.n;
+    if (!S.out_dev_ready) {
+      S.o_sid.reserve(n);
+      S.o_cols.reserve((int64_t)ar * n);
+      S.o_soff.reserve(opt.batch_size + 1);
+      uint8_t* dsh = arena.get<uint8_t>(3 * 8 + 64);
+      std::vector<uint8_t> hb(16 + 32, 0);
+      for (int c = 0; c < ar; ++c) { hb[c] = (uint8_t)S.L.shift[c]; hb[8 + c] = (uint8_t)S.L.bits[c]; }
+      std::memcpy(hb.data() + 16, S.L.mins.data(), ar * 4);
+      cuda_check(cudaMemcpyAsync(dsh, hb.data(), hb.size(), cudaMemcpyHostToDevice, st), "H2D");
+      launch_unpack(S.key.ptr(), n, S.L.has_sample, (uint8_t)S.L.sshift, ar, dsh, dsh + 8,
+                    reinterpret_cast<int32_t*>(dsh + 16), S.o_sid.ptr(), S.o_cols.ptr(), st);
+      launch_sample_offsets(S.key.ptr(), n, opt.batch_size, (uint8_t)S.L.sshift, S.L.has_sample, S.o_soff.ptr(), st);
+      kcheck("unpack");
+      sync();
+      arena.reset();
+      S.out_dev_ready = true;
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->n = n;
+    out->arity = ar;
+    out->on_device = where;
+    if (where == 1) {
+      S.col_ptrs.assign(ar, nullptr);
+      for (int c = 0; c < ar; ++c) S.col_ptrs[c] = S.o_cols.ptr() + (int64_t)c * n;
+      out->sample_ids = S.o_sid.ptr();
+      out->columns = S.col_ptrs.data();
+      out->probs = semi != S_UNIT ? S.p.ptr() : nullptr;
+      out->sample_offsets = S.o_soff.ptr();
+      if (S.has_grad) {
+        out->grad_offsets = S.goff.ptr();
+        out->grad_fact_ids = S.gfid.ptr();
+        out->grad_values = S.gval.ptr();
+      }
+      return;
+    }
+    if (!S.out_host_ready) {
+      S.h_sid.resize(n);
+      S.h_cols.resize((size_t)ar * n);
+      S.h_soff.resize(opt.batch_size + 1);
+      if (n) {
+        cuda_check(cudaMemcpyAsync(S.h_sid.data(), S.o_sid.ptr(), n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (ar) cuda_check(cudaMemcpyAsync(S.h_cols.data(), S.o_cols.ptr(), (size_t)ar * n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      }
+      cuda_check(cudaMemcpyAsync(S.h_soff.data(), S.o_soff.ptr(), (opt.batch_size + 1) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+      if (semi != S_UNIT) {
+        S.h_p.resize(n);
+        if (n) cuda_check(cudaMemcpyAsync(S.h_p.data(), S.p.ptr(), n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      }
+      if (S.has_grad) {
+        S.h_goff.resize(n + 1);
+        S.h_gfid.resize(S.ng);
+        S.h_gval.resize(S.ng);
+        cuda_check(cudaMemcpyAsync(S.h_goff.data(), S.goff.ptr(), (n + 1) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        if (S.ng) {
+          cuda_check(cudaMemcpyAsync(S.h_gfid.data(), S.gfid.ptr(), S.ng * 8, cudaMemcpyDeviceToHost, st), "D2H");
+          cuda_check(cudaMemcpyAsync(S.h_gval.data(), S.gval.ptr(), S.ng * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+      }
+      sync();
+      S.out_host_ready = true;
+    }
+    S.col_ptrs.assign(ar, nullptr);
+    for (int c = 0; c < ar; ++c) S.col_ptrs[c] = S.h_cols.data() + (size_t)c * n;
+    out->sample_ids = S.h_sid.data();
+    out->columns = S.col_ptrs.data();
+    out->probs = semi != S_UNIT ? S.h_p.data() : nullptr;
+    out->sample_offsets = S.h_soff.data();
+    if (S.has_grad) {
+      out->grad_offsets = S.h_goff.data();
+      out->grad_fact_ids = S.h_gfid.data();
+      out->grad_values = S.h_gval.data();
+    }
+  }
+
+  void backward(const char* relname, const float* upstream, float* grad_facts) {
+    if (!relname || !upstream || !grad_facts) throw Failure(LOBSTER_E_INVALID_ARG, "NULL argument");
+    auto it = prog.rel_id.find(relname);
+    if (it == prog.rel_id.end()) throw Failure(LOBSTER_E_INVALID_ARG, std::string("unknown relation ") + relname);
+    if (!ran) throw Failure(LOBSTER_E_STATE, "backward before a successful run");
+    RelState& S = *rels[it->second];
+    if (semi != S_MAXMULT || !S.has_grad) throw Failure(LOBSTER_E_INVALID_ARG, "no gradients for this relation");
+    const int64_t nf = num_facts_db;
+    cuda_check(cudaMemsetAsync(grad_facts, 0, nf * sizeof(float), st), "memset");
+    const int64_t ng = S.ng;
+    if (ng > 0) {
+      uint64_t* k0 = arena.get<uint64_t>(ng);
+      uint64_t* k1 = arena.get<uint64_t>(ng);
+      uint32_t* v0 = arena.get<uint32_t>(ng);
+      uint32_t* v1 = arena.get<uint32_t>(ng);
+      launch_grad_contrib(S.goff.ptr(), S.gfid.ptr(), S.gval.ptr(), upstream, S.n, ng, k0, v0, st);
+      int which = radix_sort<uint32_t>(k0, v0, k1, v1, ng, bits_for((uint64_t)nf), arena.alloc(sort_tmp_bytes(ng)), st);
+      launch_dense_sum(which ? k1 : k0, which ? v1 : v0, nullptr, ng, grad_facts, st);
+      kcheck("backward");
+    }
+    sync();
+    arena.reset();
+  }
+};
+
+}  // namespace lob
+
+// ============================================================================
+// small kernels used only by the driver
+// ============================================================================
+namespace lob {
+namespace {
+__global__ void scatter_p_k(const int32_t* __restrict__ fid, const float* __restrict__ p, int64_t n,
+                            float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[fid[i]] = p[i];
+}
+__global__ void tag_leaves_k(uint64_t* __restrict__ k, const int64_t* __restrict__ loff, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  for (int64_t i = loff[t]; i < loff[t + 1]; ++i) k[i] = ((uint64_t)t << 32) | (uint64_t)(uint32_t)k[i];
+}
+int gridn(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
+}
+}  // namespace
+void Ctx::scatter_fact_p(const int32_t* fid, const float* p, int64_t n) {
+  if (n > 0) scatter_p_k<<<gridn(n), 256, 0, st>>>(fid, p, n, fact_p.ptr());
+  kcheck("scatter p");
+}
+void Ctx::tag_leaves(uint64_t* k, const int64_t* loff, int64_t n, int64_t nleaf) {
+  (void)nleaf;
+  if (n > 0) tag_leaves_k<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(k, loff, n);
+  kcheck("tag leaves");
+}
+}  // namespace lob
+
+// ============================================================================
+// C ABI
+// ============================================================================
+struct lobster_ctx {
+  lob::Ctx c;
+};
+
+namespace {
+template <typename F>
+lobster_status guarded(lobster_ctx* ctx, F&& f) {
+  if (!ctx) return LOBSTER_E_INVALID_ARG;
+  try {
+    f();
+    ctx->c.err.clear();
+    return LOBSTER_OK;
+  } catch (lob::Failure& e) {
+    ctx->c.err = e.what();
+    if (e.code == LOBSTER_E_CUDA) ctx->c.sticky = true;
+    return (lobster_status)e.code;
+  } catch (std::exception& e) {
+    ctx->c.err = e.what();
+    return LOBSTER_E_INVALID_ARG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+lobster_status lobster_create(const lobster_options* options, lobster_ctx** out) {
+  if (!out) return LOBSTER_E_INVALID_ARG;
+  *out = nullptr;
+  lobster_ctx* ctx = nullptr;
+  try {
+    ctx = new lobster_ctx();
+    ctx->c.create(options);
+  } catch (lob::Failure& e) {
+    delete ctx;
+    return (lobster_status)e.code;
+  } catch (std::exception&) {
+    delete ctx;
+    return LOBSTER_E_CUDA;
+  }
+  *out = ctx;
+  return LOBSTER_OK;
+}
+
+void lobster_destroy(lobster_ctx* ctx) { delete ctx; }
+
+const char* lobster_last_error(const lobster_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "NULL context"; }
+
+lobster_status lobster_program_load(lobster_ctx* ctx, const char* text, lobster_semiring semiring) {
+  return guarded(ctx, [&]() { ctx->c.load(text, (int)semiring); });
+}
+
+lobster_status lobster_facts_push(lobster_ctx* ctx, const char* relation, int64_t n, const int32_t* const* columns,
+                                  const int32_t* sample_ids, const float* probs, int64_t* first_fact_id) {
+  int64_t dummy = 0;
+  return guarded(ctx, [&]() {
+    ctx->c.push(relation, n, columns, sample_ids, probs, first_fact_id ? first_fact_id : &dummy);
+  });
+}
+
+lobster_status lobster_run(lobster_ctx* ctx, lobster_run_stats* stats) {
+  return guarded(ctx, [&]() { ctx->c.run(stats); });
+}
+
+lobster_status lobster_output_get(lobster_ctx* ctx, const char* relation, int32_t where, lobster_output* out) {
+  return guarded(ctx, [&]() { ctx->c.output_get(relation, where, out); });
+}
+
+lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation, const float* upstream,
+                                       float* grad_facts) {
+  return guarded(ctx, [&]() { ctx->c.backward(relation, upstream, grad_facts); });
+}
+
+int64_t lobster_num_facts(const lobster_ctx* ctx) { return ctx ? ctx->c.next_fact : 0; }
+
+}  // extern "C"

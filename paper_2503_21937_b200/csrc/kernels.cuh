@@ -1,0 +1,231 @@
+// kernels.cuh — device plan structures and launchers of the sm_100a kernels.
+//
+// Every relation row is a packed u64 key (SURVEY §8(a) layout):
+//   key = sample << Σbits | (c0 - min0) << ... | (c_{n-1} - min_{n-1})
+// order-preserving for the lexicographic (sample, c0, ...) order, plus
+// SoA tag columns: p (fp32 bits) and, under diff-max-mult, w (u32 witness).
+// Keys use at most 63 bits; KEY_DEAD (all ones) marks a row removed by a filter.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lob {
+
+constexpr uint64_t KEY_DEAD = ~0ull;
+constexpr int MAXM = 10;   // max bit moves per output word
+constexpr int MAXT = 6;    // max atoms per rule (tags carried by an intermediate)
+constexpr int MAXC = 4;    // max comparisons applied in one join step
+
+enum Semi : int { S_UNIT = 0, S_MAXMIN = 1, S_ADDMULT = 2, S_MAXMULT = 3 };
+
+// Copy `bits` bits found at `sshift` of the source word (0 = probe key,
+// 1 = build key) to `dshift` of the destination word.  A variable keeps its
+// domain class (same min and width) in every relation it flows through, so a
+// projection / permutation is a pure bit move (no decode / re-encode).
+struct Move {
+  uint8_t src, sshift, bits, dshift;
+};
+
+// One side of a comparison: a decoded value (field + min) or a constant.
+struct Operand {
+  int8_t src;      // 0 probe key, 1 build key, 2 constant
+  uint8_t shift, bits;
+  int32_t base;    // min of the field, or the constant value
+};
+struct Cmp {
+  Operand a, b;
+  int8_t neq;
+};
+
+// A join step: probe rows (sorted packed keys) x a sorted build index whose key
+// is [prefix | free fields]; prefix built from the probe key by moves.
+struct JoinPlan {
+  // probe
+  const uint64_t* pkey;
+  int64_t np;
+  const float* ptag[MAXT];
+  int npt;
+  // build lookup
+  int nprem;
+  Move prem[MAXM];
+  uint64_t cprefix;         // constant bits of the prefix
+  const uint64_t* bkey;
+  const float* btag;        // nullable (unit)
+  int64_t nb;
+  const int64_t* boff;      // CSR offsets over the prefix domain, or null (binary search)
+  int64_t nprefix;          // entries of boff minus one
+  int free_bits;            // bits below the prefix in the index key
+  // repeated free variables: value at shift a must equal value at shift b (build key)
+  int nfeq;
+  Move feq[2];
+  // filters
+  int ncmp;
+  Cmp cmp[MAXC];
+  // output key
+  int nom;
+  Move om[MAXM];
+  uint64_t cout;            // constant bits of the output key
+  int final_step;           // 1: candidates (head key, ⊗, witness); 0: intermediate
+  int semi;
+  // ⊗ in body order over T = [ptag[0..npt-1], btag]: T[tag_order[k]] for k = 0..ntag-1
+  int ntag;
+  int8_t tag_order[MAXT];
+  // witness: w = wconst | moves (diff-max-mult)
+  int nwm;
+  Move wm[MAXM];
+  uint32_t wconst;
+  // outputs
+  uint64_t* okey;
+  float* otag[MAXT];        // intermediate: npt + 1 tag columns
+  uint32_t* oval32;         // final, max-min / add-mult: p bits
+  uint64_t* oval64;         // final, max-mult: p bits | w << 32
+};
+
+// Single-atom rule (projection): rows of one relation -> candidates.
+struct ProjectPlan {
+  const uint64_t* key;
+  const float* tag;
+  int64_t n;
+  int ncmp;
+  Cmp cmp[MAXC];  // operands read from src 0
+  int nom;
+  Move om[MAXM];
+  uint64_t cout;
+  int semi;
+  uint32_t wconst;
+  int nwm;
+  Move wm[MAXM];
+  uint64_t* okey;
+  uint32_t* oval32;
+  uint64_t* oval64;
+};
+
+// ---- scan ----
+// Exclusive prefix sum; writes the total to *total_dev (device).  T in
+// {uint32_t, int64_t, uint64_t}.  tmp: scratch of scan_tmp_bytes(n) bytes.
+template <typename T>
+size_t scan_tmp_bytes(int64_t n);
+template <typename T>
+void exclusive_scan(const T* in, T* out, int64_t n, T* total_dev, void* tmp, cudaStream_t st);
+
+// ---- radix sort (LSD, 8-bit digits, stable) ----
+// V in {void (keys only), uint32_t, uint64_t}.  Sorts the low `bits` bits.
+// Ping-pong between (k0,v0) and (k1,v1); returns 0 if the result is in k0/v0.
+size_t sort_tmp_bytes(int64_t n);
+template <typename V>
+int radix_sort(uint64_t* k0, V* v0, uint64_t* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st);
+
+// ---- ingest (A0) ----
+void launch_minmax(const int32_t* col, int64_t n, int32_t* out2 /* device: min,max */, cudaStream_t st);
+// key = sample << sshift | Σ (col_c - min_c) << shift_c
+struct PackPlan {
+  int ncols;
+  const int32_t* col[8];
+  int32_t min[8];
+  uint8_t shift[8];
+  const int32_t* sample;  // null for shared
+  uint8_t sshift;
+};
+void launch_pack(const PackPlan& pp, int64_t n, uint64_t* key, uint32_t* rowid, cudaStream_t st);
+// gather p / fid by rowid
+void launch_gather_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, cudaStream_t st);
+void launch_gather_i32(const int32_t* src, const uint32_t* idx, int32_t* dst, int64_t n, cudaStream_t st);
+void launch_iota_i32(int32_t* dst, int64_t n, int32_t first, cudaStream_t st);
+void launch_fill_f32(float* dst, int64_t n, float v, cudaStream_t st);
+// range check of pushed data: flags bit0 = prob NaN/out of [0,1], bit1 = sample out of range
+void launch_validate(const float* p, const int32_t* s, int64_t n, int32_t batch, uint32_t* flags, cudaStream_t st);
+
+// EDB duplicate merge (reading 16): sorted keys; heads -> scan -> reduce.
+void launch_heads(const uint64_t* key, int64_t n, uint32_t* flag, cudaStream_t st);
+void launch_edb_reduce(const uint64_t* key, const float* p, const int32_t* fid, const uint32_t* pos, int64_t n,
+                       int semi, uint64_t* okey, float* op, int32_t* ofid, cudaStream_t st);
+
+// ---- join (A3-A5) ----
+void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaStream_t st);
+void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
+                       cudaStream_t st);
+void launch_project(const ProjectPlan& pp, cudaStream_t st);
+
+// ---- index build (A1) ----
+// re-key rows: out = Σ moves(key) ; tags copied
+void launch_rekey(const uint64_t* key, int64_t n, const Move* mv, int nmv, uint64_t* out, cudaStream_t st);
+void launch_build_offsets(const uint64_t* key, int64_t n, int free_bits, int64_t nprefix, int64_t* off,
+                          cudaStream_t st);
+
+// ---- dedup (A6-A7) and merge/diff (A8-A9) ----
+// U = segmented ⊕ over sorted candidates (vals: u32 p bits or u64 p|w<<32)
+void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int semi,
+                       uint64_t* ukey, float* up, uint32_t* uw, cudaStream_t st);
+// classify U against F: flags (u64: lo = in Δ', hi = new); pos (F index or -1)
+void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu,
+                 const uint64_t* fkey, const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos,
+                 cudaStream_t st);
+// write Δ' and NEW rows, apply in-place ⊕ updates to F
+void launch_apply(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* flags,
+                  const uint64_t* offs, const int64_t* pos, int semi, float* fp, uint32_t* fw, uint64_t* dkey,
+                  float* dp, uint32_t* dw, uint64_t* nkey, float* np_, uint32_t* nw, cudaStream_t st);
+// F' = merge(F, NEW) (disjoint sorted key sets)
+void launch_merge(const uint64_t* akey, const float* ap, const uint32_t* aw, int64_t na, const uint64_t* bkey,
+                  const float* bp, const uint32_t* bw, int64_t nb, uint64_t* okey, float* op, uint32_t* ow,
+                  cudaStream_t st);
+
+// ---- witness walk + gradient (A11) ----
+struct WalkRel {
+  const uint64_t* key;
+  const float* p;
+  const uint32_t* w;       // IDB witness
+  const int32_t* fid;      // EDB fact id
+  int64_t n;
+  int input;
+  int has_sample;
+  uint8_t sshift;
+  int ncols;
+  uint8_t shift[8], bits[8];
+  int32_t min[8];
+};
+struct WalkAtom {
+  int rel;
+  int ncols;
+  int8_t var[8];   // var id or -1 for a constant
+  int32_t cst[8];
+};
+struct WalkRule {
+  int natoms;
+  WalkAtom atom[MAXT];
+  int nvars;
+  // var values: from the head tuple column, or from the witness field
+  int8_t head_col[16];        // var -> head column or -1
+  int8_t wfield[16];          // var -> witness field index or -1
+  uint8_t wshift[16], wbits[16];
+  int32_t wmin[16];
+};
+struct WalkTables {
+  WalkRel* rels;        // device arrays
+  WalkRule* rules;      // indexed by rule_base[head_rel] + local rule index
+  int* rule_base;
+  int* rule_bits;       // per relation: witness bits taken by the rule index
+  int nrels;
+};
+// pass 0: count leaves per tuple; pass 1: write leaf fact ids at offs
+void launch_walk(const WalkTables& T, int rel, int64_t n, int pass, const int64_t* offs, int64_t* cnt,
+                 int64_t* leaves, int* err, cudaStream_t st);
+// grads from sorted (tuple, fact) leaves: unique facts with multiplicity
+void launch_leaf_heads(const uint64_t* k, int64_t n, uint32_t* flag, cudaStream_t st);
+void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, int64_t nuniq, const float* fact_p,
+                 int64_t ntup, const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
+                 cudaStream_t st);
+
+// ---- output extract (A12) ----
+void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,
+                   const uint8_t* bits, const int32_t* mins, int32_t* sample, int32_t* cols, cudaStream_t st);
+void launch_sample_offsets(const uint64_t* key, int64_t n, int32_t batch, uint8_t sshift, int has_sample,
+                           int64_t* off, cudaStream_t st);
+
+// ---- backward (optional) ----
+void launch_grad_contrib(const int64_t* goff, const int64_t* gfid, const float* gval, const float* upstream,
+                         int64_t n, int64_t ng, uint64_t* key, uint32_t* val, cudaStream_t st);
+void launch_dense_sum(const uint64_t* key, const uint32_t* val, const uint32_t* pos, int64_t n, float* dense,
+                      cudaStream_t st);
+
+}  // namespace lob
