@@ -162,6 +162,9 @@ lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation,
 /* Number of facts pushed into the current database (size of grad_facts). */
 int64_t lobster_num_facts(const lobster_ctx* ctx);
 
+/* Diagnostics: CUDA kernels this library has launched in this process so far. */
+int64_t lobster_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,7 +45,7 @@ class Output(ctypes.Structure):
 
 EXPORTS = ["lobster_create", "lobster_destroy", "lobster_last_error", "lobster_program_load",
            "lobster_facts_push", "lobster_run", "lobster_output_get", "lobster_output_backward",
-           "lobster_num_facts"]
+           "lobster_num_facts", "lobster_kernel_launches"]
 
 _lib = None
 
@@ -79,5 +79,7 @@ def load():
     L.lobster_output_backward.restype = ctypes.c_int
     L.lobster_num_facts.argtypes = [vp]
     L.lobster_num_facts.restype = ctypes.c_int64
+    L.lobster_kernel_launches.argtypes = []
+    L.lobster_kernel_launches.restype = ctypes.c_int64
     _lib = L
     return L

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -30,6 +31,9 @@
 #include "program.hpp"
 
 namespace lob {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static int bits_for(uint64_t range) { return range == 0 ? 0 : 64 - __builtin_clzll(range); }
 
@@ -928,7 +932,7 @@ struct Ctx {
     uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
     {
       Phase ph(this, 2);
-      launch_seg_reduce(ks, vs, pos, nc, semi, ukey, up, uw, st);
+      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 1), st);
       kcheck("seg reduce");
     }
     uint64_t* flags = arena.get<uint64_t>(nu);
@@ -1326,12 +1330,18 @@ int gridn(int64_t n) {
 }
 }  // namespace
 void Ctx::scatter_fact_p(const int32_t* fid, const float* p, int64_t n) {
-  if (n > 0) scatter_p_k<<<gridn(n), 256, 0, st>>>(fid, p, n, fact_p.ptr());
+  if (n > 0) {
+    note_launch();
+    scatter_p_k<<<gridn(n), 256, 0, st>>>(fid, p, n, fact_p.ptr());
+  }
   kcheck("scatter p");
 }
 void Ctx::tag_leaves(uint64_t* k, const int64_t* loff, int64_t n, int64_t nleaf) {
   (void)nleaf;
-  if (n > 0) tag_leaves_k<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(k, loff, n);
+  if (n > 0) {
+    note_launch();
+    tag_leaves_k<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(k, loff, n);
+  }
   kcheck("tag leaves");
 }
 }  // namespace lob
@@ -1412,5 +1422,7 @@ lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation, c
 }
 
 int64_t lobster_num_facts(const lobster_ctx* ctx) { return ctx ? ctx->c.next_fact : 0; }
+
+int64_t lobster_kernel_launches(void) { return lob::g_launches.load(); }
 
 }  // extern "C"

@@ -59,12 +59,53 @@ __device__ __forceinline__ float tag_at(const JoinPlan& jp, int idx, int64_t row
   return t;
 }
 
+// Output-slot tiles: CTA b owns slots [b*WT, (b+1)*WT).  Thread 0 finds the
+// tile's probe-row range by binary search on the scanned offsets; when the
+// range is small its offsets are staged in shared memory and each slot's row
+// is found there (load-balanced expansion, skew-proof).
+constexpr int WT = 2048;
+constexpr int WROWS = 2048;
+
+__device__ __forceinline__ int64_t smem_row(const int64_t* s, int n, int64_t o) {
+  int lo = 0, hi = n;  // largest i with s[i] <= o
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (s[mid] <= o) lo = mid + 1; else hi = mid;
+  }
+  return lo - 1;
+}
+
 __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int64_t* __restrict__ offs,
                                                     const int64_t* __restrict__ start, int64_t total) {
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = upper_bound_m1_i64(offs, jp.np, o);
-    const int64_t j = start[row] + (o - offs[row]);
+  __shared__ int64_t soff[WROWS];
+  __shared__ int64_t r0s, r1s;
+  const int64_t o0 = (int64_t)blockIdx.x * WT;
+  if (o0 >= total) return;
+  const int64_t o1 = (o0 + WT < total ? o0 + WT : total) - 1;
+  if (threadIdx.x == 0) {
+    r0s = upper_bound_m1_i64(offs, jp.np, o0);
+    r1s = upper_bound_m1_i64(offs, jp.np, o1);
+  }
+  __syncthreads();
+  const int64_t r0 = r0s, r1 = r1s;
+  const int nrows = (int)(r1 - r0 + 1);
+  const bool staged = r1 - r0 + 1 <= WROWS;
+  if (staged)
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) soff[i] = offs[r0 + i];
+  __syncthreads();
+  for (int64_t o = o0 + threadIdx.x; o <= o1; o += blockDim.x) {
+    int64_t row;
+    if (staged) {
+      row = r0 + smem_row(soff, nrows, o);
+    } else {
+      int64_t lo = r0, hi = r1 + 1;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (offs[mid] <= o) lo = mid + 1; else hi = mid;
+      }
+      row = lo - 1;
+    }
+    const int64_t j = start[row] + (o - (staged ? soff[row - r0] : offs[row]));
     const uint64_t pk = jp.pkey[row];
     const uint64_t bk = jp.bkey[j];
     bool ok = true;
@@ -147,17 +188,20 @@ __global__ void build_offsets_k(const uint64_t* __restrict__ key, int64_t n, int
 
 void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaStream_t st) {
   if (jp.np <= 0) return;
+  note_launch();
   join_count_k<<<grid_for(jp.np, 256), 256, 0, st>>>(jp, count, start);
 }
 
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
                        cudaStream_t st) {
   if (total <= 0) return;
-  join_write_k<<<grid_for(total, 256), 256, 0, st>>>(jp, offs, start, total);
+  note_launch();
+  join_write_k<<<(unsigned)((total + WT - 1) / WT), 256, 0, st>>>(jp, offs, start, total);
 }
 
 void launch_project(const ProjectPlan& pp, cudaStream_t st) {
   if (pp.n <= 0) return;
+  note_launch();
   project_k<<<grid_for(pp.n, 256), 256, 0, st>>>(pp);
 }
 
@@ -166,11 +210,13 @@ void launch_rekey(const uint64_t* key, int64_t n, const Move* mv, int nmv, uint6
   MoveList ml = {};
   ml.n = nmv < MAXM ? nmv : MAXM;
   for (int i = 0; i < ml.n; ++i) ml.m[i] = mv[i];
+  note_launch();
   rekey_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, ml, out);
 }
 
 void launch_build_offsets(const uint64_t* key, int64_t n, int free_bits, int64_t nprefix, int64_t* off,
                           cudaStream_t st) {
+  note_launch();
   build_offsets_k<<<grid_for(nprefix + 1, 256), 256, 0, st>>>(key, n, free_bits, nprefix, off);
 }
 

@@ -112,45 +112,112 @@ __global__ void edb_reduce_k(const uint64_t* __restrict__ key, const float* __re
   }
 }
 
-// U = segmented ⊕ of sorted candidates (A7).
-template <int SEMI>
-__global__ void seg_reduce_k(const uint64_t* __restrict__ key, const void* __restrict__ valv,
-                             const uint32_t* __restrict__ pos, int64_t n, uint64_t* __restrict__ ukey,
-                             float* __restrict__ up, uint32_t* __restrict__ uw) {
+// U = segmented ⊕ of sorted candidates (A7).  Segment boundaries come from
+// the head flags' scan (pos); uend[u] = one past the last element of segment u.
+// Short segments: one thread each, left-to-right.  Long segments (> LONG_SEG,
+// e.g. the per-sample `endpoints_connected()` groups of ~1M candidates): one
+// CTA each, strided partials combined by a fixed-shape tree (deterministic).
+constexpr int LONG_SEG = 64;
+
+__global__ void seg_ends_k(const uint64_t* __restrict__ key, const uint32_t* __restrict__ pos, int64_t n,
+                           uint32_t* __restrict__ uend) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = key[i];
-    if (k == KEY_DEAD || (i > 0 && key[i - 1] == k)) continue;
-    const uint32_t u = pos[i];
-    ukey[u] = k;
-    if constexpr (SEMI == S_UNIT) continue;
-    if constexpr (SEMI == S_MAXMULT) {
-      const uint64_t* val = (const uint64_t*)valv;
-      uint64_t b = val[i];
-      float bp = u2f((uint32_t)b);
-      uint32_t bw = (uint32_t)(b >> 32);
-      for (int64_t j = i + 1; j < n && key[j] == k; ++j) {
-        const uint64_t c = val[j];
-        const float cp = u2f((uint32_t)c);
-        const uint32_t cw = (uint32_t)(c >> 32);
-        if (cp > bp || (cp == bp && cw < bw)) { bp = cp; bw = cw; }
-      }
-      up[u] = bp;
-      uw[u] = bw;
-    } else {
-      const uint32_t* val = (const uint32_t*)valv;
-      if constexpr (SEMI == S_ADDMULT) {
-        double acc = (double)u2f(val[i]);
-        for (int64_t j = i + 1; j < n && key[j] == k; ++j) acc = __dadd_rn(acc, (double)u2f(val[j]));
-        up[u] = (float)acc;
-      } else {
-        float bp = u2f(val[i]);
-        for (int64_t j = i + 1; j < n && key[j] == k; ++j) {
-          const float c = u2f(val[j]);
-          if (c > bp) bp = c;
-        }
-        up[u] = bp;
-      }
+    if (k == KEY_DEAD) continue;
+    if (i == n - 1 || key[i + 1] != k) {
+      const bool head = i == 0 || key[i - 1] != k;  // pos = exclusive count of heads
+      uend[pos[i] - (head ? 0u : 1u)] = (uint32_t)(i + 1);
     }
+  }
+}
+
+struct Acc {
+  double s;    // add-mult sum
+  float p;     // max
+  uint32_t w;  // witness (max-mult)
+};
+
+template <int SEMI>
+__device__ __forceinline__ Acc acc_load(const void* valv, int64_t j) {
+  Acc a{0.0, 0.0f, 0u};
+  if constexpr (SEMI == S_MAXMULT) {
+    const uint64_t c = ((const uint64_t*)valv)[j];
+    a.p = u2f((uint32_t)c);
+    a.w = (uint32_t)(c >> 32);
+  } else if constexpr (SEMI == S_ADDMULT) {
+    a.s = (double)u2f(((const uint32_t*)valv)[j]);
+  } else if constexpr (SEMI == S_MAXMIN) {
+    a.p = u2f(((const uint32_t*)valv)[j]);
+  }
+  return a;
+}
+
+// b follows a in canonical order
+template <int SEMI>
+__device__ __forceinline__ Acc acc_join(Acc a, Acc b) {
+  if constexpr (SEMI == S_ADDMULT) {
+    a.s = __dadd_rn(a.s, b.s);
+  } else if constexpr (SEMI == S_MAXMULT) {
+    if (b.p > a.p || (b.p == a.p && b.w < a.w)) { a.p = b.p; a.w = b.w; }
+  } else if constexpr (SEMI == S_MAXMIN) {
+    if (b.p > a.p) a.p = b.p;
+  }
+  return a;
+}
+
+template <int SEMI>
+__device__ __forceinline__ void acc_store(Acc a, int64_t u, float* up, uint32_t* uw) {
+  if constexpr (SEMI == S_ADDMULT) up[u] = (float)a.s;
+  if constexpr (SEMI == S_MAXMIN || SEMI == S_MAXMULT) up[u] = a.p;
+  if constexpr (SEMI == S_MAXMULT) uw[u] = a.w;
+}
+
+template <int SEMI>
+__global__ void seg_reduce_short_k(const uint64_t* __restrict__ key, const void* __restrict__ valv,
+                                   const uint32_t* __restrict__ uend, int64_t nu, uint64_t* __restrict__ ukey,
+                                   float* __restrict__ up, uint32_t* __restrict__ uw, uint32_t* __restrict__ nlong,
+                                   uint32_t* __restrict__ longs) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
+    ukey[u] = key[s];
+    if constexpr (SEMI == S_UNIT) continue;
+    if (e - s > LONG_SEG) {
+      longs[atomicAdd(nlong, 1u)] = (uint32_t)u;
+      continue;
+    }
+    Acc a = acc_load<SEMI>(valv, s);
+    for (int64_t j = s + 1; j < e; ++j) a = acc_join<SEMI>(a, acc_load<SEMI>(valv, j));
+    acc_store<SEMI>(a, u, up, uw);
+  }
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256) seg_reduce_long_k(const void* __restrict__ valv,
+                                                         const uint32_t* __restrict__ uend,
+                                                         const uint32_t* __restrict__ nlong,
+                                                         const uint32_t* __restrict__ longs, float* __restrict__ up,
+                                                         uint32_t* __restrict__ uw) {
+  __shared__ Acc part[256];
+  const uint32_t nl = *nlong;
+  for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+    const uint32_t u = longs[q];
+    const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
+    // thread t folds elements s+t, s+t+256, ... (in order)
+    Acc a = acc_load<SEMI>(valv, s + threadIdx.x < e ? s + threadIdx.x : s);
+    bool have = s + threadIdx.x < e;
+    for (int64_t j = s + threadIdx.x + 256; j < e; j += 256) a = acc_join<SEMI>(a, acc_load<SEMI>(valv, j));
+    part[threadIdx.x] = a;
+    __syncthreads();
+    // fixed pairwise tree over thread partials (every segment here has > 64 elements,
+    // so partials 0..63 always exist; missing partials only occur above e - s)
+    const int cnt = (int)((e - s) < 256 ? (e - s) : 256);
+    for (int d = 1; d < 256; d <<= 1) {
+      if ((threadIdx.x % (2 * d)) == 0 && threadIdx.x + d < cnt) part[threadIdx.x] = acc_join<SEMI>(part[threadIdx.x], part[threadIdx.x + d]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) acc_store<SEMI>(part[0], u, up, uw);
+    __syncthreads();
+    (void)have;
   }
 }
 
@@ -251,54 +318,95 @@ __global__ void merge_k(const uint64_t* __restrict__ ak, const float* __restrict
 
 void launch_minmax(const int32_t* col, int64_t n, int32_t* out2, cudaStream_t st) {
   if (n <= 0) return;
+  note_launch();
   minmax_k<<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(col, n, out2);
 }
 void launch_pack(const PackPlan& pp, int64_t n, uint64_t* key, uint32_t* rowid, cudaStream_t st) {
   if (n <= 0) return;
+  note_launch();
   pack_k<<<grid_for(n, 256), 256, 0, st>>>(pp, n, key, rowid);
 }
 void launch_gather_f32(const float* s, const uint32_t* idx, float* d, int64_t n, cudaStream_t st) {
-  if (n > 0) gather_f32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
+  if (n > 0) {
+    note_launch();
+    gather_f32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
+  }
 }
 void launch_gather_i32(const int32_t* s, const uint32_t* idx, int32_t* d, int64_t n, cudaStream_t st) {
-  if (n > 0) gather_i32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
+  if (n > 0) {
+    note_launch();
+    gather_i32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
+  }
 }
 void launch_iota_i32(int32_t* d, int64_t n, int32_t first, cudaStream_t st) {
-  if (n > 0) iota_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, first);
+  if (n > 0) {
+    note_launch();
+    iota_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, first);
+  }
 }
 void launch_fill_f32(float* d, int64_t n, float v, cudaStream_t st) {
-  if (n > 0) fill_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, v);
+  if (n > 0) {
+    note_launch();
+    fill_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, v);
+  }
 }
 void launch_validate(const float* p, const int32_t* s, int64_t n, int32_t batch, uint32_t* flags, cudaStream_t st) {
-  if (n > 0) validate_k<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, s, n, batch, flags);
+  if (n > 0) {
+    note_launch();
+    validate_k<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, s, n, batch, flags);
+  }
 }
 void launch_heads(const uint64_t* key, int64_t n, uint32_t* flag, cudaStream_t st) {
-  if (n > 0) heads_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, flag);
+  if (n > 0) {
+    note_launch();
+    heads_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, flag);
+  }
 }
 void launch_edb_reduce(const uint64_t* key, const float* p, const int32_t* fid, const uint32_t* pos, int64_t n,
                        int semi, uint64_t* okey, float* op, int32_t* ofid, cudaStream_t st) {
-  if (n > 0) edb_reduce_k<<<grid_for(n, 256), 256, 0, st>>>(key, p, fid, pos, n, semi, okey, op, ofid);
+  if (n > 0) {
+    note_launch();
+    edb_reduce_k<<<grid_for(n, 256), 256, 0, st>>>(key, p, fid, pos, n, semi, okey, op, ofid);
+  }
 }
-void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int semi,
-                       uint64_t* ukey, float* up, uint32_t* uw, cudaStream_t st) {
-  if (n <= 0) return;
-  const int g = grid_for(n, 256);
+void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
+                       uint64_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st) {
+  if (n <= 0 || nu <= 0) return;
+  uint32_t* uend = scratch;            // nu
+  uint32_t* nlong = scratch + nu;      // 1
+  uint32_t* longs = scratch + nu + 1;  // nu
+  cudaMemsetAsync(nlong, 0, 4, st);
+  note_launch();
+  seg_ends_k<<<grid_for(n, 256), 256, 0, st>>>(key, pos, n, uend);
+  const int g = grid_for(nu, 256);
+  note_launch();
   switch (semi) {
-    case S_UNIT: seg_reduce_k<S_UNIT><<<g, 256, 0, st>>>(key, val, pos, n, ukey, up, uw); break;
-    case S_MAXMIN: seg_reduce_k<S_MAXMIN><<<g, 256, 0, st>>>(key, val, pos, n, ukey, up, uw); break;
-    case S_ADDMULT: seg_reduce_k<S_ADDMULT><<<g, 256, 0, st>>>(key, val, pos, n, ukey, up, uw); break;
-    default: seg_reduce_k<S_MAXMULT><<<g, 256, 0, st>>>(key, val, pos, n, ukey, up, uw); break;
+    case S_UNIT: seg_reduce_short_k<S_UNIT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); return;
+    case S_MAXMIN: seg_reduce_short_k<S_MAXMIN><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
+    case S_ADDMULT: seg_reduce_short_k<S_ADDMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
+    default: seg_reduce_short_k<S_MAXMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
+  }
+  const int gl = 148 * 4;
+  note_launch();
+  switch (semi) {
+    case S_MAXMIN: seg_reduce_long_k<S_MAXMIN><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+    case S_ADDMULT: seg_reduce_long_k<S_ADDMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+    default: seg_reduce_long_k<S_MAXMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
   }
 }
 void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* fkey,
                  const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos, cudaStream_t st) {
   (void)uw;
-  if (nu > 0) diff_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, nu, fkey, fp, nf, semi, flags, pos);
+  if (nu > 0) {
+    note_launch();
+    diff_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, nu, fkey, fp, nf, semi, flags, pos);
+  }
 }
 void launch_apply(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* flags,
                   const uint64_t* offs, const int64_t* pos, int semi, float* fp, uint32_t* fw, uint64_t* dkey,
                   float* dp, uint32_t* dw, uint64_t* nkey, float* np_, uint32_t* nw, cudaStream_t st) {
   if (nu > 0)
+    note_launch();
     apply_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, uw, nu, flags, offs, pos, semi, fp, fw, dkey, dp, dw, nkey,
                                                np_, nw);
 }
@@ -308,6 +416,7 @@ void launch_merge(const uint64_t* akey, const float* ap, const uint32_t* aw, int
   const int64_t total = na + nb;
   if (total <= 0) return;
   const int64_t threads = (total + MITEMS - 1) / MITEMS;
+  note_launch();
   merge_k<<<grid_for(threads, 256), 256, 0, st>>>(akey, ap, aw, na, bkey, bp, bw, nb, okey, op, ow);
 }
 

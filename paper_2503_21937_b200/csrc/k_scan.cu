@@ -112,18 +112,24 @@ size_t scan_tmp_bytes(int64_t n) {
 template <typename T>
 void exclusive_scan(const T* in, T* out, int64_t n, T* total_dev, void* tmp, cudaStream_t st) {
   if (n <= 0) {
-    if (total_dev) zero_total_k<T><<<1, 1, 0, st>>>(total_dev);
+    if (total_dev) {
+      note_launch();
+      zero_total_k<T><<<1, 1, 0, st>>>(total_dev);
+    }
     return;
   }
   const int64_t ntiles = (n + TILE - 1) / TILE;
   if (ntiles == 1) {
+    note_launch();
     scan_tile_k<T><<<1, NT, 0, st>>>(in, out, n, nullptr, total_dev);
     return;
   }
   T* partial = reinterpret_cast<T*>(tmp);
   void* rest = reinterpret_cast<char*>(tmp) + align_up((size_t)ntiles * sizeof(T));
+  note_launch();
   scan_reduce_k<T><<<(unsigned)ntiles, NT, 0, st>>>(in, n, partial);
   exclusive_scan<T>(partial, partial, ntiles, nullptr, rest, st);
+  note_launch();
   scan_tile_k<T><<<(unsigned)ntiles, NT, 0, st>>>(in, out, n, partial, total_dev);
 }
 

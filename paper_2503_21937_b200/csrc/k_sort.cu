@@ -104,8 +104,10 @@ int radix_sort_impl(uint64_t* k0, V* v0, uint64_t* k1, V* v1, int64_t n, int bit
     const V* vi = cur ? v1 : v0;
     uint64_t* ko = cur ? k0 : k1;
     V* vo = cur ? v0 : v1;
+    note_launch();
     radix_hist_k<<<(unsigned)ntiles, NT, 0, st>>>(ki, n, shift, hist, ntiles);
     exclusive_scan<uint32_t>(hist, hist, ntiles * 256, nullptr, stmp, st);
+    note_launch();
     radix_scatter_k<V, HASV><<<(unsigned)ntiles, NT, 0, st>>>(ki, vi, ko, vo, n, shift, hist, ntiles);
     cur ^= 1;
   }

@@ -165,6 +165,7 @@ __global__ void dense_sum_k(const uint64_t* __restrict__ key, const uint32_t* __
 void launch_walk(const WalkTables& T, int rel, int64_t n, int pass, const int64_t* offs, int64_t* cnt,
                  int64_t* leaves, int* err, cudaStream_t st) {
   if (n <= 0) return;
+  note_launch();
   walk_k<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(T, rel, n, pass, offs, cnt, leaves, err);
 }
 
@@ -173,6 +174,7 @@ void launch_leaf_heads(const uint64_t* k, int64_t n, uint32_t* flag, cudaStream_
 void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, int64_t nuniq, const float* fact_p,
                   int64_t ntup, const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
                   cudaStream_t st) {
+  note_launch();
   grad_k<<<(unsigned)((ntup + 1 + 127) / 128), 128, 0, st>>>(sorted_tf, pos, nleaf, nuniq, fact_p, ntup, loff, goff,
                                                             gfid, gval, scratch);
 }
@@ -180,24 +182,32 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
 void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,
                    const uint8_t* bits, const int32_t* mins, int32_t* sample, int32_t* cols, cudaStream_t st) {
   if (n > 0)
+    note_launch();
     unpack_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, has_sample, sshift, ncols, shift, bits, mins, sample, cols);
 }
 
 void launch_sample_offsets(const uint64_t* key, int64_t n, int32_t batch, uint8_t sshift, int has_sample,
                            int64_t* off, cudaStream_t st) {
+  note_launch();
   sample_offsets_k<<<(unsigned)((batch + 1 + 255) / 256), 256, 0, st>>>(key, n, batch, sshift, has_sample, off);
 }
 
 void launch_grad_contrib(const int64_t* goff, const int64_t* gfid, const float* gval, const float* upstream,
                          int64_t n, int64_t ng, uint64_t* key, uint32_t* val, cudaStream_t st) {
   (void)ng;
-  if (n > 0) grad_contrib_k<<<grid_for(n, 256), 256, 0, st>>>(goff, gfid, gval, upstream, n, key, val);
+  if (n > 0) {
+    note_launch();
+    grad_contrib_k<<<grid_for(n, 256), 256, 0, st>>>(goff, gfid, gval, upstream, n, key, val);
+  }
 }
 
 void launch_dense_sum(const uint64_t* key, const uint32_t* val, const uint32_t* pos, int64_t n, float* dense,
                       cudaStream_t st) {
   (void)pos;
-  if (n > 0) dense_sum_k<<<grid_for(n, 256), 256, 0, st>>>(key, val, n, dense);
+  if (n > 0) {
+    note_launch();
+    dense_sum_k<<<grid_for(n, 256), 256, 0, st>>>(key, val, n, dense);
+  }
 }
 
 }  // namespace lob

@@ -19,6 +19,9 @@ constexpr int MAXC = 4;    // max comparisons applied in one join step
 
 enum Semi : int { S_UNIT = 0, S_MAXMIN = 1, S_ADDMULT = 2, S_MAXMULT = 3 };
 
+// counts every kernel launch of this library (lobster_kernel_launches)
+void note_launch();
+
 // Copy `bits` bits found at `sshift` of the source word (0 = probe key,
 // 1 = build key) to `dshift` of the destination word.  A variable keeps its
 // domain class (same min and width) in every relation it flows through, so a
@@ -155,8 +158,9 @@ void launch_build_offsets(const uint64_t* key, int64_t n, int free_bits, int64_t
 
 // ---- dedup (A6-A7) and merge/diff (A8-A9) ----
 // U = segmented ⊕ over sorted candidates (vals: u32 p bits or u64 p|w<<32)
-void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int semi,
-                       uint64_t* ukey, float* up, uint32_t* uw, cudaStream_t st);
+// scratch: 2*nu + 1 uint32 words
+void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
+                       uint64_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st);
 // classify U against F: flags (u64: lo = in Δ', hi = new); pos (F index or -1)
 void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu,
                  const uint64_t* fkey, const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos,
