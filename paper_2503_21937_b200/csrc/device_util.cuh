@@ -1,5 +1,7 @@
 // device_util.cuh — small device helpers shared by the kernels of this library.
 #pragma once
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -10,14 +12,30 @@ namespace lob {
 
 __device__ __forceinline__ uint64_t bmask(int bits) { return bits >= 64 ? ~0ull : ((1ull << bits) - 1ull); }
 
+template <typename K>
+__device__ __forceinline__ constexpr K dead() { return ~K(0); }
+
+// Moves are merged host-side (adjacent fields with the same shift delta become
+// one move), so the common case has <= 4 moves: a short predicated loop.
 __device__ __forceinline__ uint64_t apply_moves(const Move* mv, int n, uint64_t a, uint64_t b) {
   uint64_t o = 0;
+  if (n <= 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < n) {
+        const Move m = mv[i];
+        const uint64_t s = m.src ? b : a;
+        o |= ((s >> m.sshift) & ((1ull << m.bits) - 1ull)) << m.dshift;
+      }
+    }
+    return o;
+  }
 #pragma unroll
   for (int i = 0; i < MAXM; ++i) {
     if (i < n) {
       const Move m = mv[i];
       const uint64_t s = m.src ? b : a;
-      o |= ((s >> m.sshift) & bmask(m.bits)) << m.dshift;
+      o |= ((s >> m.sshift) & ((1ull << m.bits) - 1ull)) << m.dshift;
     }
   }
   return o;
@@ -56,6 +74,47 @@ __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 __device__ __forceinline__ float otimes(int semi, float a, float b) {
   if (semi == S_MAXMIN) return a < b ? a : b;
   return __fmul_rn(a, b);
+}
+
+// Direct ⊕ of one live candidate into a dense store (see kernels.cuh Direct).
+// Called by the threads that hold a live candidate (any divergence).  With
+// `aggregate` (narrow heads, e.g. endpoints_connected() sends ~1M candidates
+// to each of 64 slots) lanes of a warp aiming at the same slot are pre-reduced
+// (match + shuffle tree) so one atomic per (warp, slot) reaches L2.
+__device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, float p, uint32_t w, uint32_t* dirty,
+                                             int aggregate) {
+  namespace cg = cooperative_groups;
+  bool app = false;
+  if (semi == S_UNIT) {
+    const uint32_t bit = 1u << (slot & 31u);
+    const uint32_t old = atomicOr(reinterpret_cast<uint32_t*>(f) + (slot >> 5), bit);
+    app = !(old & bit);
+  } else if (semi == S_MAXMIN) {
+    uint32_t v = (f2u(p) + 1u) << 1;
+    bool lead = true;
+    if (aggregate) {
+      cg::coalesced_group part = cg::labeled_partition(cg::coalesced_threads(), (int)slot);
+      v = cg::reduce(part, v, cg::greater<uint32_t>());
+      lead = part.thread_rank() == 0;
+    }
+    if (lead) {
+      const uint32_t old = atomicMax(reinterpret_cast<uint32_t*>(f) + slot, v);
+      app = old < v && (old == 0u || (old & 1u));
+    }
+  } else {
+    unsigned long long v = ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
+    bool lead = true;
+    if (aggregate) {
+      cg::coalesced_group part = cg::labeled_partition(cg::coalesced_threads(), (int)slot);
+      v = cg::reduce(part, v, cg::greater<unsigned long long>());
+      lead = part.thread_rank() == 0;
+    }
+    if (lead) {
+      const unsigned long long old = atomicMax(reinterpret_cast<unsigned long long*>(f) + slot, v);
+      app = old < v && (old == 0ull || ((old >> 32) & 1ull));
+    }
+  }
+  if (app) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
 }
 
 inline int grid_for(int64_t n, int threads, int cap = 148 * 32) {

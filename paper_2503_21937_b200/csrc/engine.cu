@@ -37,6 +37,29 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static int bits_for(uint64_t range) { return range == 0 ? 0 : 64 - __builtin_clzll(range); }
 
+// Merge bit moves that are adjacent in both source and destination with the
+// same source word (e.g. (sample, x) kept together from probe to head): fewer
+// moves per output key in the join kernels.
+static void merge_moves(Move* mv, int& n) {
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int a = 0; a < n && !changed; ++a)
+      for (int b = 0; b < n && !changed; ++b) {
+        if (a == b || mv[a].src != mv[b].src) continue;
+        if (mv[a].sshift == mv[b].sshift + mv[b].bits && mv[a].dshift == mv[b].dshift + mv[b].bits &&
+            mv[a].bits + mv[b].bits <= 63) {
+          mv[b].bits = (uint8_t)(mv[a].bits + mv[b].bits);
+          mv[a] = mv[n - 1];
+          --n;
+          changed = true;
+        }
+      }
+  }
+  for (int i = 0; i < n;)  // zero-width moves contribute nothing
+    if (mv[i].bits == 0) mv[i] = mv[--n]; else ++i;
+}
+
 constexpr int MAXARITY = 8;
 
 struct Layout {
@@ -71,6 +94,16 @@ struct RelState {
   DBuf<uint32_t> ow;
   int64_t no = 0;
   bool need_old = false;
+  bool build_local = false;  // read as B^new / B^old by a rule with >= 2 local atoms
+  // dense direct-mapped store (NEXT-1) while the relation's stratum runs;
+  // keys of Δ / C / U are then u32 (packed key < 2^31)
+  bool dense = false;
+  bool direct = false;  // dense + idempotent ⊕ fused into the join write (kernels.cuh Direct)
+  int64_t nslots = 0;
+  DevMem dirf;          // direct store words
+  DBuf<uint32_t> dirty;  // bitmap of the slots improved this round
+  DBuf<float> dfp;
+  DBuf<uint32_t> dfw, dfbits, dkey32, ckey32, ckey32b;
   DBuf<uint64_t> ckey, ckey2, cv64, cv64b;
   DBuf<uint32_t> cv32, cv32b;
   int64_t nc = 0;
@@ -92,7 +125,10 @@ struct RelState {
   void bind(cudaStream_t st) {
     for (auto* b : {&key, &key2, &dkey, &okey, &ckey, &ckey2, &cv64, &cv64b}) b->bind(st);
     for (auto* b : {&p, &p2, &dp, &op, &gval}) b->bind(st);
-    for (auto* b : {&w, &w2, &dw, &ow, &cv32, &cv32b}) b->bind(st);
+    for (auto* b : {&w, &w2, &dw, &ow, &cv32, &cv32b, &dfw, &dfbits, &dkey32, &ckey32, &ckey32b, &dirty})
+      b->bind(st);
+    dfp.bind(st);
+    dirf.bind(st);
     for (auto* b : {&fid, &o_sid, &o_cols}) b->bind(st);
     for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
     for (auto& c : in.cols) c.bind(st);
@@ -114,13 +150,15 @@ struct Index {
   const int64_t* offp = nullptr;
   int64_t nprefix = 0;
   int free_bits = 0, prefix_bits = 0;
+  int64_t maxdeg = -1;  // max rows per prefix (static CSR indexes), -1 unknown
   bool has_sample = false;
   int sshift = 0, sbits = 0;
   std::vector<int> col_shift, col_bits;
 };
 
 struct Table {  // probe side of a join step
-  const uint64_t* key = nullptr;
+  const void* key = nullptr;
+  bool k32 = false;  // u32 keys (Δ of a dense relation)
   int64_t n = 0;
   std::vector<const float*> tags;
   std::vector<int> tag_atom;
@@ -149,7 +187,11 @@ struct Ctx {
   std::vector<std::vector<int>> wshift, wbits;  // per rule, per nonhead var
   DBuf<float> fact_p;
   lobster_run_stats stats{};
+  unsigned long long* d_ncand = nullptr;  // device counter of fused-join candidates
+  bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
+  bool force_sorted = getenv("LOBSTER_SORTED_STORE") != nullptr;      // A/B: merge-based store
+  bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
   int64_t num_facts_db = 0;
   // timing
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -196,6 +238,7 @@ struct Ctx {
     arena.free_all();
     fact_p.release();
     if (st) cudaStreamSynchronize(st);
+    if (d_ncand) cudaFree(d_ncand);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (hbuf) cudaFreeHost(hbuf);
   }
@@ -250,6 +293,9 @@ struct Ctx {
           seen++;
         }
       }
+      if (seen >= 2)
+        for (auto& a : R.body)
+          if (!prog.rels[a.rel].input && prog.rels[a.rel].stratum == s) rels[a.rel]->build_local = true;
     }
     rule_bits.assign(prog.rels.size(), 0);
     for (size_t r = 0; r < prog.rels.size(); ++r)
@@ -433,7 +479,7 @@ struct Ctx {
       uint32_t* r1 = arena.get<uint32_t>(n);
       void* stmp = arena.alloc(sort_tmp_bytes(n));
       launch_pack(pp, n, k0, r0, st);
-      int which = radix_sort<uint32_t>(k0, r0, k1, r1, n, S.L.total, stmp, st);
+      int which = radix_sort(k0, r0, k1, r1, n, S.L.total, stmp, st);
       uint64_t* ks = which ? k1 : k0;
       uint32_t* rs = which ? r1 : r0;
       float* ps = arena.get<float>(n);
@@ -522,8 +568,8 @@ struct Ctx {
       if (p) cuda_check(cudaMemcpyAsync(p0, p, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "index p");
       void* stmp = arena.alloc(sort_tmp_bytes(n));
       int which;
-      if (p) which = radix_sort<uint32_t>(k0, (uint32_t*)p0, k1, (uint32_t*)p1, n, L.total, stmp, st);
-      else which = radix_sort<void>(k0, nullptr, k1, nullptr, n, L.total, stmp, st);
+      if (p) which = radix_sort(k0, (uint32_t*)p0, k1, (uint32_t*)p1, n, L.total, stmp, st);
+      else which = radix_sort<uint64_t, void>(k0, nullptr, k1, nullptr, n, L.total, stmp, st);
       ix.key = which ? k1 : k0;
       ix.p = p ? (which ? p1 : p0) : nullptr;
       kcheck("index build");
@@ -542,6 +588,12 @@ struct Ctx {
       launch_build_offsets(ix.key, n, ix.free_bits, ix.nprefix, off, st);
       kcheck("offsets");
       ix.offp = off;
+      if (persistent) {  // fan-out bound: selects the row-centric fused join
+        unsigned long long* d = arena.get<unsigned long long>(1);
+        cuda_check(cudaMemsetAsync(d, 0, 8, st), "memset");
+        launch_max_degree(off, ix.nprefix, d, st);
+        ix.maxdeg = (int64_t)read_dev(d);
+      }
     }
   }
 
@@ -560,17 +612,20 @@ struct Ctx {
 
   // ------------------------------------------------------------ rule eval
   struct VerData {
-    const uint64_t* key;
+    const void* key;
     const float* p;
     int64_t n;
+    bool k32;
   };
   VerData version_data(int rel, Version v) {
     RelState& S = *rels[rel];
     const bool tag = semi != S_UNIT;
     switch (v) {
-      case V_DELTA: return {S.dkey.ptr(), tag ? S.dp.ptr() : nullptr, S.nd};
-      case V_OLD: return {S.okey.ptr(), tag ? S.op.ptr() : nullptr, S.no};
-      default: return {S.key.ptr(), tag ? S.p.ptr() : nullptr, S.n};
+      case V_DELTA:
+        if (S.dense) return {S.dkey32.ptr(), tag ? S.dp.ptr() : nullptr, S.nd, true};
+        return {S.dkey.ptr(), tag ? S.dp.ptr() : nullptr, S.nd, false};
+      case V_OLD: return {S.okey.ptr(), tag ? S.op.ptr() : nullptr, S.no, false};
+      default: return {S.key.ptr(), tag ? S.p.ptr() : nullptr, S.n, false};
     }
   }
 
@@ -615,6 +670,7 @@ struct Ctx {
     VerData d0 = version_data(A0.rel, ver[start]);
     if (d0.n == 0) return;
     T.key = d0.key;
+    T.k32 = d0.k32;
     T.n = d0.n;
     if (semi != S_UNIT) { T.tags.push_back(d0.p); T.tag_atom.push_back(start); }
     T.has_sample = L0.has_sample;
@@ -644,6 +700,8 @@ struct Ctx {
     if (na == 1) {  // projection
       ProjectPlan pp{};
       pp.key = T.key;
+      pp.pk32 = T.k32;
+      pp.ok32 = H.dense;
       pp.tag = semi != S_UNIT ? T.tags[0] : nullptr;
       pp.n = T.n;
       for (auto& c : pending_start) pp.cmp[pp.ncmp++] = c;
@@ -659,10 +717,16 @@ struct Ctx {
       head_moves(R, H, T, nullptr, pp.om, pp.nom, pp.cout);
       pp.semi = semi;
       witness_moves(R, T, nullptr, pp.wm, pp.nwm, pp.wconst);
-      reserve_candidates(H, H.nc + T.n);
-      pp.okey = H.ckey.ptr() + H.nc;
-      pp.oval32 = H.cv32.ptr() ? H.cv32.ptr() + H.nc : nullptr;
-      pp.oval64 = H.cv64.ptr() ? H.cv64.ptr() + H.nc : nullptr;
+      if (H.direct) {
+        direct_target(H, pp.direct, pp.fdir, pp.dirty, pp.aggregate);
+      } else {
+        reserve_candidates(H, H.nc + T.n);
+        pp.okey = cand_key(H);
+        pp.oval32 = H.cv32.ptr() ? H.cv32.ptr() + H.nc : nullptr;
+        pp.oval64 = H.cv64.ptr() ? H.cv64.ptr() + H.nc : nullptr;
+      }
+      merge_moves(pp.om, pp.nom);
+      merge_moves(pp.wm, pp.nwm);
       launch_project(pp, st);
       kcheck("project");
       H.nc += T.n;
@@ -690,12 +754,13 @@ struct Ctx {
         ix = static_index(A.rel, iorder, nbound);
       } else {
         VerData vd = version_data(A.rel, ver[ai]);
-        build_index(local_ix, L, iorder, nbound, vd.key, vd.p, vd.n, false, false);
+        build_index(local_ix, L, iorder, nbound, (const uint64_t*)vd.key, vd.p, vd.n, false, false);
         ix = &local_ix;
       }
       if (ix->n == 0) return;
       JoinPlan jp{};
       jp.pkey = T.key;
+      jp.pk32 = T.k32;
       jp.np = T.n;
       jp.npt = (int)T.tags.size();
       for (int k = 0; k < jp.npt; ++k) jp.ptag[k] = T.tags[k];
@@ -752,6 +817,28 @@ struct Ctx {
       jp.semi = semi;
       const bool last = s == na - 1;
       jp.final_step = last ? 1 : 0;
+      // fused row-centric join + direct ⊕: bounded fan-out, one probe tag
+      if (last && H.direct && (H.L.total - H.L.sbits) > 8 && T.tags.size() <= 1 && na == 2 && ix->offp &&
+          ix->maxdeg >= 0 && ix->maxdeg <= 8 && jp.nfeq == 0 && !force_slot_join) {
+        head_moves(R, H, T, &nshift, jp.om, jp.nom, jp.cout, &nbits);
+        witness_moves(R, T, &nshift, jp.wm, jp.nwm, jp.wconst, &nbits);
+        if (semi != S_UNIT) {
+          jp.ntag = 2;
+          jp.tag_order[0] = (int8_t)(start < ai ? 0 : 1);
+          jp.tag_order[1] = (int8_t)(start < ai ? 1 : 0);
+        }
+        direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate);
+        merge_moves(jp.prem, jp.nprem);
+        merge_moves(jp.om, jp.nom);
+        merge_moves(jp.wm, jp.nwm);
+        {
+          Phase ph(this, 0);
+          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand, st);
+          kcheck("join rows direct");
+        }
+        H.nc += T.n;  // candidates counted on the device (d_ncand)
+        return;
+      }
       // count + scan (A3-A4)
       int64_t* count = arena.get<int64_t>(T.n);
       int64_t* start_ = arena.get<int64_t>(T.n);
@@ -759,6 +846,7 @@ struct Ctx {
       int64_t* tot = arena.get<int64_t>(1);
       {
         Phase ph(this, 0);
+        merge_moves(jp.prem, jp.nprem);
         launch_join_count(jp, count, start_, st);
         exclusive_scan<int64_t>(count, offs, T.n, tot, arena.alloc(scan_tmp_bytes<int64_t>(T.n)), st);
         kcheck("join count");
@@ -780,10 +868,15 @@ struct Ctx {
             jp.tag_order[k] = (int8_t)idx;
           }
         }
-        reserve_candidates(H, H.nc + total);
-        jp.okey = H.ckey.ptr() + H.nc;
-        jp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
-        jp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
+        if (H.direct) {
+          direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate);
+        } else {
+          reserve_candidates(H, H.nc + total);
+          jp.ok32 = H.dense;
+          jp.okey = cand_key(H);
+          jp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
+          jp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
+        }
       } else {
         // intermediate layout: sample + all bound vars (var id order)
         N.has_sample = true;
@@ -808,8 +901,10 @@ struct Ctx {
           else jp.om[jp.nom++] = Move{1, (uint8_t)nshift[v], (uint8_t)nbits[v], (uint8_t)N.vshift[v]};
         }
         N.key = arena.get<uint64_t>(total);
+        N.k32 = false;
         N.n = total;
-        jp.okey = const_cast<uint64_t*>(N.key);
+        jp.okey = const_cast<void*>(N.key);
+        jp.ok32 = 0;
         if (semi != S_UNIT) {
           for (int k = 0; k <= jp.npt; ++k) {
             float* t = arena.get<float>(total);
@@ -822,6 +917,8 @@ struct Ctx {
       }
       {
         Phase ph(this, 0);
+        merge_moves(jp.om, jp.nom);
+        merge_moves(jp.wm, jp.nwm);
         launch_join_write(jp, offs, start_, total, st);
         kcheck("join write");
       }
@@ -872,16 +969,205 @@ struct Ctx {
     }
   }
 
+  void* cand_key(RelState& H) {
+    return H.dense ? (void*)(H.ckey32.ptr() + H.nc) : (void*)(H.ckey.ptr() + H.nc);
+  }
+
   void reserve_candidates(RelState& H, int64_t n) {
-    H.ckey.reserve(n, H.nc);
+    if (H.dense) H.ckey32.reserve(n, H.nc);
+    else H.ckey.reserve(n, H.nc);
     if (semi == S_MAXMIN || semi == S_ADDMULT) H.cv32.reserve(n, H.nc);
     if (semi == S_MAXMULT) H.cv64.reserve(n, H.nc);
   }
 
   // -------------------------------------------------- per-relation epilogue
-  // sort + segmented ⊕ (A6-A7), diff + apply + merge (A8); returns |Δ'|
+  // Dense store: u32 keys; sort + segmented ⊕ (A6-A7), then one in-place
+  // classify/apply pass over U against the direct-mapped F and a compaction
+  // of Δ' (A8) — O(|C|) per round, no O(|F|) merge.
+  int64_t settle_dense(RelState& S) {
+    const int64_t nc = S.nc;
+    S.nc = 0;
+    if (nc == 0) { S.nd = 0; return 0; }
+    const int tb = S.L.total + 1;  // +1 bit: dead key (all ones) sorts last
+    S.ckey32b.reserve(nc);
+    uint32_t* ks;
+    const void* vs;
+    {
+      Phase ph(this, 1);
+      void* stmp = arena.alloc(sort_tmp_bytes(nc));
+      int which;
+      if (semi == S_MAXMULT) {
+        S.cv64b.reserve(nc);
+        which = radix_sort(S.ckey32.ptr(), S.cv64.ptr(), S.ckey32b.ptr(), S.cv64b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv64b.ptr() : S.cv64.ptr();
+      } else if (semi == S_UNIT) {
+        which = radix_sort<uint32_t, void>(S.ckey32.ptr(), nullptr, S.ckey32b.ptr(), nullptr, nc, tb, stmp, st);
+        vs = nullptr;
+      } else {
+        S.cv32b.reserve(nc);
+        which = radix_sort(S.ckey32.ptr(), S.cv32.ptr(), S.ckey32b.ptr(), S.cv32b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv32b.ptr() : S.cv32.ptr();
+      }
+      ks = which ? S.ckey32b.ptr() : S.ckey32.ptr();
+      kcheck("sort");
+    }
+    uint32_t* fl = arena.get<uint32_t>(nc);
+    uint32_t* pos = arena.get<uint32_t>(nc);
+    uint32_t* tot = arena.get<uint32_t>(1);
+    {
+      Phase ph(this, 2);
+      launch_heads(ks, nc, fl, st);
+      exclusive_scan<uint32_t>(fl, pos, nc, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nc)), st);
+      kcheck("heads");
+    }
+    const int64_t nu = read_dev(tot);
+    uint32_t* ukey = arena.get<uint32_t>(nu);
+    float* up = semi != S_UNIT ? arena.get<float>(nu) : nullptr;
+    uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
+    {
+      Phase ph(this, 2);
+      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 1), st);
+      kcheck("seg reduce");
+    }
+    uint64_t* flags = arena.get<uint64_t>(nu);
+    uint64_t* offs = arena.get<uint64_t>(nu);
+    uint64_t* t2 = arena.get<uint64_t>(1);
+    {
+      Phase ph(this, 3);
+      launch_dense_diff(ukey, up, uw, nu, semi, S.dfp.ptr(), S.dfw.ptr(), S.dfbits.ptr(), flags, st);
+      exclusive_scan<uint64_t>(flags, offs, nu, t2, arena.alloc(scan_tmp_bytes<uint64_t>(nu)), st);
+      kcheck("dense diff");
+    }
+    const uint64_t tt = read_dev(t2);
+    const int64_t nd = (int64_t)(tt & 0xffffffffull), nnew = (int64_t)(tt >> 32);
+    stats.bytes_algorithmic += bytes_round(nc, nu, nd);
+    S.n += nnew;
+    S.nd = nd;
+    if (nd == 0) return 0;
+    Phase ph(this, 3);
+    S.dkey32.reserve(nd);
+    if (semi != S_UNIT) S.dp.reserve(nd);
+    if (semi == S_MAXMULT) S.dw.reserve(nd);
+    launch_dense_delta(ukey, up, uw, nu, flags, offs, semi, S.dkey32.ptr(), semi != S_UNIT ? S.dp.ptr() : nullptr,
+                       semi == S_MAXMULT ? S.dw.ptr() : nullptr, st);
+    kcheck("dense delta");
+    return nd;
+  }
+
+  // dense F -> sorted list (key, p, w) for later strata, outputs and the walk
+  void dense_to_sorted(RelState& S) {
+    const int64_t ns = S.nslots;
+    uint32_t* fl = arena.get<uint32_t>(ns);
+    uint32_t* pos = arena.get<uint32_t>(ns);
+    uint32_t* tot = arena.get<uint32_t>(1);
+    if (S.direct) launch_direct_present(S.dirf.get(), ns, semi, fl, st);
+    else launch_dense_present(S.dfp.ptr(), S.dfbits.ptr(), ns, semi, fl, st);
+    exclusive_scan<uint32_t>(fl, pos, ns, tot, arena.alloc(scan_tmp_bytes<uint32_t>(ns)), st);
+    kcheck("dense present");
+    const int64_t n = read_dev(tot);
+    S.key.reserve(n);
+    if (semi != S_UNIT) S.p.reserve(n);
+    if (semi == S_MAXMULT) S.w.reserve(n);
+    if (S.direct)
+      launch_direct_compact(S.dirf.get(), pos, ns, semi, S.key.ptr(), semi != S_UNIT ? S.p.ptr() : nullptr,
+                            semi == S_MAXMULT ? S.w.ptr() : nullptr, st);
+    else
+      launch_dense_compact(S.dfp.ptr(), S.dfw.ptr(), S.dfbits.ptr(), pos, ns, semi, S.key.ptr(),
+                           semi != S_UNIT ? S.p.ptr() : nullptr, semi == S_MAXMULT ? S.w.ptr() : nullptr, st);
+    kcheck("dense compact");
+    S.n = n;
+  }
+
+  // Store choice for a local relation: direct-mapped
+  // when its packed key fits 30 bits, it is only ever probed through Δ (no
+  // B^new / B^old index is needed) and the slot array fits half of free HBM.
+  // direct ⊕ target for `n` more candidates of head H this round: dlist must
+  // hold every slot improved so far (<= candidates so far) plus n.
+  void direct_target(RelState& H, int& direct, void*& f, uint32_t*& dirty, int& aggregate) {
+    direct = 1;
+    aggregate = (H.L.total - H.L.sbits) <= 8 ? 1 : 0;  // narrow head: many candidates per slot
+    f = H.dirf.get();
+    dirty = H.dirty.ptr();
+  }
+
+  void choose_store(RelState& S) {
+    S.dense = false;
+    S.direct = false;
+    if (S.build_local || S.L.total > 30 || force_sorted) return;
+    if (semi != S_ADDMULT && !force_sort_dedup) {  // idempotent ⊕: fused direct store
+      const int64_t ns = (int64_t)1 << S.L.total;
+      const size_t bytes = semi == S_UNIT ? (size_t)((ns + 31) / 32) * 4 : (size_t)ns * (semi == S_MAXMULT ? 8 : 4);
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if ((double)bytes > 0.5 * (double)fr) return;
+      S.dense = S.direct = true;
+      S.nslots = ns;
+      S.dirf.reserve(bytes);
+      launch_direct_fill(S.dirf.get(), ns, semi, st);
+      S.dirty.reserve((ns + 31) / 32);
+      cuda_check(cudaMemsetAsync(S.dirty.ptr(), 0, (size_t)((ns + 31) / 32) * 4, st), "memset");
+      return;
+    }
+    const int64_t ns = (int64_t)1 << S.L.total;
+    const double bytes = semi == S_UNIT ? ns / 8.0 : (double)ns * (semi == S_MAXMULT ? 8 : 4);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    if (bytes > 0.5 * (double)fr) return;
+    S.dense = true;
+    S.nslots = ns;
+    if (semi == S_UNIT) {
+      S.dfbits.reserve((ns + 31) / 32);
+    } else {
+      S.dfp.reserve(ns);
+      if (semi == S_MAXMULT) S.dfw.reserve(ns);
+    }
+    launch_dense_fill(S.dfp.ptr(), S.dfbits.ptr(), ns, semi, st);
+    kcheck("dense fill");
+  }
+
+  // Sorted store: sort + segmented ⊕ (A6-A7), diff + apply + merge (A8); returns |Δ'|
+  // Direct store: the join already ⊕-ed every candidate into F; Δ' = the
+  // improved slots with their round-final tags (re-settled for the next round).
+  int64_t settle_direct(RelState& S) {
+    const int64_t nc = S.nc;
+    S.nc = 0;
+    if (nc == 0) { S.nd = 0; return 0; }
+    const int64_t nw = (S.nslots + 31) / 32;
+    uint32_t* cnt = arena.get<uint32_t>(nw);
+    uint32_t* pos = arena.get<uint32_t>(nw);
+    uint32_t* tot = arena.get<uint32_t>(1);
+    {
+      Phase ph(this, 3);
+      launch_direct_dirty_count(S.dirty.ptr(), nw, cnt, st);
+      exclusive_scan<uint32_t>(cnt, pos, nw, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nw)), st);
+      kcheck("dirty count");
+    }
+    const int64_t nd = read_dev(tot);
+    stats.bytes_algorithmic += bytes_round_direct(nc, nd);
+    S.nd = nd;
+    if (nd == 0) return 0;
+    Phase ph(this, 3);
+    S.dkey32.reserve(nd);
+    if (semi != S_UNIT) S.dp.reserve(nd);
+    if (semi == S_MAXMULT) S.dw.reserve(nd);
+    // Δ' in slot order (sorted, deterministic); dirty bits cleared, slots re-settled
+    launch_direct_dirty_extract(S.dirf.get(), S.dirty.ptr(), pos, nw, semi, S.dkey32.ptr(),
+                                semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr, st);
+    kcheck("direct extract");
+    return nd;
+  }
+
+  int64_t bytes_round_direct(int64_t nc, int64_t nd) const {
+    // probe read is counted by the caller's Δ (|Δ| r_Δ of the previous round's Δ'):
+    // one slot read-modify-write per candidate + Δ' write + Δ re-read next round
+    const int64_t slot = semi == S_MAXMULT ? 8 : 4;
+    const int64_t rD = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
+    return nc * slot + nd * (slot + 2 * rD);
+  }
+
   int64_t settle(int r) {
     RelState& S = *rels[r];
+    if (S.direct) return settle_direct(S);
     if (S.need_old) {  // OLD = F before this round's update (B^old of the next round)
       S.okey.reserve(S.n);
       if (S.n) cuda_check(cudaMemcpyAsync(S.okey.ptr(), S.key.ptr(), S.n * 8, cudaMemcpyDeviceToDevice, st), "old");
@@ -891,6 +1177,7 @@ struct Ctx {
       }
       S.no = S.n;
     }
+    if (S.dense) return settle_dense(S);
     const int64_t nc = S.nc;
     S.nc = 0;
     if (nc == 0) { S.nd = 0; return 0; }
@@ -904,14 +1191,14 @@ struct Ctx {
       int which;
       if (semi == S_MAXMULT) {
         S.cv64b.reserve(nc);
-        which = radix_sort<uint64_t>(S.ckey.ptr(), S.cv64.ptr(), S.ckey2.ptr(), S.cv64b.ptr(), nc, tb, stmp, st);
+        which = radix_sort(S.ckey.ptr(), S.cv64.ptr(), S.ckey2.ptr(), S.cv64b.ptr(), nc, tb, stmp, st);
         vs = which ? S.cv64b.ptr() : S.cv64.ptr();
       } else if (semi == S_UNIT) {
-        which = radix_sort<void>(S.ckey.ptr(), nullptr, S.ckey2.ptr(), nullptr, nc, tb, stmp, st);
+        which = radix_sort<uint64_t, void>(S.ckey.ptr(), nullptr, S.ckey2.ptr(), nullptr, nc, tb, stmp, st);
         vs = nullptr;
       } else {
         S.cv32b.reserve(nc);
-        which = radix_sort<uint32_t>(S.ckey.ptr(), S.cv32.ptr(), S.ckey2.ptr(), S.cv32b.ptr(), nc, tb, stmp, st);
+        which = radix_sort(S.ckey.ptr(), S.cv32.ptr(), S.ckey2.ptr(), S.cv32b.ptr(), nc, tb, stmp, st);
         vs = which ? S.cv32b.ptr() : S.cv32.ptr();
       }
       ks = which ? S.ckey2.ptr() : S.ckey.ptr();
@@ -989,6 +1276,8 @@ struct Ctx {
     if (!loaded) throw Failure(LOBSTER_E_STATE, "run before program_load");
     if (sticky) throw Failure(LOBSTER_E_CUDA, "context is in a failed state");
     stats = lobster_run_stats{};
+    if (!d_ncand) cuda_check(cudaMalloc(&d_ncand, 8), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(d_ncand, 0, 8, st), "memset");
     ev.clear();
     ev_used = 0;
     cudaEvent_t t0 = get_event(), t1;
@@ -1010,6 +1299,7 @@ struct Ctx {
         S.key.reserve(1);
         if (semi != S_UNIT) S.p.reserve(1);
         if (semi == S_MAXMULT) S.w.reserve(1);
+        choose_store(S);
       }
       int rounds = 0;
       bool first = true;
@@ -1049,12 +1339,15 @@ struct Ctx {
         for (int r : strat) changed += settle(r);
         if (changed == 0) break;
       }
+      for (int r : strat)
+        if (rels[r]->dense) dense_to_sorted(*rels[r]);
       stats.rounds_total += rounds;
       stats.strata++;
       if (round_cap_hit) break;
     }
     for (size_t r = 0; r < prog.rels.size(); ++r)
       if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
+    stats.candidates += (int64_t)read_dev(d_ncand);
     if (!round_cap_hit && semi == S_MAXMULT) {
       Phase ph(this, 4);
       gradients();
@@ -1176,7 +1469,7 @@ struct Ctx {
       // leaf keys: tuple << 32 | fact, sorted -> unique (tuple, fact) runs
       tag_leaves(k0, loff, n, nleaf);
       const int tbits = 32 + bits_for((uint64_t)n);
-      int which = radix_sort<void>(k0, nullptr, k1, nullptr, nleaf, tbits, arena.alloc(sort_tmp_bytes(nleaf)), st);
+      int which = radix_sort<uint64_t, void>(k0, nullptr, k1, nullptr, nleaf, tbits, arena.alloc(sort_tmp_bytes(nleaf)), st);
       uint64_t* ks = which ? k1 : k0;
       uint32_t* fl = arena.get<uint32_t>(nleaf);
       uint32_t* pos = arena.get<uint32_t>(nleaf);
@@ -1298,7 +1591,7 @@ struct Ctx {
       uint32_t* v0 = arena.get<uint32_t>(ng);
       uint32_t* v1 = arena.get<uint32_t>(ng);
       launch_grad_contrib(S.goff.ptr(), S.gfid.ptr(), S.gval.ptr(), upstream, S.n, ng, k0, v0, st);
-      int which = radix_sort<uint32_t>(k0, v0, k1, v1, ng, bits_for((uint64_t)nf), arena.alloc(sort_tmp_bytes(ng)), st);
+      int which = radix_sort(k0, v0, k1, v1, ng, bits_for((uint64_t)nf), arena.alloc(sort_tmp_bytes(ng)), st);
       launch_dense_sum(which ? k1 : k0, which ? v1 : v0, nullptr, ng, grad_facts, st);
       kcheck("backward");
     }

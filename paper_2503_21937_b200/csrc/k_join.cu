@@ -6,42 +6,40 @@
 // Build sides are sorted index keys [prefix | free fields] (static EDB indexes
 // are built once per run, §4.2) with optional CSR offsets
 // over the dense prefix domain; otherwise binary search.  The write stage is
-// balanced over OUTPUT slots (skew-proof for power-law hubs): each slot finds
-// its probe row by binary search on the scanned offsets.
+// balanced over OUTPUT slots (skew-proof for power-law hubs): each CTA owns a
+// tile of output slots, finds its probe-row range once, stages those offsets
+// in shared memory and resolves each slot's row there.
+//
+// Probe / output keys are u32 or u64 (template PK / OK): relations whose
+// packed key fits 31 bits move half the key bytes.
 #include "device_util.cuh"
 
 namespace lob {
 namespace {
 
 __device__ __forceinline__ uint64_t probe_prefix(const JoinPlan& jp, uint64_t pk) {
-  uint64_t pre = jp.cprefix;
-#pragma unroll
-  for (int i = 0; i < MAXM; ++i) {
-    if (i < jp.nprem) {
-      const Move m = jp.prem[i];
-      pre |= ((pk >> m.sshift) & bmask(m.bits)) << m.dshift;
-    }
-  }
-  return pre;
+  return jp.cprefix | apply_moves(jp.prem, jp.nprem, pk, 0);
 }
 
+template <typename PK>
 __global__ void __launch_bounds__(256) join_count_k(const JoinPlan jp, int64_t* __restrict__ count,
                                                     int64_t* __restrict__ start) {
+  const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < jp.np;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t pk = jp.pkey[i];
+    const PK pk = pkey[i];
     int64_t lo = 0, hi = 0;
-    if (pk != KEY_DEAD) {
-      const uint64_t pre = probe_prefix(jp, pk);
+    if (pk != dead<PK>()) {
+      const uint64_t pre = probe_prefix(jp, (uint64_t)pk);
       if (jp.boff) {
         if (pre < (uint64_t)jp.nprefix) {
           lo = jp.boff[pre];
           hi = jp.boff[pre + 1];
         }
       } else {
-        const uint64_t a = pre << jp.free_bits;
+        const uint64_t a = pre << jp.free_bits;  // prefix + free bits <= 63: no overflow
         const uint64_t b = (pre + 1) << jp.free_bits;
-        lo = lower_bound_u64(jp.bkey, jp.nb, a);  // prefix + free bits <= 63: no overflow
+        lo = lower_bound_u64(jp.bkey, jp.nb, a);
         hi = lower_bound_u64(jp.bkey, jp.nb, b);
       }
     }
@@ -59,14 +57,11 @@ __device__ __forceinline__ float tag_at(const JoinPlan& jp, int idx, int64_t row
   return t;
 }
 
-// Output-slot tiles: CTA b owns slots [b*WT, (b+1)*WT).  Thread 0 finds the
-// tile's probe-row range by binary search on the scanned offsets; when the
-// range is small its offsets are staged in shared memory and each slot's row
-// is found there (load-balanced expansion, skew-proof).
-constexpr int WT = 2048;
-constexpr int WROWS = 2048;
+constexpr int WT = 2048;    // output slots per CTA (8 per thread)
+constexpr int WROWS = 2048; // probe-row offsets staged in shared memory
+constexpr int SPT = WT / 256;
 
-__device__ __forceinline__ int64_t smem_row(const int64_t* s, int n, int64_t o) {
+__device__ __forceinline__ int smem_row(const int64_t* s, int n, int64_t o) {
   int lo = 0, hi = n;  // largest i with s[i] <= o
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
@@ -75,10 +70,25 @@ __device__ __forceinline__ int64_t smem_row(const int64_t* s, int n, int64_t o) 
   return lo - 1;
 }
 
+// ⊗ in body order over T = [ptag[0..npt-1], btag] (reading 9).  Fast path:
+// one probe tag followed by the build tag (every linear TC-shaped rule).
+__device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int64_t row, int64_t j) {
+  if (jp.npt == 1 && jp.ntag == 2) {
+    const float a = jp.ptag[0][row], b = jp.btag[j];
+    return jp.tag_order[0] == 0 ? otimes(jp.semi, a, b) : otimes(jp.semi, b, a);
+  }
+  float t = tag_at(jp, jp.tag_order[0], row, j);
+  for (int k = 1; k < jp.ntag; ++k) t = otimes(jp.semi, t, tag_at(jp, jp.tag_order[k], row, j));
+  return t;
+}
+
+template <typename PK, typename OK>
 __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int64_t* __restrict__ offs,
                                                     const int64_t* __restrict__ start, int64_t total) {
   __shared__ int64_t soff[WROWS];
   __shared__ int64_t r0s, r1s;
+  const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
+  OK* __restrict__ okey = reinterpret_cast<OK*>(jp.okey);
   const int64_t o0 = (int64_t)blockIdx.x * WT;
   if (o0 >= total) return;
   const int64_t o1 = (o0 + WT < total ? o0 + WT : total) - 1;
@@ -93,10 +103,18 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
   if (staged)
     for (int i = threadIdx.x; i < nrows; i += blockDim.x) soff[i] = offs[r0 + i];
   __syncthreads();
-  for (int64_t o = o0 + threadIdx.x; o <= o1; o += blockDim.x) {
-    int64_t row;
+  // phase 1: resolve every slot of this thread (independent loads in flight)
+  int64_t rowv[SPT], jv[SPT];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t o = o0 + threadIdx.x + k * 256;
+    rowv[k] = -1;
+    if (o > o1) continue;
+    int64_t row, base;
     if (staged) {
-      row = r0 + smem_row(soff, nrows, o);
+      const int r = smem_row(soff, nrows, o);
+      row = r0 + r;
+      base = soff[r];
     } else {
       int64_t lo = r0, hi = r1 + 1;
       while (lo < hi) {
@@ -104,9 +122,23 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
         if (offs[mid] <= o) lo = mid + 1; else hi = mid;
       }
       row = lo - 1;
+      base = offs[row];
     }
-    const int64_t j = start[row] + (o - (staged ? soff[row - r0] : offs[row]));
-    const uint64_t pk = jp.pkey[row];
+    rowv[k] = row;
+    jv[k] = o - base;
+  }
+  uint64_t keyv[SPT];
+  float tv[SPT];
+  uint32_t wv[SPT];
+  bool okv[SPT];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    okv[k] = false;
+    if (rowv[k] < 0) continue;
+    const int64_t row = rowv[k];
+    const int64_t j = start[row] + jv[k];
+    jv[k] = j;
+    const uint64_t pk = (uint64_t)pkey[row];
     const uint64_t bk = jp.bkey[j];
     bool ok = true;
     for (int e = 0; e < jp.nfeq; ++e) {
@@ -118,37 +150,96 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
       const int64_t b = operand_value(jp.cmp[c].b, pk, bk);
       ok &= jp.cmp[c].neq ? (a != b) : (a == b);
     }
-    const uint64_t key = ok ? (jp.cout | apply_moves(jp.om, jp.nom, pk, bk)) : KEY_DEAD;
-    jp.okey[o] = key;
-    if (jp.final_step) {
-      if (jp.semi == S_UNIT) continue;
-      // ⊗ left-deep in body order (reading 9)
-      float t = tag_at(jp, jp.tag_order[0], row, j);
-      for (int k = 1; k < jp.ntag; ++k) t = otimes(jp.semi, t, tag_at(jp, jp.tag_order[k], row, j));
-      if (jp.semi == S_MAXMULT) {
-        const uint32_t w = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
-        jp.oval64[o] = (uint64_t)f2u(t) | ((uint64_t)w << 32);
-      } else {
-        jp.oval32[o] = f2u(t);
+    okv[k] = ok;
+    keyv[k] = jp.cout | apply_moves(jp.om, jp.nom, pk, bk);
+    tv[k] = 1.0f;
+    wv[k] = 0;
+    if (jp.final_step && jp.semi != S_UNIT) {
+      tv[k] = candidate_tag(jp, row, j);
+      if (jp.semi == S_MAXMULT) wv[k] = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
+    }
+  }
+  // phase 2: emit
+  if (jp.direct) {  // fused A5-A8: ⊕ straight into the direct-mapped store
+    if (!jp.aggregate && jp.semi != S_UNIT) {
+      // issue all of this thread's atomics before consuming any result
+      unsigned long long oldv[SPT], newv[SPT];
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        newv[k] = 0ull;
+        oldv[k] = ~0ull;
+        if (rowv[k] < 0 || !okv[k]) continue;
+        const uint32_t slot = (uint32_t)keyv[k];
+        if (jp.semi == S_MAXMIN) {
+          const uint32_t v = (f2u(tv[k]) + 1u) << 1;
+          newv[k] = v;
+          oldv[k] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slot, v);
+        } else {
+          const unsigned long long v = ((unsigned long long)(f2u(tv[k]) + 1u) << 33) | (unsigned long long)(~wv[k]);
+          newv[k] = v;
+          oldv[k] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slot, v);
+        }
       }
-    } else if (jp.semi != S_UNIT) {
-      for (int k = 0; k < jp.npt; ++k) jp.otag[k][o] = jp.ptag[k][row];
-      jp.otag[jp.npt][o] = jp.btag ? jp.btag[j] : 1.0f;
+      // the unique first improver of a slot marks it dirty (no shared counter)
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const unsigned long long old = oldv[k], v = newv[k];
+        const bool settled_or_absent =
+            jp.semi == S_MAXMIN ? (old == 0ull || (old & 1ull)) : (old == 0ull || ((old >> 32) & 1ull));
+        if (rowv[k] >= 0 && okv[k] && old < v && settled_or_absent) {
+          const uint32_t slot = (uint32_t)keyv[k];
+          atomicOr(jp.dirty + (slot >> 5), 1u << (slot & 31u));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < SPT; ++k)
+        if (rowv[k] >= 0 && okv[k])
+          direct_oplus(jp.semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate);
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    if (rowv[k] < 0) continue;
+    const int64_t o = o0 + threadIdx.x + k * 256;
+    okey[o] = okv[k] ? (OK)keyv[k] : dead<OK>();
+    if (jp.semi == S_UNIT) continue;
+    if (jp.final_step) {
+      if (jp.semi == S_MAXMULT) jp.oval64[o] = (uint64_t)f2u(tv[k]) | ((uint64_t)wv[k] << 32);
+      else jp.oval32[o] = f2u(tv[k]);
+    } else {
+      const int64_t row = rowv[k];
+      for (int q = 0; q < jp.npt; ++q) jp.otag[q][o] = jp.ptag[q][row];
+      jp.otag[jp.npt][o] = jp.btag ? jp.btag[jv[k]] : 1.0f;
     }
   }
 }
 
+template <typename PK, typename OK>
 __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
+  const PK* __restrict__ key = reinterpret_cast<const PK*>(pp.key);
+  OK* __restrict__ okey = reinterpret_cast<OK*>(pp.okey);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pp.n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = pp.key[i];
-    bool ok = k != KEY_DEAD;
+    const PK kk = key[i];
+    const uint64_t k = (uint64_t)kk;
+    bool ok = kk != dead<PK>();
     for (int c = 0; c < pp.ncmp; ++c) {
       const int64_t a = operand_value(pp.cmp[c].a, k, 0);
       const int64_t b = operand_value(pp.cmp[c].b, k, 0);
       ok &= pp.cmp[c].neq ? (a != b) : (a == b);
     }
-    pp.okey[i] = ok ? (pp.cout | apply_moves(pp.om, pp.nom, k, 0)) : KEY_DEAD;
+    const uint64_t hk = pp.cout | apply_moves(pp.om, pp.nom, k, 0);
+    if (pp.direct) {
+      if (ok) {
+        const float t = (pp.semi != S_UNIT && pp.tag) ? pp.tag[i] : 1.0f;
+        const uint32_t w = pp.semi == S_MAXMULT ? (pp.wconst | (uint32_t)apply_moves(pp.wm, pp.nwm, k, 0)) : 0u;
+        direct_oplus(pp.semi, pp.fdir, (uint32_t)hk, t, w, pp.dirty, pp.aggregate);
+      }
+      continue;
+    }
+    okey[i] = ok ? (OK)hk : dead<OK>();
     if (pp.semi == S_UNIT) continue;
     const float t = pp.tag ? pp.tag[i] : 1.0f;
     if (pp.semi == S_MAXMULT) {
@@ -158,6 +249,78 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
       pp.oval32[i] = f2u(t);
     }
   }
+}
+
+// Row-centric fused join + direct ⊕ for bounded fan-out (every prefix of the
+// static CSR index has <= MAXDEG rows, e.g. lattice edges: 4).  One thread per
+// probe row: coalesced probe key / tag loads, its matches unrolled, all
+// atomics issued before any result is consumed.  No count / scan / host sync.
+template <typename PK, int MAXDEG>
+__global__ void __launch_bounds__(256) join_rows_direct_k(const JoinPlan jp,
+                                                          unsigned long long* __restrict__ ncand) {
+  const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
+  uint32_t mycount = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < jp.np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const PK pkr = pkey[i];
+    if (pkr == dead<PK>()) continue;
+    const uint64_t pk = (uint64_t)pkr;
+    const uint64_t pre = probe_prefix(jp, pk);
+    if (pre >= (uint64_t)jp.nprefix) continue;
+    const int64_t lo = jp.boff[pre];
+    const int n = (int)(jp.boff[pre + 1] - lo);
+    mycount += (uint32_t)n;
+    const float pt = jp.semi != S_UNIT ? jp.ptag[0][i] : 1.0f;
+    unsigned long long oldv[MAXDEG], newv[MAXDEG];
+    uint32_t slotv[MAXDEG];
+    bool live[MAXDEG];
+#pragma unroll
+    for (int d = 0; d < MAXDEG; ++d) {
+      live[d] = false;
+      if (d >= n) continue;
+      const uint64_t bk = jp.bkey[lo + d];
+      bool ok = true;
+      for (int c = 0; c < jp.ncmp; ++c) {
+        const int64_t a = operand_value(jp.cmp[c].a, pk, bk);
+        const int64_t b = operand_value(jp.cmp[c].b, pk, bk);
+        ok &= jp.cmp[c].neq ? (a != b) : (a == b);
+      }
+      if (!ok) continue;
+      const uint32_t slot = (uint32_t)(jp.cout | apply_moves(jp.om, jp.nom, pk, bk));
+      slotv[d] = slot;
+      live[d] = true;
+      if (jp.semi == S_UNIT) {
+        const uint32_t bit = 1u << (slot & 31u);
+        newv[d] = bit;
+        oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slot >> 5), bit);
+        continue;
+      }
+      const float bt = jp.btag[lo + d];
+      const float t = jp.tag_order[0] == 0 ? otimes(jp.semi, pt, bt) : otimes(jp.semi, bt, pt);
+      if (jp.semi == S_MAXMIN) {
+        const uint32_t v = (f2u(t) + 1u) << 1;
+        newv[d] = v;
+        oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slot, v);
+      } else {
+        const uint32_t w = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
+        const unsigned long long v = ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
+        newv[d] = v;
+        oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slot, v);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < MAXDEG; ++d) {
+      if (!live[d]) continue;
+      const unsigned long long old = oldv[d], v = newv[d];
+      bool first;
+      if (jp.semi == S_UNIT) first = !(old & v);
+      else if (jp.semi == S_MAXMIN) first = old < v && (old == 0ull || (old & 1ull));
+      else first = old < v && (old == 0ull || ((old >> 32) & 1ull));
+      if (first) atomicOr(jp.dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
+    }
+  }
+  mycount = __reduce_add_sync(0xffffffffu, mycount);
+  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
 }
 
 struct MoveList {
@@ -189,20 +352,58 @@ __global__ void build_offsets_k(const uint64_t* __restrict__ key, int64_t n, int
 void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaStream_t st) {
   if (jp.np <= 0) return;
   note_launch();
-  join_count_k<<<grid_for(jp.np, 256), 256, 0, st>>>(jp, count, start);
+  if (jp.pk32) join_count_k<uint32_t><<<grid_for(jp.np, 256), 256, 0, st>>>(jp, count, start);
+  else join_count_k<uint64_t><<<grid_for(jp.np, 256), 256, 0, st>>>(jp, count, start);
 }
 
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
                        cudaStream_t st) {
   if (total <= 0) return;
+  const unsigned g = (unsigned)((total + WT - 1) / WT);
   note_launch();
-  join_write_k<<<(unsigned)((total + WT - 1) / WT), 256, 0, st>>>(jp, offs, start, total);
+  if (jp.pk32 && jp.ok32) join_write_k<uint32_t, uint32_t><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else if (jp.pk32) join_write_k<uint32_t, uint64_t><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else if (jp.ok32) join_write_k<uint64_t, uint32_t><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else join_write_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(jp, offs, start, total);
+}
+
+void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st) {
+  if (jp.np <= 0) return;
+  const int g = grid_for(jp.np, 256);
+  note_launch();
+  if (jp.pk32) {
+    if (maxdeg <= 4) join_rows_direct_k<uint32_t, 4><<<g, 256, 0, st>>>(jp, ncand);
+    else join_rows_direct_k<uint32_t, 8><<<g, 256, 0, st>>>(jp, ncand);
+  } else {
+    if (maxdeg <= 4) join_rows_direct_k<uint64_t, 4><<<g, 256, 0, st>>>(jp, ncand);
+    else join_rows_direct_k<uint64_t, 8><<<g, 256, 0, st>>>(jp, ncand);
+  }
+}
+
+__global__ void max_degree_k(const int64_t* __restrict__ off, int64_t np, unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = (unsigned long long)(off[p + 1] - off[p]);
+    m = d > m ? d : m;
+  }
+  m = __reduce_max_sync(0xffffffffu, (unsigned)m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+void launch_max_degree(const int64_t* off, int64_t nprefix, unsigned long long* out, cudaStream_t st) {
+  if (nprefix <= 0) return;
+  note_launch();
+  max_degree_k<<<grid_for(nprefix, 256, 148 * 8), 256, 0, st>>>(off, nprefix, out);
 }
 
 void launch_project(const ProjectPlan& pp, cudaStream_t st) {
   if (pp.n <= 0) return;
+  const int g = grid_for(pp.n, 256);
   note_launch();
-  project_k<<<grid_for(pp.n, 256), 256, 0, st>>>(pp);
+  if (pp.pk32 && pp.ok32) project_k<uint32_t, uint32_t><<<g, 256, 0, st>>>(pp);
+  else if (pp.pk32) project_k<uint32_t, uint64_t><<<g, 256, 0, st>>>(pp);
+  else if (pp.ok32) project_k<uint64_t, uint32_t><<<g, 256, 0, st>>>(pp);
+  else project_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(pp);
 }
 
 void launch_rekey(const uint64_t* key, int64_t n, const Move* mv, int nmv, uint64_t* out, cudaStream_t st) {

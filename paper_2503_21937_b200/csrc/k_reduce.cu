@@ -9,6 +9,10 @@
 // add-mult accumulates in fp64 and rounds once; max-mult keeps the larger p and,
 // on equal p, the smaller witness (rule, non-head variables); across rounds a
 // tie keeps the existing tag.
+//
+// Two relation stores: sorted (keys + SoA tags, merged each round) and dense
+// (a direct-mapped tag array over the packed-key domain,
+// so A8 is an O(|U|) in-place update instead of an O(|F|) merge).
 #include "device_util.cuh"
 
 namespace lob {
@@ -78,10 +82,11 @@ __global__ void validate_k(const float* __restrict__ p, const int32_t* __restric
 }
 
 // -------------------------------------------------------- heads / dedup ----
-__global__ void heads_k(const uint64_t* __restrict__ key, int64_t n, uint32_t* __restrict__ flag) {
+template <typename K>
+__global__ void heads_k(const K* __restrict__ key, int64_t n, uint32_t* __restrict__ flag) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = key[i];
-    flag[i] = (k != KEY_DEAD && (i == 0 || key[i - 1] != k)) ? 1u : 0u;
+    const K k = key[i];
+    flag[i] = (k != dead<K>() && (i == 0 || key[i - 1] != k)) ? 1u : 0u;
   }
 }
 
@@ -119,11 +124,12 @@ __global__ void edb_reduce_k(const uint64_t* __restrict__ key, const float* __re
 // CTA each, strided partials combined by a fixed-shape tree (deterministic).
 constexpr int LONG_SEG = 64;
 
-__global__ void seg_ends_k(const uint64_t* __restrict__ key, const uint32_t* __restrict__ pos, int64_t n,
+template <typename K>
+__global__ void seg_ends_k(const K* __restrict__ key, const uint32_t* __restrict__ pos, int64_t n,
                            uint32_t* __restrict__ uend) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = key[i];
-    if (k == KEY_DEAD) continue;
+    const K k = key[i];
+    if (k == dead<K>()) continue;
     if (i == n - 1 || key[i + 1] != k) {
       const bool head = i == 0 || key[i - 1] != k;  // pos = exclusive count of heads
       uend[pos[i] - (head ? 0u : 1u)] = (uint32_t)(i + 1);
@@ -172,9 +178,9 @@ __device__ __forceinline__ void acc_store(Acc a, int64_t u, float* up, uint32_t*
   if constexpr (SEMI == S_MAXMULT) uw[u] = a.w;
 }
 
-template <int SEMI>
-__global__ void seg_reduce_short_k(const uint64_t* __restrict__ key, const void* __restrict__ valv,
-                                   const uint32_t* __restrict__ uend, int64_t nu, uint64_t* __restrict__ ukey,
+template <typename K, int SEMI>
+__global__ void seg_reduce_short_k(const K* __restrict__ key, const void* __restrict__ valv,
+                                   const uint32_t* __restrict__ uend, int64_t nu, K* __restrict__ ukey,
                                    float* __restrict__ up, uint32_t* __restrict__ uw, uint32_t* __restrict__ nlong,
                                    uint32_t* __restrict__ longs) {
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
@@ -202,22 +208,20 @@ __global__ void __launch_bounds__(256) seg_reduce_long_k(const void* __restrict_
   for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
     const uint32_t u = longs[q];
     const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
-    // thread t folds elements s+t, s+t+256, ... (in order)
+    // thread t folds elements s+t, s+t+256, ... in order (every long segment
+    // has more than 256 > LONG_SEG elements or at least LONG_SEG+1: guard)
     Acc a = acc_load<SEMI>(valv, s + threadIdx.x < e ? s + threadIdx.x : s);
-    bool have = s + threadIdx.x < e;
     for (int64_t j = s + threadIdx.x + 256; j < e; j += 256) a = acc_join<SEMI>(a, acc_load<SEMI>(valv, j));
     part[threadIdx.x] = a;
     __syncthreads();
-    // fixed pairwise tree over thread partials (every segment here has > 64 elements,
-    // so partials 0..63 always exist; missing partials only occur above e - s)
     const int cnt = (int)((e - s) < 256 ? (e - s) : 256);
-    for (int d = 1; d < 256; d <<= 1) {
-      if ((threadIdx.x % (2 * d)) == 0 && threadIdx.x + d < cnt) part[threadIdx.x] = acc_join<SEMI>(part[threadIdx.x], part[threadIdx.x + d]);
+    for (int d = 1; d < 256; d <<= 1) {  // fixed pairwise tree over the thread partials
+      if ((threadIdx.x % (2 * d)) == 0 && threadIdx.x + d < cnt)
+        part[threadIdx.x] = acc_join<SEMI>(part[threadIdx.x], part[threadIdx.x + d]);
       __syncthreads();
     }
     if (threadIdx.x == 0) acc_store<SEMI>(part[0], u, up, uw);
     __syncthreads();
-    (void)have;
   }
 }
 
@@ -314,6 +318,198 @@ __global__ void merge_k(const uint64_t* __restrict__ ak, const float* __restrict
   }
 }
 
+// ----------------------------------------------------------- dense store ----
+__global__ void dense_fill_k(uint32_t* __restrict__ a, int64_t n, uint32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+template <int SEMI>
+__global__ void dense_diff_k(const uint32_t* __restrict__ ukey, const float* __restrict__ up,
+                             const uint32_t* __restrict__ uw, int64_t nu, float* __restrict__ fp,
+                             uint32_t* __restrict__ fw, uint32_t* __restrict__ fbits, uint64_t* __restrict__ flags) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t slot = ukey[u];
+    uint64_t fl = 0;
+    if constexpr (SEMI == S_UNIT) {
+      const uint32_t bit = 1u << (slot & 31u);
+      const uint32_t old = atomicOr(fbits + (slot >> 5), bit);  // other bits of the word belong to other U rows
+      if (!(old & bit)) fl = (1ull << 32) | 1ull;
+    } else {
+      const float s = fp[slot];
+      const float b = up[u];
+      if (f2u(s) == DENSE_ABSENT) {
+        fl = (1ull << 32) | 1ull;
+        fp[slot] = b;
+        if constexpr (SEMI == S_MAXMULT) fw[slot] = uw[u];
+      } else {
+        const float nv = state_oplus(SEMI, s, b);
+        if (f2u(nv) != f2u(s)) {
+          fl = 1ull;
+          fp[slot] = nv;
+          if constexpr (SEMI == S_MAXMULT) fw[slot] = uw[u];  // strict improvement: witness follows p
+        }
+      }
+    }
+    flags[u] = fl;
+  }
+}
+
+__global__ void dense_delta_k(const uint32_t* __restrict__ ukey, const float* __restrict__ up,
+                              const uint32_t* __restrict__ uw, int64_t nu, const uint64_t* __restrict__ flags,
+                              const uint64_t* __restrict__ offs, int semi, uint32_t* __restrict__ dkey,
+                              float* __restrict__ dp, uint32_t* __restrict__ dw) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+    if (!(flags[u] & 1ull)) continue;
+    const uint32_t d = (uint32_t)offs[u];
+    dkey[d] = ukey[u];
+    if (semi != S_UNIT) dp[d] = up[u];  // Δ carries the increment b (reading 5)
+    if (semi == S_MAXMULT) dw[d] = uw[u];
+  }
+}
+
+__global__ void dense_present_k(const float* __restrict__ fp, const uint32_t* __restrict__ fbits, int64_t n,
+                                int semi, uint32_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (semi == S_UNIT) flag[i] = (fbits[i >> 5] >> (i & 31)) & 1u;
+    else flag[i] = f2u(fp[i]) != DENSE_ABSENT ? 1u : 0u;
+  }
+}
+
+__global__ void dense_compact_k(const float* __restrict__ fp, const uint32_t* __restrict__ fw,
+                                const uint32_t* __restrict__ fbits, const uint32_t* __restrict__ pos, int64_t n,
+                                int semi, uint64_t* __restrict__ key, float* __restrict__ p,
+                                uint32_t* __restrict__ w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool present;
+    if (semi == S_UNIT) present = (fbits[i >> 5] >> (i & 31)) & 1u;
+    else present = f2u(fp[i]) != DENSE_ABSENT;
+    if (!present) continue;
+    const uint32_t o = pos[i];
+    key[o] = (uint64_t)i;
+    if (semi != S_UNIT) p[o] = fp[i];
+    if (semi == S_MAXMULT) w[o] = fw[i];
+  }
+}
+
+// ------------------------------------------------------ direct ⊕ store ----
+__device__ __forceinline__ void direct_decode(const void* f, int semi, int64_t slot, bool& present, float& p,
+                                              uint32_t& w) {
+  present = false;
+  p = 0.0f;
+  w = 0;
+  if (semi == S_UNIT) {
+    present = (reinterpret_cast<const uint32_t*>(f)[slot >> 5] >> (slot & 31)) & 1u;
+  } else if (semi == S_MAXMIN) {
+    const uint32_t v = reinterpret_cast<const uint32_t*>(f)[slot];
+    present = v != 0u;
+    p = u2f((v >> 1) - 1u);
+  } else {
+    const unsigned long long v = reinterpret_cast<const unsigned long long*>(f)[slot];
+    present = v != 0ull;
+    p = u2f((uint32_t)(v >> 33) - 1u);
+    w = ~(uint32_t)v;
+  }
+}
+
+// dirty bitmap -> Δ': per-word popcounts, exclusive scan, then each word's set
+// bits are written in slot order (Δ' sorted by key), re-settled and cleared.
+__global__ void direct_dirty_count_k(const uint32_t* __restrict__ dirty, int64_t nw, uint32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = __popc(dirty[i]);
+}
+
+__global__ void direct_dirty_extract_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
+                                       const uint32_t* __restrict__ pos, int64_t nw, int semi,
+                                       uint32_t* __restrict__ dkey, float* __restrict__ dp,
+                                       uint32_t* __restrict__ dw) {
+  for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = dirty[wi];
+    if (!m) continue;
+    dirty[wi] = 0u;
+    uint32_t o = pos[wi];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1u;
+      const uint32_t slot = (uint32_t)(wi * 32 + b);
+      dkey[o] = slot;
+      if (semi == S_MAXMIN) {
+        uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
+        const uint32_t v = *a;
+        *a = v | 1u;
+        dp[o] = u2f((v >> 1) - 1u);
+      } else if (semi == S_MAXMULT) {
+        unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
+        const unsigned long long v = *a;
+        *a = v | (1ull << 32);
+        dp[o] = u2f((uint32_t)(v >> 33) - 1u);
+        dw[o] = ~(uint32_t)v;
+      }
+      ++o;
+    }
+  }
+}
+
+__global__ void direct_present_k(const void* __restrict__ f, int64_t n, int semi, uint32_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool pr;
+    float p;
+    uint32_t w;
+    direct_decode(f, semi, i, pr, p, w);
+    flag[i] = pr ? 1u : 0u;
+  }
+}
+
+__global__ void direct_compact_k(const void* __restrict__ f, const uint32_t* __restrict__ pos, int64_t n, int semi,
+                                 uint64_t* __restrict__ key, float* __restrict__ p, uint32_t* __restrict__ w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool pr;
+    float pp;
+    uint32_t ww;
+    direct_decode(f, semi, i, pr, pp, ww);
+    if (!pr) continue;
+    const uint32_t o = pos[i];
+    key[o] = (uint64_t)i;
+    if (semi != S_UNIT) p[o] = pp;
+    if (semi == S_MAXMULT) w[o] = ww;
+  }
+}
+
+template <typename K>
+void seg_reduce_impl(const K* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi, K* ukey,
+                     float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st) {
+  if (n <= 0 || nu <= 0) return;
+  uint32_t* uend = scratch;            // nu
+  uint32_t* nlong = scratch + nu;      // 1
+  uint32_t* longs = scratch + nu + 1;  // nu
+  cudaMemsetAsync(nlong, 0, 4, st);
+  note_launch();
+  seg_ends_k<K><<<grid_for(n, 256), 256, 0, st>>>(key, pos, n, uend);
+  const int g = grid_for(nu, 256);
+  note_launch();
+  switch (semi) {
+    case S_UNIT:
+      seg_reduce_short_k<K, S_UNIT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs);
+      return;
+    case S_MAXMIN:
+      seg_reduce_short_k<K, S_MAXMIN><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs);
+      break;
+    case S_ADDMULT:
+      seg_reduce_short_k<K, S_ADDMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs);
+      break;
+    default:
+      seg_reduce_short_k<K, S_MAXMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs);
+      break;
+  }
+  const int gl = 148 * 4;
+  note_launch();
+  switch (semi) {
+    case S_MAXMIN: seg_reduce_long_k<S_MAXMIN><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+    case S_ADDMULT: seg_reduce_long_k<S_ADDMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+    default: seg_reduce_long_k<S_MAXMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+  }
+}
+
 }  // namespace
 
 void launch_minmax(const int32_t* col, int64_t n, int32_t* out2, cudaStream_t st) {
@@ -327,88 +523,68 @@ void launch_pack(const PackPlan& pp, int64_t n, uint64_t* key, uint32_t* rowid, 
   pack_k<<<grid_for(n, 256), 256, 0, st>>>(pp, n, key, rowid);
 }
 void launch_gather_f32(const float* s, const uint32_t* idx, float* d, int64_t n, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    gather_f32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
-  }
+  if (n <= 0) return;
+  note_launch();
+  gather_f32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
 }
 void launch_gather_i32(const int32_t* s, const uint32_t* idx, int32_t* d, int64_t n, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    gather_i32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
-  }
+  if (n <= 0) return;
+  note_launch();
+  gather_i32_k<<<grid_for(n, 256), 256, 0, st>>>(s, idx, d, n);
 }
 void launch_iota_i32(int32_t* d, int64_t n, int32_t first, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    iota_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, first);
-  }
+  if (n <= 0) return;
+  note_launch();
+  iota_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, first);
 }
 void launch_fill_f32(float* d, int64_t n, float v, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    fill_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, v);
-  }
+  if (n <= 0) return;
+  note_launch();
+  fill_k<<<grid_for(n, 256), 256, 0, st>>>(d, n, v);
 }
 void launch_validate(const float* p, const int32_t* s, int64_t n, int32_t batch, uint32_t* flags, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    validate_k<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, s, n, batch, flags);
-  }
+  if (n <= 0) return;
+  note_launch();
+  validate_k<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, s, n, batch, flags);
 }
 void launch_heads(const uint64_t* key, int64_t n, uint32_t* flag, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    heads_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, flag);
-  }
+  if (n <= 0) return;
+  note_launch();
+  heads_k<uint64_t><<<grid_for(n, 256), 256, 0, st>>>(key, n, flag);
+}
+void launch_heads(const uint32_t* key, int64_t n, uint32_t* flag, cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch();
+  heads_k<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(key, n, flag);
 }
 void launch_edb_reduce(const uint64_t* key, const float* p, const int32_t* fid, const uint32_t* pos, int64_t n,
                        int semi, uint64_t* okey, float* op, int32_t* ofid, cudaStream_t st) {
-  if (n > 0) {
-    note_launch();
-    edb_reduce_k<<<grid_for(n, 256), 256, 0, st>>>(key, p, fid, pos, n, semi, okey, op, ofid);
-  }
+  if (n <= 0) return;
+  note_launch();
+  edb_reduce_k<<<grid_for(n, 256), 256, 0, st>>>(key, p, fid, pos, n, semi, okey, op, ofid);
 }
 void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
                        uint64_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st) {
-  if (n <= 0 || nu <= 0) return;
-  uint32_t* uend = scratch;            // nu
-  uint32_t* nlong = scratch + nu;      // 1
-  uint32_t* longs = scratch + nu + 1;  // nu
-  cudaMemsetAsync(nlong, 0, 4, st);
-  note_launch();
-  seg_ends_k<<<grid_for(n, 256), 256, 0, st>>>(key, pos, n, uend);
-  const int g = grid_for(nu, 256);
-  note_launch();
-  switch (semi) {
-    case S_UNIT: seg_reduce_short_k<S_UNIT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); return;
-    case S_MAXMIN: seg_reduce_short_k<S_MAXMIN><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
-    case S_ADDMULT: seg_reduce_short_k<S_ADDMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
-    default: seg_reduce_short_k<S_MAXMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs); break;
-  }
-  const int gl = 148 * 4;
-  note_launch();
-  switch (semi) {
-    case S_MAXMIN: seg_reduce_long_k<S_MAXMIN><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
-    case S_ADDMULT: seg_reduce_long_k<S_ADDMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
-    default: seg_reduce_long_k<S_MAXMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
-  }
+  seg_reduce_impl<uint64_t>(key, val, pos, n, nu, semi, ukey, up, uw, scratch, st);
+}
+void launch_seg_reduce(const uint32_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
+                       uint32_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st) {
+  seg_reduce_impl<uint32_t>(key, val, pos, n, nu, semi, ukey, up, uw, scratch, st);
 }
 void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* fkey,
                  const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos, cudaStream_t st) {
   (void)uw;
-  if (nu > 0) {
-    note_launch();
-    diff_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, nu, fkey, fp, nf, semi, flags, pos);
-  }
+  if (nu <= 0) return;
+  note_launch();
+  diff_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, nu, fkey, fp, nf, semi, flags, pos);
 }
 void launch_apply(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* flags,
                   const uint64_t* offs, const int64_t* pos, int semi, float* fp, uint32_t* fw, uint64_t* dkey,
                   float* dp, uint32_t* dw, uint64_t* nkey, float* np_, uint32_t* nw, cudaStream_t st) {
-  if (nu > 0)
-    note_launch();
-    apply_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, uw, nu, flags, offs, pos, semi, fp, fw, dkey, dp, dw, nkey,
-                                               np_, nw);
+  if (nu <= 0) return;
+  note_launch();
+  apply_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, uw, nu, flags, offs, pos, semi, fp, fw, dkey, dp, dw, nkey,
+                                             np_, nw);
 }
 void launch_merge(const uint64_t* akey, const float* ap, const uint32_t* aw, int64_t na, const uint64_t* bkey,
                   const float* bp, const uint32_t* bw, int64_t nb, uint64_t* okey, float* op, uint32_t* ow,
@@ -418,6 +594,68 @@ void launch_merge(const uint64_t* akey, const float* ap, const uint32_t* aw, int
   const int64_t threads = (total + MITEMS - 1) / MITEMS;
   note_launch();
   merge_k<<<grid_for(threads, 256), 256, 0, st>>>(akey, ap, aw, na, bkey, bp, bw, nb, okey, op, ow);
+}
+void launch_dense_fill(float* fp, uint32_t* fbits, int64_t nslots, int semi, cudaStream_t st) {
+  note_launch();
+  if (semi == S_UNIT) dense_fill_k<<<grid_for((nslots + 31) / 32, 256), 256, 0, st>>>(fbits, (nslots + 31) / 32, 0u);
+  else dense_fill_k<<<grid_for(nslots, 256), 256, 0, st>>>(reinterpret_cast<uint32_t*>(fp), nslots, DENSE_ABSENT);
+}
+void launch_dense_diff(const uint32_t* ukey, const float* up, const uint32_t* uw, int64_t nu, int semi, float* fp,
+                       uint32_t* fw, uint32_t* fbits, uint64_t* flags, cudaStream_t st) {
+  if (nu <= 0) return;
+  const int g = grid_for(nu, 256);
+  note_launch();
+  switch (semi) {
+    case S_UNIT: dense_diff_k<S_UNIT><<<g, 256, 0, st>>>(ukey, up, uw, nu, fp, fw, fbits, flags); break;
+    case S_MAXMIN: dense_diff_k<S_MAXMIN><<<g, 256, 0, st>>>(ukey, up, uw, nu, fp, fw, fbits, flags); break;
+    case S_ADDMULT: dense_diff_k<S_ADDMULT><<<g, 256, 0, st>>>(ukey, up, uw, nu, fp, fw, fbits, flags); break;
+    default: dense_diff_k<S_MAXMULT><<<g, 256, 0, st>>>(ukey, up, uw, nu, fp, fw, fbits, flags); break;
+  }
+}
+void launch_dense_delta(const uint32_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* flags,
+                        const uint64_t* offs, int semi, uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st) {
+  if (nu <= 0) return;
+  note_launch();
+  dense_delta_k<<<grid_for(nu, 256), 256, 0, st>>>(ukey, up, uw, nu, flags, offs, semi, dkey, dp, dw);
+}
+void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st) {
+  const size_t bytes = semi == S_UNIT ? (size_t)((nslots + 31) / 32) * 4
+                                      : (size_t)nslots * (semi == S_MAXMULT ? 8 : 4);
+  cudaMemsetAsync(f, 0, bytes, st);
+}
+void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  direct_dirty_count_k<<<grid_for(nwords, 256), 256, 0, st>>>(dirty, nwords, cnt);
+}
+void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
+                                 uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  direct_dirty_extract_k<<<grid_for(nwords, 256), 256, 0, st>>>(f, dirty, pos, nwords, semi, dkey, dp, dw);
+}
+void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
+  if (nslots <= 0) return;
+  note_launch();
+  direct_present_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, nslots, semi, flag);
+}
+void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
+                           uint32_t* w, cudaStream_t st) {
+  if (nslots <= 0) return;
+  note_launch();
+  direct_compact_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, pos, nslots, semi, key, p, w);
+}
+void launch_dense_present(const float* fp, const uint32_t* fbits, int64_t nslots, int semi, uint32_t* flag,
+                          cudaStream_t st) {
+  if (nslots <= 0) return;
+  note_launch();
+  dense_present_k<<<grid_for(nslots, 256), 256, 0, st>>>(fp, fbits, nslots, semi, flag);
+}
+void launch_dense_compact(const float* fp, const uint32_t* fw, const uint32_t* fbits, const uint32_t* pos,
+                          int64_t nslots, int semi, uint64_t* key, float* p, uint32_t* w, cudaStream_t st) {
+  if (nslots <= 0) return;
+  note_launch();
+  dense_compact_k<<<grid_for(nslots, 256), 256, 0, st>>>(fp, fw, fbits, pos, nslots, semi, key, p, w);
 }
 
 }  // namespace lob

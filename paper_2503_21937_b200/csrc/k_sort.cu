@@ -1,7 +1,8 @@
-// k_sort.cu — stable LSD radix sort of packed u64 keys (A6; the `sort`
+// k_sort.cu — stable LSD radix sort of packed keys (A6; the `sort`
 // instruction, Table 1, run every round by the Stratum rule,
 // PAPER.md:1296).  Only the significant bits of the key are sorted (keys are
-// packed with per-column domain widths), 8 bits per pass.
+// packed with per-column domain widths), 8 bits per pass; u32 keys are used
+// whenever the relation's packed key fits, halving the bytes moved.
 //
 // Per pass: (1) per-tile digit histogram in shared memory, written digit-major
 // so (2) one exclusive scan yields every (digit, tile) global base; (3) scatter:
@@ -20,7 +21,8 @@ constexpr int IPT = 16;
 constexpr int TILE = NT * IPT;
 constexpr int NW = NT / 32;
 
-__global__ void __launch_bounds__(NT) radix_hist_k(const uint64_t* __restrict__ key, int64_t n, int shift,
+template <typename K>
+__global__ void __launch_bounds__(NT) radix_hist_k(const K* __restrict__ key, int64_t n, int shift,
                                                    uint32_t* __restrict__ hist, int64_t ntiles) {
   __shared__ uint32_t h[256];
   h[threadIdx.x] = 0;
@@ -29,15 +31,15 @@ __global__ void __launch_bounds__(NT) radix_hist_k(const uint64_t* __restrict__ 
 #pragma unroll 4
   for (int k = 0; k < IPT; ++k) {
     int64_t i = base + k * NT + threadIdx.x;
-    if (i < n) atomicAdd(&h[(key[i] >> shift) & 255u], 1u);
+    if (i < n) atomicAdd(&h[(uint32_t)(key[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
   hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-template <typename V, bool HASV>
-__global__ void __launch_bounds__(NT) radix_scatter_k(const uint64_t* __restrict__ kin, const V* __restrict__ vin,
-                                                      uint64_t* __restrict__ kout, V* __restrict__ vout, int64_t n,
+template <typename K, typename V, bool HASV>
+__global__ void __launch_bounds__(NT) radix_scatter_k(const K* __restrict__ kin, const V* __restrict__ vin,
+                                                      K* __restrict__ kout, V* __restrict__ vout, int64_t n,
                                                       int shift, const uint32_t* __restrict__ base_off,
                                                       int64_t ntiles) {
   __shared__ uint32_t wcnt[NW][256];
@@ -45,7 +47,7 @@ __global__ void __launch_bounds__(NT) radix_scatter_k(const uint64_t* __restrict
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   run[tid] = base_off[(int64_t)tid * ntiles + blockIdx.x];
   const int64_t base = (int64_t)blockIdx.x * TILE;
-  uint64_t k[IPT];
+  K k[IPT];
   V v[HASV ? IPT : 1];
 #pragma unroll
   for (int s = 0; s < IPT; ++s) {
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(NT) radix_scatter_k(const uint64_t* __restrict
   for (int s = 0; s < IPT; ++s) {
     const int64_t i = base + s * NT + tid;
     const bool valid = i < n;
-    const uint32_t d = valid ? (uint32_t)((k[s] >> shift) & 255u) : 256u + 0u;
+    const uint32_t d = valid ? ((uint32_t)(k[s] >> shift) & 255u) : 256u;
 #pragma unroll
     for (int j = 0; j < 8; ++j) wcnt[w][lane * 8 + j] = 0;
     __syncwarp();
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(NT) radix_scatter_k(const uint64_t* __restrict
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-template <typename V, bool HASV>
-int radix_sort_impl(uint64_t* k0, V* v0, uint64_t* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st) {
+template <typename K, typename V, bool HASV>
+int radix_sort_impl(K* k0, V* v0, K* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st) {
   if (n <= 1 || bits <= 0) return 0;
   const int64_t ntiles = (n + TILE - 1) / TILE;
   uint32_t* hist = reinterpret_cast<uint32_t*>(tmp);
@@ -100,15 +102,15 @@ int radix_sort_impl(uint64_t* k0, V* v0, uint64_t* k1, V* v1, int64_t n, int bit
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    const uint64_t* ki = cur ? k1 : k0;
+    const K* ki = cur ? k1 : k0;
     const V* vi = cur ? v1 : v0;
-    uint64_t* ko = cur ? k0 : k1;
+    K* ko = cur ? k0 : k1;
     V* vo = cur ? v0 : v1;
     note_launch();
-    radix_hist_k<<<(unsigned)ntiles, NT, 0, st>>>(ki, n, shift, hist, ntiles);
+    radix_hist_k<K><<<(unsigned)ntiles, NT, 0, st>>>(ki, n, shift, hist, ntiles);
     exclusive_scan<uint32_t>(hist, hist, ntiles * 256, nullptr, stmp, st);
     note_launch();
-    radix_scatter_k<V, HASV><<<(unsigned)ntiles, NT, 0, st>>>(ki, vi, ko, vo, n, shift, hist, ntiles);
+    radix_scatter_k<K, V, HASV><<<(unsigned)ntiles, NT, 0, st>>>(ki, vi, ko, vo, n, shift, hist, ntiles);
     cur ^= 1;
   }
   return cur;
@@ -121,20 +123,23 @@ size_t sort_tmp_bytes(int64_t n) {
   return align_up((size_t)ntiles * 256 * sizeof(uint32_t)) + scan_tmp_bytes<uint32_t>(ntiles * 256) + 256;
 }
 
-template <>
-int radix_sort<void>(uint64_t* k0, void* v0, uint64_t* k1, void* v1, int64_t n, int bits, void* tmp,
-                     cudaStream_t st) {
-  return radix_sort_impl<uint32_t, false>(k0, (uint32_t*)v0, k1, (uint32_t*)v1, n, bits, tmp, st);
+template <typename K, typename V>
+int radix_sort(K* k0, V* v0, K* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st) {
+  if constexpr (std::is_void_v<V>)
+    return radix_sort_impl<K, uint32_t, false>(k0, (uint32_t*)v0, k1, (uint32_t*)v1, n, bits, tmp, st);
+  else
+    return radix_sort_impl<K, V, true>(k0, v0, k1, v1, n, bits, tmp, st);
 }
-template <>
-int radix_sort<uint32_t>(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, int64_t n, int bits, void* tmp,
-                         cudaStream_t st) {
-  return radix_sort_impl<uint32_t, true>(k0, v0, k1, v1, n, bits, tmp, st);
-}
-template <>
-int radix_sort<uint64_t>(uint64_t* k0, uint64_t* v0, uint64_t* k1, uint64_t* v1, int64_t n, int bits, void* tmp,
-                         cudaStream_t st) {
-  return radix_sort_impl<uint64_t, true>(k0, v0, k1, v1, n, bits, tmp, st);
-}
+
+template int radix_sort<uint64_t, void>(uint64_t*, void*, uint64_t*, void*, int64_t, int, void*, cudaStream_t);
+template int radix_sort<uint64_t, uint32_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, int64_t, int, void*,
+                                            cudaStream_t);
+template int radix_sort<uint64_t, uint64_t>(uint64_t*, uint64_t*, uint64_t*, uint64_t*, int64_t, int, void*,
+                                            cudaStream_t);
+template int radix_sort<uint32_t, void>(uint32_t*, void*, uint32_t*, void*, int64_t, int, void*, cudaStream_t);
+template int radix_sort<uint32_t, uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t, int, void*,
+                                            cudaStream_t);
+template int radix_sort<uint32_t, uint64_t>(uint32_t*, uint64_t*, uint32_t*, uint64_t*, int64_t, int, void*,
+                                            cudaStream_t);
 
 }  // namespace lob

@@ -45,7 +45,8 @@ struct Cmp {
 // is [prefix | free fields]; prefix built from the probe key by moves.
 struct JoinPlan {
   // probe
-  const uint64_t* pkey;
+  const void* pkey;         // u32 or u64 keys (pk32)
+  int8_t pk32, ok32;
   int64_t np;
   const float* ptag[MAXT];
   int npt;
@@ -79,15 +80,30 @@ struct JoinPlan {
   Move wm[MAXM];
   uint32_t wconst;
   // outputs
-  uint64_t* okey;
+  void* okey;               // u32 or u64 keys (ok32)
   float* otag[MAXT];        // intermediate: npt + 1 tag columns
   uint32_t* oval32;         // final, max-min / add-mult: p bits
   uint64_t* oval64;         // final, max-mult: p bits | w << 32
+  // direct ⊕ into a dense store (final step, idempotent semirings; see Direct)
+  int direct;
+  void* fdir;               // u32 bitmap (unit) / u32 packed (max-min) / u64 packed (max-mult)
+  uint32_t* dirty;          // bitmap: slots improved this round
+  int aggregate;            // warp pre-reduction of equal slots (narrow heads)
 };
+
+// Direct ⊕ (idempotent semirings on a direct-mapped store): F[slot] holds
+//   max-min : (pbits + 1) << 1 | settled
+//   max-mult: (pbits + 1) << 33 | settled << 32 | ~w
+// so one atomicMax per candidate computes "larger p wins; on equal p the
+// existing (settled) tag wins, then the smaller witness" (readings 8a, 8b).
+// The unique thread whose atomic lifts a settled or absent slot sets the
+// slot's bit in the round's dirty bitmap; the epilogue compacts the bitmap in
+// slot order into Δ' (sorted, deterministic) and re-settles those slots.
 
 // Single-atom rule (projection): rows of one relation -> candidates.
 struct ProjectPlan {
-  const uint64_t* key;
+  const void* key;          // u32 or u64 keys (pk32)
+  int8_t pk32, ok32;
   const float* tag;
   int64_t n;
   int ncmp;
@@ -99,9 +115,13 @@ struct ProjectPlan {
   uint32_t wconst;
   int nwm;
   Move wm[MAXM];
-  uint64_t* okey;
+  void* okey;
   uint32_t* oval32;
   uint64_t* oval64;
+  int direct;
+  void* fdir;
+  uint32_t* dirty;
+  int aggregate;
 };
 
 // ---- scan ----
@@ -116,8 +136,8 @@ void exclusive_scan(const T* in, T* out, int64_t n, T* total_dev, void* tmp, cud
 // V in {void (keys only), uint32_t, uint64_t}.  Sorts the low `bits` bits.
 // Ping-pong between (k0,v0) and (k1,v1); returns 0 if the result is in k0/v0.
 size_t sort_tmp_bytes(int64_t n);
-template <typename V>
-int radix_sort(uint64_t* k0, V* v0, uint64_t* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st);
+template <typename K, typename V>
+int radix_sort(K* k0, V* v0, K* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st);
 
 // ---- ingest (A0) ----
 void launch_minmax(const int32_t* col, int64_t n, int32_t* out2 /* device: min,max */, cudaStream_t st);
@@ -141,6 +161,7 @@ void launch_validate(const float* p, const int32_t* s, int64_t n, int32_t batch,
 
 // EDB duplicate merge (reading 16): sorted keys; heads -> scan -> reduce.
 void launch_heads(const uint64_t* key, int64_t n, uint32_t* flag, cudaStream_t st);
+void launch_heads(const uint32_t* key, int64_t n, uint32_t* flag, cudaStream_t st);
 void launch_edb_reduce(const uint64_t* key, const float* p, const int32_t* fid, const uint32_t* pos, int64_t n,
                        int semi, uint64_t* okey, float* op, int32_t* ofid, cudaStream_t st);
 
@@ -149,6 +170,10 @@ void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaS
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
                        cudaStream_t st);
 void launch_project(const ProjectPlan& pp, cudaStream_t st);
+// fused row-centric join + direct ⊕ (bounded fan-out <= 8 per prefix); adds |C| to *ncand
+void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st);
+// max_p (off[p+1] - off[p]) -> atomicMax into *out
+void launch_max_degree(const int64_t* off, int64_t nprefix, unsigned long long* out, cudaStream_t st);
 
 // ---- index build (A1) ----
 // re-key rows: out = Σ moves(key) ; tags copied
@@ -161,6 +186,32 @@ void launch_build_offsets(const uint64_t* key, int64_t n, int free_bits, int64_t
 // scratch: 2*nu + 1 uint32 words
 void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
                        uint64_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st);
+void launch_seg_reduce(const uint32_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
+                       uint32_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st);
+
+// ---- dense direct-mapped store: F[slot = packed key] ----
+// p = DENSE_ABSENT marks an absent tuple; under UNIT a presence bitmap.
+constexpr uint32_t DENSE_ABSENT = 0xffffffffu;
+void launch_dense_fill(float* fp, uint32_t* fbits, int64_t nslots, int semi, cudaStream_t st);
+// classify + apply U (unique u32 keys) in place: flags lo = in Δ', hi = new tuple
+void launch_dense_diff(const uint32_t* ukey, const float* up, const uint32_t* uw, int64_t nu, int semi, float* fp,
+                       uint32_t* fw, uint32_t* fbits, uint64_t* flags, cudaStream_t st);
+void launch_dense_delta(const uint32_t* ukey, const float* up, const uint32_t* uw, int64_t nu, const uint64_t* flags,
+                        const uint64_t* offs, int semi, uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
+// dense -> sorted list (end of stratum): flag present slots, scan, compact
+void launch_dense_present(const float* fp, const uint32_t* fbits, int64_t nslots, int semi, uint32_t* flag,
+                          cudaStream_t st);
+void launch_dense_compact(const float* fp, const uint32_t* fw, const uint32_t* fbits, const uint32_t* pos,
+                          int64_t nslots, int semi, uint64_t* key, float* p, uint32_t* w, cudaStream_t st);
+// direct ⊕ store: zero-fill, list -> Δ' (+ re-settle), present flags, compaction
+void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
+// dirty bitmap -> per-word popcounts (scan them), then Δ' in slot order
+void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st);
+void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
+                                 uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
+void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st);
+void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
+                           uint32_t* w, cudaStream_t st);
 // classify U against F: flags (u64: lo = in Δ', hi = new); pos (F index or -1)
 void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu,
                  const uint64_t* fkey, const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos,

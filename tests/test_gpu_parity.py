@@ -290,3 +290,15 @@ def test_rerun_new_database():
     eng.run()
     res = oracle.run(w2.program, 1, 2, w2.facts, outputs=["path"])
     assert_parity(eng, res, "path", 1)
+
+
+@pytest.mark.parametrize("env", ["LOBSTER_SORTED_STORE", "LOBSTER_SORT_DEDUP"])
+@pytest.mark.parametrize("sr", [0, 1, 3])
+def test_store_paths_match(sr, env, monkeypatch):
+    """Every relation-store path (merge-based sorted store; dense store with
+    radix sort + segmented ⊕; default dense direct ⊕) matches the oracle."""
+    monkeypatch.setenv(env, "1")
+    w = W.c2_workload(semiring=sr, n=8, batch=5)
+    eng, stats, res = run_both(w, outputs=["path", "endpoints_connected"])
+    assert_parity(eng, res, "path", sr, check_grads=False)
+    assert_parity(eng, res, "endpoints_connected", sr)
