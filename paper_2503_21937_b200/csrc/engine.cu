@@ -102,6 +102,8 @@ struct RelState {
   int64_t nslots = 0;
   DevMem dirf;          // direct store words
   DBuf<uint32_t> dirty;  // bitmap of the slots improved this round
+  DBuf<unsigned long long> dctr;  // |Δ'| counter of the single-pass extraction
+  int64_t cand_bound = 0;         // upper bound on slots dirtied this round
   DBuf<float> dfp;
   DBuf<uint32_t> dfw, dfbits, dkey32, ckey32, ckey32b;
   DBuf<uint64_t> ckey, ckey2, cv64, cv64b;
@@ -131,6 +133,7 @@ struct RelState {
     dirf.bind(st);
     for (auto* b : {&fid, &o_sid, &o_cols}) b->bind(st);
     for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
+    dctr.bind(st);
     for (auto& c : in.cols) c.bind(st);
     in.sid.bind(st);
     in.p.bind(st);
@@ -631,6 +634,16 @@ struct Ctx {
 
   int32_t class_base(int cl) const { return (int32_t)class_min[cl]; }
 
+  // atom k binds every variable of the rule: all other atoms are point lookups
+  static bool covers_rule(const Rule& R, int k) {
+    std::vector<char> b(R.var_names.size(), 0);
+    for (auto& t : R.body[k].args)
+      if (t.is_var()) b[t.var] = 1;
+    for (char x : b)
+      if (!x) return false;
+    return true;
+  }
+
   // Evaluate one rule (variant) and append its candidates to the head's buffer.
   void eval_rule(const Rule& R, const std::vector<Version>& ver, int start) {
     const int na = (int)R.body.size();
@@ -697,6 +710,90 @@ struct Ctx {
     std::vector<char> cmp_done(R.cmps.size(), 0);
     auto var_bound = [&](const Term& t, const std::vector<int>& vs) { return !t.is_var() || vs[t.var] >= 0; };
 
+    if (na >= 2 && covers_rule(R, start) && !force_slot_join) {  // lookup chain
+      LookupPlan lp{};
+      lp.pkey = T.key;
+      lp.pk32 = T.k32;
+      lp.np = T.n;
+      lp.ptag = semi != S_UNIT ? T.tags[0] : nullptr;
+      std::vector<int> tag_atoms{start};
+      for (int a = 0; a < na; ++a) {
+        if (a == start) continue;
+        const BodyAtom& A = R.body[a];
+        const Layout& L = rels[A.rel]->L;
+        std::vector<int> order(A.args.size());
+        std::iota(order.begin(), order.end(), 0);
+        Index* ix;
+        Index local_ix;
+        if (ver[a] == V_EXT) {
+          ix = static_index(A.rel, order, (int)order.size());
+        } else {
+          VerData vd = version_data(A.rel, ver[a]);
+          build_index(local_ix, L, order, (int)order.size(), (const uint64_t*)vd.key, vd.p, vd.n, false, false);
+          ix = &local_ix;
+        }
+        if (ix->n == 0) return;
+        if (lp.nlk >= MAXL) throw Failure(LOBSTER_E_PARSE, "too many lookup atoms in one rule");
+        Lookup& K = lp.lk[lp.nlk++];
+        if (L.has_sample && L.sbits) K.prem[K.nprem++] = Move{0, (uint8_t)T.sshift, (uint8_t)T.sbits, (uint8_t)ix->sshift};
+        for (int c = 0; c < (int)A.args.size(); ++c) {
+          const Term& t = A.args[c];
+          if (!t.is_var()) {
+            const int64_t f = (int64_t)t.cst - L.mins[c];
+            if (f < 0 || f >= ((int64_t)1 << L.bits[c])) return;  // constant outside the domain: no match
+            K.cprefix |= (uint64_t)f << ix->col_shift[c];
+          } else if (L.bits[c]) {
+            if (K.nprem >= MAXM) throw Failure(LOBSTER_E_PARSE, "lookup atom too wide");
+            K.prem[K.nprem++] = Move{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], (uint8_t)ix->col_shift[c]};
+          }
+        }
+        merge_moves(K.prem, K.nprem);
+        K.bkey = ix->key;
+        K.btag = semi != S_UNIT ? ix->p : nullptr;
+        K.nb = ix->n;
+        K.boff = ix->offp;
+        K.nprefix = ix->nprefix;
+        tag_atoms.push_back(a);
+      }
+      for (auto& c : pending_start) lp.cmp[lp.ncmp++] = c;
+      for (size_t i = 0; i < R.cmps.size(); ++i) {
+        auto op = [&](const Term& t) -> Operand {
+          if (!t.is_var()) return Operand{2, 0, 0, t.cst};
+          return Operand{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
+        };
+        if (lp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
+        lp.cmp[lp.ncmp++] = Cmp{op(R.cmps[i].a), op(R.cmps[i].b), (int8_t)R.cmps[i].neq};
+      }
+      head_moves(R, H, T, nullptr, lp.om, lp.nom, lp.cout);
+      witness_moves(R, T, nullptr, lp.wm, lp.nwm, lp.wconst);
+      merge_moves(lp.om, lp.nom);
+      merge_moves(lp.wm, lp.nwm);
+      lp.semi = semi;
+      if (semi != S_UNIT) {
+        lp.ntag = na;
+        for (int k = 0; k < na; ++k)
+          for (size_t q = 0; q < tag_atoms.size(); ++q)
+            if (tag_atoms[q] == k) lp.tag_order[k] = (int8_t)q;
+      }
+      if (H.direct) {
+        direct_target(H, lp.direct, lp.fdir, lp.dirty, lp.aggregate);
+      } else {
+        reserve_candidates(H, H.nc + T.n);
+        lp.ok32 = H.dense;
+        lp.okey = cand_key(H);
+        lp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
+        lp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
+      }
+      {
+        Phase ph(this, 0);
+        launch_lookup_chain(lp, d_ncand, st);
+        kcheck("lookup chain");
+      }
+      H.nc += T.n;  // live candidates are counted on the device (d_ncand)
+      H.cand_bound += T.n;
+      return;
+    }
+
     if (na == 1) {  // projection
       ProjectPlan pp{};
       pp.key = T.key;
@@ -730,6 +827,7 @@ struct Ctx {
       launch_project(pp, st);
       kcheck("project");
       H.nc += T.n;
+      H.cand_bound += T.n;
       stats.candidates += T.n;
       return;
     }
@@ -837,6 +935,7 @@ struct Ctx {
           kcheck("join rows direct");
         }
         H.nc += T.n;  // candidates counted on the device (d_ncand)
+        H.cand_bound += T.n * ix->maxdeg;
         return;
       }
       // count + scan (A3-A4)
@@ -924,6 +1023,7 @@ struct Ctx {
       }
       if (last) {
         H.nc += total;
+        H.cand_bound += total;
         stats.candidates += total;
       } else {
         T = N;
@@ -1105,6 +1205,9 @@ struct Ctx {
       S.dirf.reserve(bytes);
       launch_direct_fill(S.dirf.get(), ns, semi, st);
       S.dirty.reserve((ns + 31) / 32);
+      S.dctr.reserve(1);
+      cuda_check(cudaMemsetAsync(S.dctr.ptr(), 0, 8, st), "memset");
+      S.cand_bound = 0;
       cuda_check(cudaMemsetAsync(S.dirty.ptr(), 0, (size_t)((ns + 31) / 32) * 4, st), "memset");
       return;
     }
@@ -1133,27 +1236,26 @@ struct Ctx {
     S.nc = 0;
     if (nc == 0) { S.nd = 0; return 0; }
     const int64_t nw = (S.nslots + 31) / 32;
-    uint32_t* cnt = arena.get<uint32_t>(nw);
-    uint32_t* pos = arena.get<uint32_t>(nw);
-    uint32_t* tot = arena.get<uint32_t>(1);
-    {
+    const int64_t cap = std::min<int64_t>(std::max<int64_t>(S.cand_bound, 1), S.nslots);
+    S.cand_bound = 0;
+    S.dkey32.reserve(cap);
+    if (semi != S_UNIT) S.dp.reserve(cap);
+    if (semi == S_MAXMULT) S.dw.reserve(cap);
+    const int64_t ntiles = (nw + 1023) / 1024;
+    uint32_t* tcnt = arena.get<uint32_t>(ntiles);
+    uint32_t* tbase = arena.get<uint32_t>(ntiles + 1);
+    {  // Δ' in slot order: tile popcounts -> scan -> extract; dirty bits cleared, slots re-settled
       Phase ph(this, 3);
-      launch_direct_dirty_count(S.dirty.ptr(), nw, cnt, st);
-      exclusive_scan<uint32_t>(cnt, pos, nw, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nw)), st);
-      kcheck("dirty count");
+      launch_dirty_tile_count(S.dirty.ptr(), nw, tcnt, st);
+      exclusive_scan<uint32_t>(tcnt, tbase, ntiles, tbase + ntiles, arena.alloc(scan_tmp_bytes<uint32_t>(ntiles)), st);
+      launch_direct_extract1(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
+                             semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr,
+                             S.dctr.ptr(), tbase, st);
+      kcheck("direct extract");
     }
-    const int64_t nd = read_dev(tot);
+    const int64_t nd = (int64_t)read_dev(tbase + ntiles);
     stats.bytes_algorithmic += bytes_round_direct(nc, nd);
     S.nd = nd;
-    if (nd == 0) return 0;
-    Phase ph(this, 3);
-    S.dkey32.reserve(nd);
-    if (semi != S_UNIT) S.dp.reserve(nd);
-    if (semi == S_MAXMULT) S.dw.reserve(nd);
-    // Δ' in slot order (sorted, deterministic); dirty bits cleared, slots re-settled
-    launch_direct_dirty_extract(S.dirf.get(), S.dirty.ptr(), pos, nw, semi, S.dkey32.ptr(),
-                                semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr, st);
-    kcheck("direct extract");
     return nd;
   }
 
@@ -1315,14 +1417,17 @@ struct Ctx {
           if (lpos.empty()) {
             if (!first) continue;
             std::vector<Version> ver(R.body.size(), V_EXT);
-            // start: smallest batched atom (ties: body order)
+            // start: a batched atom covering every variable (the rest become
+            // point lookups: no intermediate), else the smallest batched atom
             int start = -1;
             int64_t best = INT64_MAX;
-            for (int k = 0; k < (int)R.body.size(); ++k) {
-              if (prog.rels[R.body[k].rel].shared) continue;
-              int64_t n = rels[R.body[k].rel]->n;
-              if (n < best) { best = n; start = k; }
-            }
+            for (int pass = 0; pass < 2 && start < 0; ++pass)
+              for (int k = 0; k < (int)R.body.size(); ++k) {
+                if (prog.rels[R.body[k].rel].shared) continue;
+                if (pass == 0 && !(R.body.size() >= 2 && covers_rule(R, k))) continue;
+                int64_t n = rels[R.body[k].rel]->n;
+                if (n < best) { best = n; start = k; }
+              }
             eval_rule(R, ver, start);
             continue;
           }

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // probe row: coalesced probe key / tag loads, its matches unrolled, all
 // atomics issued before any result is consumed.  No count / scan / host sync.
 template <typename PK, int MAXDEG>
-__global__ void __launch_bounds__(256) join_rows_direct_k(const JoinPlan jp,
+__global__ void __launch_bounds__(256, (MAXDEG <= 4) ? 6 : 4) join_rows_direct_k(const JoinPlan jp,
                                                           unsigned long long* __restrict__ ncand) {
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   uint32_t mycount = 0;
@@ -323,6 +323,71 @@ __global__ void __launch_bounds__(256) join_rows_direct_k(const JoinPlan jp,
   if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
 }
 
+template <typename PK, typename OK>
+__global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsigned long long* __restrict__ ncand) {
+  const PK* __restrict__ pkey = reinterpret_cast<const PK*>(lp.pkey);
+  OK* __restrict__ okey = reinterpret_cast<OK*>(lp.okey);
+  uint32_t mycount = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lp.np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const PK pkr = pkey[i];
+    bool ok = pkr != dead<PK>();
+    const uint64_t pk = (uint64_t)pkr;
+    for (int c = 0; c < lp.ncmp; ++c) {
+      const int64_t a = operand_value(lp.cmp[c].a, pk, 0);
+      const int64_t b = operand_value(lp.cmp[c].b, pk, 0);
+      ok &= lp.cmp[c].neq ? (a != b) : (a == b);
+    }
+    float tags[MAXL + 1];
+    tags[0] = (lp.semi != S_UNIT && lp.ptag) ? lp.ptag[i] : 1.0f;
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) {
+      if (l >= lp.nlk) break;
+      tags[l + 1] = 1.0f;
+      if (!ok) continue;
+      const Lookup& L = lp.lk[l];
+      const uint64_t pre = L.cprefix | apply_moves(L.prem, L.nprem, pk, 0);
+      int64_t j = -1;
+      if (L.boff) {
+        if (pre < (uint64_t)L.nprefix && L.boff[pre + 1] > L.boff[pre]) j = L.boff[pre];
+      } else {
+        const int64_t q = lower_bound_u64(L.bkey, L.nb, pre);
+        if (q < L.nb && L.bkey[q] == pre) j = q;
+      }
+      if (j < 0) ok = false;
+      else if (lp.semi != S_UNIT && L.btag) tags[l + 1] = L.btag[j];
+    }
+    float t = 1.0f;
+    uint32_t w = 0;
+    if (ok && lp.semi != S_UNIT) {
+      float v[MAXL + 1];
+#pragma unroll
+      for (int k = 0; k <= MAXL; ++k) v[k] = tags[k];
+      auto pick = [&](int idx) {
+        float r = v[0];
+#pragma unroll
+        for (int k = 1; k <= MAXL; ++k)
+          if (k == idx) r = v[k];
+        return r;
+      };
+      t = pick(lp.tag_order[0]);
+      for (int k = 1; k < lp.ntag; ++k) t = otimes(lp.semi, t, pick(lp.tag_order[k]));
+      if (lp.semi == S_MAXMULT) w = lp.wconst | (uint32_t)apply_moves(lp.wm, lp.nwm, pk, 0);
+    }
+    const uint64_t key = lp.cout | apply_moves(lp.om, lp.nom, pk, 0);
+    if (ok) ++mycount;
+    if (lp.direct) {
+      if (ok) direct_oplus(lp.semi, lp.fdir, (uint32_t)key, t, w, lp.dirty, lp.aggregate);
+      continue;
+    }
+    okey[i] = ok ? (OK)key : dead<OK>();
+    if (lp.semi == S_MAXMULT) lp.oval64[i] = (uint64_t)f2u(t) | ((uint64_t)w << 32);
+    else if (lp.semi != S_UNIT) lp.oval32[i] = f2u(t);
+  }
+  mycount = __reduce_add_sync(0xffffffffu, mycount);
+  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+}
+
 struct MoveList {
   Move m[MAXM];
   int n;
@@ -378,6 +443,16 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
     if (maxdeg <= 4) join_rows_direct_k<uint64_t, 4><<<g, 256, 0, st>>>(jp, ncand);
     else join_rows_direct_k<uint64_t, 8><<<g, 256, 0, st>>>(jp, ncand);
   }
+}
+
+void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaStream_t st) {
+  if (lp.np <= 0) return;
+  const int g = grid_for(lp.np, 256);
+  note_launch();
+  if (lp.pk32 && lp.ok32) lookup_chain_k<uint32_t, uint32_t><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.pk32) lookup_chain_k<uint32_t, uint64_t><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.ok32) lookup_chain_k<uint64_t, uint32_t><<<g, 256, 0, st>>>(lp, ncand);
+  else lookup_chain_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(lp, ncand);
 }
 
 __global__ void max_degree_k(const int64_t* __restrict__ off, int64_t np, unsigned long long* __restrict__ out) {

@@ -450,6 +450,97 @@ __global__ void direct_dirty_extract_k(void* __restrict__ f, uint32_t* __restric
   }
 }
 
+// Single pass: each CTA tile = 1024 dirty words (4 consecutive per thread,
+// one 16-B load), block scan of popcounts, one global atomic per tile for the
+// output base.  Slots come out sorted within a tile (tiles in any order;
+// results do not depend on Δ order under idempotent ⊕).
+__global__ void __launch_bounds__(256) direct_extract1_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
+                                                         int64_t nw, int semi, uint32_t* __restrict__ dkey,
+                                                         float* __restrict__ dp, uint32_t* __restrict__ dw,
+                                                         unsigned long long* __restrict__ counter,
+                                                         const uint32_t* __restrict__ tile_base) {
+  // A tile is 4 sub-tiles of 256 words, one word per thread (short serial bit
+  // loops); tile bases come from the scanned tile popcounts (slot order).
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t s_run;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  (void)counter;
+  for (int64_t base = (int64_t)blockIdx.x * 1024; base < nw; base += (int64_t)gridDim.x * 1024) {
+    if (threadIdx.x == 0) s_run = tile_base[base / 1024];
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      const int64_t w = base + k * 256 + threadIdx.x;
+      uint32_t m = w < nw ? dirty[w] : 0u;
+      const uint32_t c = __popc(m);
+      uint32_t inc = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += u;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t t = s_run;
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t x = wsum[j];
+          wsum[j] = t;
+          t += x;
+        }
+        s_run = t;
+      }
+      __syncthreads();
+      uint32_t o = wsum[warp] + inc - c;
+      __syncthreads();  // wsum reused by the next sub-tile
+      if (!m) continue;
+      dirty[w] = 0u;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1u;
+        const uint32_t slot = (uint32_t)(w * 32 + b);
+        dkey[o] = slot;
+        if (semi == S_MAXMIN) {  // settle and fetch in one atomic
+          const uint32_t v = atomicOr(reinterpret_cast<uint32_t*>(f) + slot, 1u);
+          dp[o] = u2f((v >> 1) - 1u);
+        } else if (semi == S_MAXMULT) {
+          const unsigned long long v = atomicOr(reinterpret_cast<unsigned long long*>(f) + slot, 1ull << 32);
+          dp[o] = u2f((uint32_t)(v >> 33) - 1u);
+          dw[o] = ~(uint32_t)v;
+        }
+        ++o;
+      }
+    }
+  }
+}
+
+// popcount of each 1024-word tile of the dirty bitmap
+__global__ void __launch_bounds__(256) dirty_tile_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
+                                                          uint32_t* __restrict__ tcnt) {
+  const int64_t ntiles = (nw + 1023) / 1024;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t w0 = t * 1024 + threadIdx.x * 4;
+    uint32_t c = 0;
+    if (w0 + 3 < nw) {
+      const uint4 m = *reinterpret_cast<const uint4*>(dirty + w0);
+      c = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (w0 + k < nw) c += __popc(dirty[w0 + k]);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t s = 0;
+      for (int k = 0; k < 8; ++k) s += ws[k];
+      tcnt[t] = s;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void direct_present_k(const void* __restrict__ f, int64_t n, int semi, uint32_t* __restrict__ flag) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     bool pr;
@@ -622,6 +713,18 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st) {
   const size_t bytes = semi == S_UNIT ? (size_t)((nslots + 31) / 32) * 4
                                       : (size_t)nslots * (semi == S_MAXMULT ? 8 : 4);
   cudaMemsetAsync(f, 0, bytes, st);
+}
+void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
+                            uint32_t* dw, unsigned long long* counter, const uint32_t* tile_base, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  direct_extract1_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(f, dirty, nwords, semi, dkey, dp, dw,
+                                                                                 counter, tile_base);
+}
+void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  dirty_tile_count_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(dirty, nwords, tcnt);
 }
 void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st) {
   if (nwords <= 0) return;

@@ -124,6 +124,50 @@ struct ProjectPlan {
   int aggregate;
 };
 
+// Lookup chain: probe rows whose variables cover the whole rule; every other
+// body atom is fully bound, i.e. a point lookup (<= 1 row, EDB deduplicated).
+// One thread per probe row; no intermediate, no count / scan.
+constexpr int MAXL = 4;
+struct Lookup {
+  int nprem;
+  Move prem[MAXM];
+  uint64_t cprefix;
+  const uint64_t* bkey;
+  const float* btag;
+  int64_t nb;
+  const int64_t* boff;  // CSR over the (full-key) prefix, or null (binary search)
+  int64_t nprefix;
+};
+struct LookupPlan {
+  const void* pkey;
+  int8_t pk32, ok32;
+  int64_t np;
+  const float* ptag;
+  int nlk;
+  Lookup lk[MAXL];
+  int ncmp;
+  Cmp cmp[MAXC];  // operands read from the probe key (src 0)
+  int nom;
+  Move om[MAXM];
+  uint64_t cout;
+  int semi;
+  // ⊗ in body order over T = [probe tag, lookup tags...]
+  int ntag;
+  int8_t tag_order[MAXT];
+  int nwm;
+  Move wm[MAXM];
+  uint32_t wconst;
+  // outputs: candidates (dead key for a miss / filtered row) or direct ⊕
+  void* okey;
+  uint32_t* oval32;
+  uint64_t* oval64;
+  int direct;
+  void* fdir;
+  uint32_t* dirty;
+  int aggregate;
+};
+void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaStream_t st);
+
 // ---- scan ----
 // Exclusive prefix sum; writes the total to *total_dev (device).  T in
 // {uint32_t, int64_t, uint64_t}.  tmp: scratch of scan_tmp_bytes(n) bytes.
@@ -205,6 +249,13 @@ void launch_dense_compact(const float* fp, const uint32_t* fw, const uint32_t* f
                           int64_t nslots, int semi, uint64_t* key, float* p, uint32_t* w, cudaStream_t st);
 // direct ⊕ store: zero-fill, list -> Δ' (+ re-settle), present flags, compaction
 void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
+// single-pass dirty bitmap -> Δ' (tile-sorted); *counter += |Δ'|; dkey/dp/dw
+// must hold every slot that can be dirty this round
+// tile_base (scanned per-1024-word popcounts, see launch_dirty_tile_count) gives
+// slot-sorted Δ'; null = bases from an atomic counter (tiles unordered)
+void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
+                            uint32_t* dw, unsigned long long* counter, const uint32_t* tile_base, cudaStream_t st);
+void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st);
 // dirty bitmap -> per-word popcounts (scan them), then Δ' in slot order
 void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st);
 void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
