@@ -122,6 +122,12 @@ typedef struct {
   int64_t candidates;             /* Σ join outputs (|C|) over all rounds                 */
   double ms_total, ms_join, ms_sort, ms_reduce, ms_merge, ms_grad, ms_comm;
   int64_t bytes_algorithmic;      /* SURVEY §8(d) B_alg summed over rounds               */
+  /* the fused row-centric join + direct ⊕ kernel (the dominant kernel on
+     bounded-fan-out programs): launches, CUDA-event time, probe rows and
+     candidates it processed, and its row bytes (key + tag) for §8(d) bytes   */
+  int64_t fj_launches, fj_probe_rows, fj_candidates;
+  double ms_fused_join;
+  int32_t fj_row_bytes, pad0;
 } lobster_run_stats;
 
 /* Evaluate every stratum to fixpoint (termination: no new tuple and no tag whose

@@ -29,7 +29,10 @@ class RunStats(ctypes.Structure):
     _fields_ = [("strata", ctypes.c_int32), ("rounds_total", ctypes.c_int32), ("tuples_derived", ctypes.c_int64),
                 ("candidates", ctypes.c_int64), ("ms_total", ctypes.c_double), ("ms_join", ctypes.c_double),
                 ("ms_sort", ctypes.c_double), ("ms_reduce", ctypes.c_double), ("ms_merge", ctypes.c_double),
-                ("ms_grad", ctypes.c_double), ("ms_comm", ctypes.c_double), ("bytes_algorithmic", ctypes.c_int64)]
+                ("ms_grad", ctypes.c_double), ("ms_comm", ctypes.c_double), ("bytes_algorithmic", ctypes.c_int64),
+                ("fj_launches", ctypes.c_int64), ("fj_probe_rows", ctypes.c_int64),
+                ("fj_candidates", ctypes.c_int64), ("ms_fused_join", ctypes.c_double),
+                ("fj_row_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -930,11 +930,13 @@ struct Ctx {
         merge_moves(jp.om, jp.nom);
         merge_moves(jp.wm, jp.nwm);
         {
-          Phase ph(this, 0);
-          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand, st);
+          Phase ph(this, 5);
+          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand + 1, st);
           kcheck("join rows direct");
         }
-        H.nc += T.n;  // candidates counted on the device (d_ncand)
+        stats.fj_launches++;
+        stats.fj_probe_rows += T.n;
+        H.nc += T.n;  // candidates counted on the device (d_ncand[1])
         H.cand_bound += T.n * ix->maxdeg;
         return;
       }
@@ -1378,8 +1380,8 @@ struct Ctx {
     if (!loaded) throw Failure(LOBSTER_E_STATE, "run before program_load");
     if (sticky) throw Failure(LOBSTER_E_CUDA, "context is in a failed state");
     stats = lobster_run_stats{};
-    if (!d_ncand) cuda_check(cudaMalloc(&d_ncand, 8), "cudaMalloc");
-    cuda_check(cudaMemsetAsync(d_ncand, 0, 8, st), "memset");
+    if (!d_ncand) cuda_check(cudaMalloc(&d_ncand, 16), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(d_ncand, 0, 16, st), "memset");
     ev.clear();
     ev_used = 0;
     cudaEvent_t t0 = get_event(), t1;
@@ -1452,7 +1454,9 @@ struct Ctx {
     }
     for (size_t r = 0; r < prog.rels.size(); ++r)
       if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
-    stats.candidates += (int64_t)read_dev(d_ncand);
+    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1);
+    stats.candidates += (int64_t)read_dev(d_ncand) + stats.fj_candidates;
+    stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
     if (!round_cap_hit && semi == S_MAXMULT) {
       Phase ph(this, 4);
       gradients();
@@ -1471,6 +1475,10 @@ struct Ctx {
         case 1: stats.ms_sort += m; break;
         case 2: stats.ms_reduce += m; break;
         case 3: stats.ms_merge += m; break;
+        case 5:
+          stats.ms_fused_join += m;
+          stats.ms_join += m;
+          break;
         default: stats.ms_grad += m; break;
       }
     }
