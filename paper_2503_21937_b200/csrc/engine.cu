@@ -193,6 +193,19 @@ struct Ctx {
   unsigned long long* d_ncand = nullptr;  // device counter of fused-join candidates
   bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
+  int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line
+  double host_ms[8] = {};
+  struct HostTimer {  // accumulates host wall time of a scope (diagnostics)
+    double& acc;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    bool on = true;
+    explicit HostTimer(double& a) : acc(a) {}
+    void stop() {
+      if (on) acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      on = false;
+    }
+    ~HostTimer() { stop(); }
+  };
   bool force_sorted = getenv("LOBSTER_SORTED_STORE") != nullptr;      // A/B: merge-based store
   bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
   int64_t num_facts_db = 0;
@@ -1199,9 +1212,12 @@ struct Ctx {
     if (semi != S_ADDMULT && !force_sort_dedup) {  // idempotent ⊕: fused direct store
       const int64_t ns = (int64_t)1 << S.L.total;
       const size_t bytes = semi == S_UNIT ? (size_t)((ns + 31) / 32) * 4 : (size_t)ns * (semi == S_MAXMULT ? 8 : 4);
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      if ((double)bytes > 0.5 * (double)fr) return;
+      if (S.dirf.capacity() < bytes) {  // cudaMemGetInfo costs 0.2-11 ms: only when a new slot array is needed
+        size_t fr = 0, tot = 0;
+        HostTimer hm(host_ms[6]);
+        cudaMemGetInfo(&fr, &tot);
+        if ((double)bytes > 0.5 * (double)fr) return;
+      }
       S.dense = S.direct = true;
       S.nslots = ns;
       S.dirf.reserve(bytes);
@@ -1215,9 +1231,11 @@ struct Ctx {
     }
     const int64_t ns = (int64_t)1 << S.L.total;
     const double bytes = semi == S_UNIT ? ns / 8.0 : (double)ns * (semi == S_MAXMULT ? 8 : 4);
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    if (bytes > 0.5 * (double)fr) return;
+    if ((double)S.dfp.bytes() < bytes) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if (bytes > 0.5 * (double)fr) return;
+    }
     S.dense = true;
     S.nslots = ns;
     if (semi == S_UNIT) {
@@ -1243,16 +1261,15 @@ struct Ctx {
     S.dkey32.reserve(cap);
     if (semi != S_UNIT) S.dp.reserve(cap);
     if (semi == S_MAXMULT) S.dw.reserve(cap);
-    const int64_t ntiles = (nw + 1023) / 1024;
+    const int64_t ntiles = (nw + 31) / 32;  // warp chunks of 32 words
     uint32_t* tcnt = arena.get<uint32_t>(ntiles);
     uint32_t* tbase = arena.get<uint32_t>(ntiles + 1);
-    {  // Δ' in slot order: tile popcounts -> scan -> extract; dirty bits cleared, slots re-settled
+    {  // Δ' in slot order: chunk popcounts -> scan -> extract; dirty bits cleared, slots re-settled
       Phase ph(this, 3);
-      launch_dirty_tile_count(S.dirty.ptr(), nw, tcnt, st);
+      launch_dirty_chunk_count(S.dirty.ptr(), nw, tcnt, st);
       exclusive_scan<uint32_t>(tcnt, tbase, ntiles, tbase + ntiles, arena.alloc(scan_tmp_bytes<uint32_t>(ntiles)), st);
-      launch_direct_extract1(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
-                             semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr,
-                             S.dctr.ptr(), tbase, st);
+      launch_direct_extract_warp(S.dirf.get(), S.dirty.ptr(), tbase, nw, semi, S.dkey32.ptr(),
+                                 semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr, st);
       kcheck("direct extract");
     }
     const int64_t nd = (int64_t)read_dev(tbase + ntiles);
@@ -1392,7 +1409,11 @@ struct Ctx {
     }
     static_idx.clear();
     arena.reset();
-    ingest();
+    for (double& h : host_ms) h = 0.0;
+    {
+      HostTimer ht(host_ms[0]);
+      ingest();
+    }
     int64_t round_cap_hit = 0;
     for (size_t si = 0; si < prog.strata.size(); ++si) {
       const std::vector<int>& strat = prog.strata[si];
@@ -1403,6 +1424,7 @@ struct Ctx {
         S.key.reserve(1);
         if (semi != S_UNIT) S.p.reserve(1);
         if (semi == S_MAXMULT) S.w.reserve(1);
+        HostTimer hts(host_ms[4]);
         choose_store(S);
       }
       int rounds = 0;
@@ -1411,6 +1433,7 @@ struct Ctx {
         if (rounds >= max_iters) { round_cap_hit = 1; break; }
         rounds++;
         arena.reset();
+        HostTimer ht_rules(host_ms[1]);
         for (const Rule& R : prog.rules) {
           if (!local.count(R.head_rel)) continue;
           std::vector<int> lpos;
@@ -1441,11 +1464,16 @@ struct Ctx {
             eval_rule(R, ver, lpos[j]);
           }
         }
+        ht_rules.stop();
         first = false;
         int64_t changed = 0;
-        for (int r : strat) changed += settle(r);
+        {
+          HostTimer ht(host_ms[2]);
+          for (int r : strat) changed += settle(r);
+        }
         if (changed == 0) break;
       }
+      HostTimer ht(host_ms[3]);
       for (int r : strat)
         if (rels[r]->dense) dense_to_sorted(*rels[r]);
       stats.rounds_total += rounds;
@@ -1459,6 +1487,7 @@ struct Ctx {
     stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
     if (!round_cap_hit && semi == S_MAXMULT) {
       Phase ph(this, 4);
+      HostTimer htg(host_ms[5]);
       gradients();
     }
     t1 = get_event();
@@ -1484,6 +1513,12 @@ struct Ctx {
     }
     ran = true;
     arena.reset();
+    if (log_level >= 1)
+      fprintf(stderr,
+              "[lobster] run: %.2f ms (events) | host: ingest %.2f, rules %.2f, settle %.2f, dense->sorted %.2f | "
+              "store setup %.2f (memgetinfo %.2f), gradients %.2f | phases: join %.2f (fused %.2f), sort %.2f, reduce %.2f, merge %.2f, grad %.2f | rounds %d\n",
+              stats.ms_total, host_ms[0], host_ms[1], host_ms[2], host_ms[3], host_ms[4], host_ms[6], host_ms[5], stats.ms_join, stats.ms_fused_join,
+              stats.ms_sort, stats.ms_reduce, stats.ms_merge, stats.ms_grad, stats.rounds_total);
     if (out) *out = stats;
     if (round_cap_hit) throw Failure(LOBSTER_E_ITER_CAP, "max_iters rounds reached");
   }

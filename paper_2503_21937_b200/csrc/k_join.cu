@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? 6 : 4) join_rows_direct_k
     unsigned long long oldv[MAXDEG], newv[MAXDEG];
     uint32_t slotv[MAXDEG];
     bool live[MAXDEG];
+    // phase A: candidate slot + packed value, and a plain (possibly stale) read
+    // of the slot.  The store is monotone (atomicMax / OR only), so a stale
+    // read is a lower bound: a candidate not above it can never improve the
+    // slot and needs no atomic.
 #pragma unroll
     for (int d = 0; d < MAXDEG; ++d) {
       live[d] = false;
@@ -290,22 +294,35 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? 6 : 4) join_rows_direct_k
       slotv[d] = slot;
       live[d] = true;
       if (jp.semi == S_UNIT) {
-        const uint32_t bit = 1u << (slot & 31u);
-        newv[d] = bit;
-        oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slot >> 5), bit);
+        newv[d] = 1u << (slot & 31u);
+        oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + (slot >> 5));
         continue;
       }
       const float bt = jp.btag[lo + d];
       const float t = jp.tag_order[0] == 0 ? otimes(jp.semi, pt, bt) : otimes(jp.semi, bt, pt);
       if (jp.semi == S_MAXMIN) {
-        const uint32_t v = (f2u(t) + 1u) << 1;
-        newv[d] = v;
-        oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slot, v);
+        newv[d] = (f2u(t) + 1u) << 1;
+        oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
       } else {
         const uint32_t w = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
-        const unsigned long long v = ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
-        newv[d] = v;
-        oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slot, v);
+        newv[d] = ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
+        oldv[d] = __ldcg(reinterpret_cast<const unsigned long long*>(jp.fdir) + slot);
+      }
+    }
+    // phase B: atomics only for candidates above the stale bound
+#pragma unroll
+    for (int d = 0; d < MAXDEG; ++d) {
+      if (!live[d]) continue;
+      const unsigned long long v = newv[d];
+      if (jp.semi == S_UNIT) {
+        if (oldv[d] & v) { live[d] = false; continue; }
+        oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
+      } else if (jp.semi == S_MAXMIN) {
+        if (v <= oldv[d]) { live[d] = false; continue; }
+        oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
+      } else {
+        if (v <= oldv[d]) { live[d] = false; continue; }
+        oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], v);
       }
     }
 #pragma unroll

@@ -500,15 +500,87 @@ __global__ void __launch_bounds__(256) direct_extract1_k(void* __restrict__ f, u
         m &= m - 1u;
         const uint32_t slot = (uint32_t)(w * 32 + b);
         dkey[o] = slot;
-        if (semi == S_MAXMIN) {  // settle and fetch in one atomic
-          const uint32_t v = atomicOr(reinterpret_cast<uint32_t*>(f) + slot, 1u);
+        if (semi == S_MAXMIN) {  // settle: each slot appears once here, no atomic needed
+          uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
+          const uint32_t v = __ldcg(a);
+          __stcg(a, v | 1u);
           dp[o] = u2f((v >> 1) - 1u);
         } else if (semi == S_MAXMULT) {
-          const unsigned long long v = atomicOr(reinterpret_cast<unsigned long long*>(f) + slot, 1ull << 32);
+          unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
+          const unsigned long long v = __ldcg(a);
+          __stcg(a, v | (1ull << 32));
           dp[o] = u2f((uint32_t)(v >> 33) - 1u);
           dw[o] = ~(uint32_t)v;
         }
         ++o;
+      }
+    }
+  }
+}
+
+// Warp-granular variant (no block barriers): chunk = 32 words, one per lane.
+__global__ void __launch_bounds__(256) dirty_chunk_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
+                                                           uint32_t* __restrict__ ccnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (nw + 31) / 32;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t w = c * 32 + lane;
+    const uint32_t n = __reduce_add_sync(0xffffffffu, w < nw ? (uint32_t)__popc(dirty[w]) : 0u);
+    if (lane == 0) ccnt[c] = n;
+  }
+}
+
+__global__ void __launch_bounds__(256) direct_extract_warp_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
+                                                             const uint32_t* __restrict__ cbase, int64_t nw, int semi,
+                                                             uint32_t* __restrict__ dkey, float* __restrict__ dp,
+                                                             uint32_t* __restrict__ dw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (nw + 31) / 32;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t w = c * 32 + lane;
+    uint32_t m = w < nw ? dirty[w] : 0u;
+    const uint32_t cnt = __popc(m);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    if (!total) continue;
+    if (m) dirty[w] = 0u;
+    const uint32_t base = cbase[c];
+    // the chunk's set bits are spread evenly over the lanes: lane handles bit
+    // k = lane, lane+32, ...; its word = first lane whose inclusive count > k
+    for (uint32_t kb = 0; kb < total; kb += 32) {  // warp-uniform trip count (shuffles below)
+      const uint32_t k = kb + lane;
+      const bool act = k < total;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {  // branch-free search over the 32 inclusive counts
+        const uint32_t v = __shfl_sync(0xffffffffu, inc, lo + step - 1);
+        if (v <= k) lo += step;
+      }
+      const uint32_t wm = __shfl_sync(0xffffffffu, m, lo);
+      const uint32_t wex = __shfl_sync(0xffffffffu, inc - cnt, lo);
+      if (!act) continue;
+      const uint32_t bit = __fns(wm, 0, (int)(k - wex) + 1);
+      const uint32_t slot = (uint32_t)((c * 32 + lo) * 32 + bit);
+      const uint32_t o = base + k;
+      dkey[o] = slot;
+      if (semi == S_MAXMIN) {  // settle: each slot appears once here, no atomic needed
+        uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
+        const uint32_t v = __ldcg(a);
+        __stcg(a, v | 1u);
+        dp[o] = u2f((v >> 1) - 1u);
+      } else if (semi == S_MAXMULT) {
+        unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
+        const unsigned long long v = __ldcg(a);
+        __stcg(a, v | (1ull << 32));
+        dp[o] = u2f((uint32_t)(v >> 33) - 1u);
+        dw[o] = ~(uint32_t)v;
       }
     }
   }
@@ -720,6 +792,18 @@ void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   note_launch();
   direct_extract1_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(f, dirty, nwords, semi, dkey, dp, dw,
                                                                                  counter, tile_base);
+}
+void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  dirty_chunk_count_k<<<grid_for((nwords + 31) / 32 * 32, 256), 256, 0, st>>>(dirty, nwords, ccnt);
+}
+void launch_direct_extract_warp(void* f, uint32_t* dirty, const uint32_t* cbase, int64_t nwords, int semi,
+                                uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st) {
+  if (nwords <= 0) return;
+  note_launch();
+  direct_extract_warp_k<<<grid_for((nwords + 31) / 32 * 32, 256), 256, 0, st>>>(f, dirty, cbase, nwords, semi, dkey,
+                                                                               dp, dw);
 }
 void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st) {
   if (nwords <= 0) return;

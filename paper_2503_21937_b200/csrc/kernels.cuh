@@ -256,6 +256,10 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
 void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, unsigned long long* counter, const uint32_t* tile_base, cudaStream_t st);
 void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st);
+// warp-granular: per-32-word chunk popcounts (scan them) -> Δ' in slot order, no block barriers
+void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st);
+void launch_direct_extract_warp(void* f, uint32_t* dirty, const uint32_t* cbase, int64_t nwords, int semi,
+                                uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
 // dirty bitmap -> per-word popcounts (scan them), then Δ' in slot order
 void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st);
 void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
