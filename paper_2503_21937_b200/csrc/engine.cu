@@ -123,6 +123,12 @@ struct RelState {
   DBuf<int64_t> goff, gfid;
   DBuf<float> gval;
   int64_t ng = 0;
+  // micro-batched runs: `output` relations accumulated over sample chunks
+  bool retained = true;
+  DBuf<int32_t> acc_sid, acc_col[MAXARITY];
+  DBuf<float> acc_p, acc_gval;
+  DBuf<int64_t> acc_goff, acc_gfid;
+  int64_t acc_n = 0, acc_ng = 0;
 
   void bind(cudaStream_t st) {
     for (auto* b : {&key, &key2, &dkey, &okey, &ckey, &ckey2, &cv64, &cv64b}) b->bind(st);
@@ -135,6 +141,12 @@ struct RelState {
     for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
     dctr.bind(st);
     for (auto& c : in.cols) c.bind(st);
+    for (auto& c : acc_col) c.bind(st);
+    acc_sid.bind(st);
+    acc_p.bind(st);
+    acc_gval.bind(st);
+    acc_goff.bind(st);
+    acc_gfid.bind(st);
     in.sid.bind(st);
     in.p.bind(st);
     in.fid.bind(st);
@@ -193,6 +205,8 @@ struct Ctx {
   unsigned long long* d_ncand = nullptr;  // device counter of fused-join candidates
   bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
+  int32_t batch_cur = 1;  // samples of the (micro-)batch being evaluated
+  bool micro = false;     // the last run was split into sample chunks
   int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line
   double host_ms[8] = {};
   struct HostTimer {  // accumulates host wall time of a scope (diagnostics)
@@ -391,7 +405,7 @@ struct Ctx {
     const Relation& R = prog.rels[r];
     Layout L;
     L.has_sample = !R.shared;
-    L.sbits = L.has_sample ? bits_for((uint64_t)opt.batch_size - 1) : 0;
+    L.sbits = L.has_sample ? bits_for((uint64_t)batch_cur - 1) : 0;
     int pos = 0;
     L.bits.assign(R.arity, 0);
     L.shift.assign(R.arity, 0);
@@ -412,7 +426,7 @@ struct Ctx {
   }
 
   // ----------------------------------------------------------------- ingest
-  void ingest() {
+  void ingest_domains() {
     const int nr = (int)prog.rels.size();
     // A0: per-column min/max of every input relation -> domain classes
     std::vector<std::pair<int, int>> cols;
@@ -450,6 +464,13 @@ struct Ctx {
       }
       if (class_min[cl] > class_max[cl]) class_min[cl] = class_max[cl] = 0;
     }
+  }
+
+  // Per-chunk part of A0: layouts for the current (micro-)batch, witness
+  // layouts, then pack + sort + ⊕-merge the facts of samples [s_lo, s_hi)
+  // (rebased to 0) of every input relation; shared relations whole.
+  void ingest_chunk(int32_t s_lo, int32_t s_hi) {
+    const int nr = (int)prog.rels.size();
     for (int r = 0; r < nr; ++r) rels[r]->L = make_layout(r);
     // witness layouts (diff-max-mult): rule index in the top bits, non-head
     // variables below, first variable most significant (tie order, reading 8b)
@@ -489,13 +510,15 @@ struct Ctx {
       }
       pp.sample = S.L.has_sample ? S.in.sid.ptr() : nullptr;
       pp.sshift = (uint8_t)S.L.sshift;
+      pp.s_lo = s_lo;
+      pp.s_hi = s_hi;
       uint64_t* k0 = arena.get<uint64_t>(n);
       uint64_t* k1 = arena.get<uint64_t>(n);
       uint32_t* r0 = arena.get<uint32_t>(n);
       uint32_t* r1 = arena.get<uint32_t>(n);
       void* stmp = arena.alloc(sort_tmp_bytes(n));
       launch_pack(pp, n, k0, r0, st);
-      int which = radix_sort(k0, r0, k1, r1, n, S.L.total, stmp, st);
+      int which = radix_sort(k0, r0, k1, r1, n, S.L.total + 1, stmp, st);  // +1: dead rows last
       uint64_t* ks = which ? k1 : k0;
       uint32_t* rs = which ? r1 : r0;
       float* ps = arena.get<float>(n);
@@ -1401,7 +1424,7 @@ struct Ctx {
     cuda_check(cudaMemsetAsync(d_ncand, 0, 16, st), "memset");
     ev.clear();
     ev_used = 0;
-    cudaEvent_t t0 = get_event(), t1;
+    cudaEvent_t t0 = get_event();
     cudaEventRecord(t0, st);
     for (auto& r : rels) {
       r->out_dev_ready = r->out_host_ready = false;
@@ -1412,8 +1435,148 @@ struct Ctx {
     for (double& h : host_ms) h = 0.0;
     {
       HostTimer ht(host_ms[0]);
-      ingest();
+      ingest_domains();
     }
+    // Micro-batching (SURVEY §5 memory planner): samples are independent
+    // databases, so the fixpoint runs over sample ranges whose
+    // packed keys fit the direct-mapped store; `output` relations are
+    // collected across ranges.
+    const int32_t B = opt.batch_size;
+    const int32_t mb = choose_micro_batch();
+    micro = mb < B;
+    for (auto& r : rels) {
+      r->retained = true;
+      r->acc_n = r->acc_ng = 0;
+    }
+    int64_t round_cap_hit = 0;
+    for (int32_t s0 = 0; s0 < B && !round_cap_hit; s0 += mb) {
+      const int32_t s1 = std::min<int32_t>(B, s0 + mb);
+      batch_cur = micro ? s1 - s0 : B;
+      {
+        HostTimer ht(host_ms[0]);
+        static_idx.clear();
+        ingest_chunk(micro ? s0 : 0, micro ? s1 : B);
+      }
+      round_cap_hit = run_strata();
+      for (size_t r = 0; r < prog.rels.size(); ++r)
+        if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
+      if (!round_cap_hit && semi == S_MAXMULT) {
+        Phase ph(this, 4);
+        HostTimer htg(host_ms[5]);
+        gradients();
+      }
+      if (micro) collect_outputs(s0);
+    }
+    batch_cur = B;
+    if (micro) finalize_collected();
+    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1);
+    stats.candidates += (int64_t)read_dev(d_ncand) + stats.fj_candidates;
+    stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
+    finish_run(t0, round_cap_hit, out);
+  }
+
+  // largest power-of-two sample range whose dense-eligible relations fit 30 bits
+  int32_t choose_micro_batch() {
+    const int32_t B = opt.batch_size;
+    if (opt.micro_batch > 0) return std::min(opt.micro_batch, B);
+    const int sb_full = bits_for((uint64_t)B - 1);
+    int excess = 0;
+    for (size_t r = 0; r < prog.rels.size(); ++r) {
+      const Relation& R = prog.rels[r];
+      if (R.input || R.shared || rels[r]->build_local) continue;
+      int cols = 0;
+      for (int c = 0; c < R.arity; ++c) {
+        const int cl = R.col_class[c];
+        cols += bits_for((uint64_t)(class_max[cl] - class_min[cl]));
+      }
+      excess = std::max(excess, cols + sb_full - 30);
+    }
+    if (excess <= 0) return B;
+    const int sb = sb_full - excess;
+    if (sb < 0) return B;  // does not fit even per sample: sorted store, whole batch
+    return std::min<int32_t>(B, (int32_t)1 << sb);
+  }
+
+  // append this chunk's `output` relations (sample ids rebased by s0) to the accumulators
+  void collect_outputs(int32_t s0) {
+    for (size_t r = 0; r < prog.rels.size(); ++r) {
+      const Relation& R = prog.rels[r];
+      if (R.input) continue;
+      RelState& S = *rels[r];
+      if (!R.output) {
+        S.retained = false;
+        continue;
+      }
+      const int64_t n = S.n, a = S.acc_n, ar = R.arity;
+      S.acc_sid.reserve(a + n, a);
+      for (int c = 0; c < ar; ++c) S.acc_col[c].reserve(a + n, a);
+      if (n > 0) {
+        int32_t* tcols = arena.get<int32_t>(std::max<int64_t>(1, ar * n));
+        uint8_t* dsh = arena.get<uint8_t>(64);
+        std::vector<uint8_t> hb(48, 0);
+        for (int c = 0; c < ar; ++c) { hb[c] = (uint8_t)S.L.shift[c]; hb[8 + c] = (uint8_t)S.L.bits[c]; }
+        std::memcpy(hb.data() + 16, S.L.mins.data(), ar * 4);
+        cuda_check(cudaMemcpyAsync(dsh, hb.data(), hb.size(), cudaMemcpyHostToDevice, st), "H2D");
+        launch_unpack(S.key.ptr(), n, S.L.has_sample, (uint8_t)S.L.sshift, (int)ar, dsh, dsh + 8,
+                      reinterpret_cast<int32_t*>(dsh + 16), S.acc_sid.ptr() + a, tcols, st);
+        launch_add_i32(S.acc_sid.ptr() + a, n, s0, st);
+        for (int c = 0; c < ar; ++c)
+          cuda_check(cudaMemcpyAsync(S.acc_col[c].ptr() + a, tcols + (int64_t)c * n, n * 4, cudaMemcpyDeviceToDevice, st),
+                     "collect");
+        if (semi != S_UNIT) {
+          S.acc_p.reserve(a + n, a);
+          cuda_check(cudaMemcpyAsync(S.acc_p.ptr() + a, S.p.ptr(), n * 4, cudaMemcpyDeviceToDevice, st), "collect");
+        }
+      }
+      if (S.has_grad) {
+        S.acc_goff.reserve(a + n + 1, a);
+        launch_add_i64(S.goff.ptr(), n + 1, S.acc_ng, S.acc_goff.ptr() + a, st);
+        S.acc_gfid.reserve(S.acc_ng + S.ng, S.acc_ng);
+        S.acc_gval.reserve(S.acc_ng + S.ng, S.acc_ng);
+        if (S.ng) {
+          cuda_check(cudaMemcpyAsync(S.acc_gfid.ptr() + S.acc_ng, S.gfid.ptr(), S.ng * 8, cudaMemcpyDeviceToDevice, st),
+                     "collect");
+          cuda_check(cudaMemcpyAsync(S.acc_gval.ptr() + S.acc_ng, S.gval.ptr(), S.ng * 4, cudaMemcpyDeviceToDevice, st),
+                     "collect");
+        }
+        S.acc_ng += S.ng;
+      }
+      S.acc_n += n;
+      kcheck("collect outputs");
+    }
+    sync();
+    arena.reset();
+  }
+
+  // accumulated outputs become the relation's output views
+  void finalize_collected() {
+    for (size_t r = 0; r < prog.rels.size(); ++r) {
+      const Relation& R = prog.rels[r];
+      RelState& S = *rels[r];
+      if (R.input || !S.retained) continue;
+      const int64_t n = S.acc_n, ar = R.arity;
+      S.n = n;
+      S.o_sid.swap(S.acc_sid);
+      S.o_cols.reserve(std::max<int64_t>(1, ar * n));
+      for (int c = 0; c < ar; ++c)
+        if (n) cuda_check(cudaMemcpyAsync(S.o_cols.ptr() + (int64_t)c * n, S.acc_col[c].ptr(), n * 4,
+                                          cudaMemcpyDeviceToDevice, st), "finalize");
+      S.o_soff.reserve(opt.batch_size + 1);
+      launch_sample_offsets_i32(S.o_sid.ptr(), n, opt.batch_size, S.o_soff.ptr(), st);
+      if (semi != S_UNIT) S.p.swap(S.acc_p);
+      if (S.has_grad) {
+        S.goff.swap(S.acc_goff);
+        S.gfid.swap(S.acc_gfid);
+        S.gval.swap(S.acc_gval);
+        S.ng = S.acc_ng;
+      }
+      S.out_dev_ready = true;
+      kcheck("finalize outputs");
+    }
+  }
+
+  // one (micro-)batch: every stratum to fixpoint; returns 1 if max_iters was hit
+  int64_t run_strata() {
     int64_t round_cap_hit = 0;
     for (size_t si = 0; si < prog.strata.size(); ++si) {
       const std::vector<int>& strat = prog.strata[si];
@@ -1480,17 +1643,11 @@ struct Ctx {
       stats.strata++;
       if (round_cap_hit) break;
     }
-    for (size_t r = 0; r < prog.rels.size(); ++r)
-      if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
-    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1);
-    stats.candidates += (int64_t)read_dev(d_ncand) + stats.fj_candidates;
-    stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
-    if (!round_cap_hit && semi == S_MAXMULT) {
-      Phase ph(this, 4);
-      HostTimer htg(host_ms[5]);
-      gradients();
-    }
-    t1 = get_event();
+    return round_cap_hit;
+  }
+
+  void finish_run(cudaEvent_t t0, int64_t round_cap_hit, lobster_run_stats* out) {
+    cudaEvent_t t1 = get_event();
     cudaEventRecord(t1, st);
     sync();
     float ms = 0;
@@ -1647,6 +1804,9 @@ struct Ctx {
     if (!ran) throw Failure(LOBSTER_E_STATE, "output_get before a successful run");
     const int r = it->second;
     RelState& S = *rels[r];
+    if (!S.retained)
+      throw Failure(LOBSTER_E_INVALID_ARG, std::string("relation ") + relname +
+                                               " was not retained by a micro-batched run (declare it `output`)");
     const int ar = prog.rels[r].arity;
     const int64_t n = S.n;
     if (!S.out_dev_ready) {

@@ -39,9 +39,15 @@ __global__ void minmax_k(const int32_t* __restrict__ col, int64_t n, int32_t* __
 
 __global__ void pack_k(const PackPlan pp, int64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ rowid) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = pp.sample ? ((uint64_t)(uint32_t)pp.sample[i] << pp.sshift) : 0ull;
+    uint64_t k = 0ull;
+    bool live = true;
+    if (pp.sample) {
+      const int32_t s = pp.sample[i];
+      live = s >= pp.s_lo && s < pp.s_hi;
+      k = (uint64_t)(uint32_t)(s - pp.s_lo) << pp.sshift;
+    }
     for (int c = 0; c < pp.ncols; ++c) k |= (uint64_t)(uint32_t)(pp.col[c][i] - pp.min[c]) << pp.shift[c];
-    key[i] = k;
+    key[i] = live ? k : KEY_DEAD;
     rowid[i] = (uint32_t)i;
   }
 }
@@ -96,7 +102,7 @@ __global__ void edb_reduce_k(const uint64_t* __restrict__ key, const float* __re
                              uint64_t* __restrict__ okey, float* __restrict__ op, int32_t* __restrict__ ofid) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = key[i];
-    if (i > 0 && key[i - 1] == k) continue;
+    if (k == KEY_DEAD || (i > 0 && key[i - 1] == k)) continue;  // dead: outside the micro-batch
     float bp = p[i];
     int32_t bf = fid[i];
     double acc = (double)bp;

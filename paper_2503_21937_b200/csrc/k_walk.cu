@@ -160,7 +160,42 @@ __global__ void dense_sum_k(const uint64_t* __restrict__ key, const uint32_t* __
   }
 }
 
+__global__ void add_i32_k(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += v;
+}
+__global__ void add_i64_k(const int64_t* __restrict__ s, int64_t n, int64_t v, int64_t* __restrict__ d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i] + v;
+}
+__global__ void sample_offsets_i32_k(const int32_t* __restrict__ sid, int64_t n, int32_t batch,
+                                     int64_t* __restrict__ off) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > batch) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sid[mid] < s) lo = mid + 1; else hi = mid;
+  }
+  off[s] = lo;
+}
+
 }  // namespace
+
+void launch_add_i32(int32_t* a, int64_t n, int32_t v, cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch();
+  add_i32_k<<<grid_for(n, 256), 256, 0, st>>>(a, n, v);
+}
+void launch_add_i64(const int64_t* s, int64_t n, int64_t v, int64_t* d, cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch();
+  add_i64_k<<<grid_for(n, 256), 256, 0, st>>>(s, n, v, d);
+}
+void launch_sample_offsets_i32(const int32_t* sid, int64_t n, int32_t batch, int64_t* off, cudaStream_t st) {
+  note_launch();
+  sample_offsets_i32_k<<<(unsigned)((batch + 1 + 255) / 256), 256, 0, st>>>(sid, n, batch, off);
+}
 
 void launch_walk(const WalkTables& T, int rel, int64_t n, int pass, const int64_t* offs, int64_t* cnt,
                  int64_t* leaves, int* err, cudaStream_t st) {

@@ -193,6 +193,7 @@ struct PackPlan {
   uint8_t shift[8];
   const int32_t* sample;  // null for shared
   uint8_t sshift;
+  int32_t s_lo, s_hi;     // micro-batch: samples outside [s_lo, s_hi) -> dead key; sample - s_lo packed
 };
 void launch_pack(const PackPlan& pp, int64_t n, uint64_t* key, uint32_t* rowid, cudaStream_t st);
 // gather p / fid by rowid
@@ -329,6 +330,10 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
 // ---- output extract (A12) ----
 void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,
                    const uint8_t* bits, const int32_t* mins, int32_t* sample, int32_t* cols, cudaStream_t st);
+// micro-batch output collection helpers
+void launch_add_i32(int32_t* a, int64_t n, int32_t v, cudaStream_t st);
+void launch_add_i64(const int64_t* s, int64_t n, int64_t v, int64_t* d, cudaStream_t st);
+void launch_sample_offsets_i32(const int32_t* sid, int64_t n, int32_t batch, int64_t* off, cudaStream_t st);
 void launch_sample_offsets(const uint64_t* key, int64_t n, int32_t batch, uint8_t sshift, int has_sample,
                            int64_t* off, cudaStream_t st);
 

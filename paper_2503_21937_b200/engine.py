@@ -88,7 +88,7 @@ class Engine:
     """One lobster context: program_load -> facts_push* -> run -> output_get*."""
 
     def __init__(self, program: str, semiring: int, batch_size: int = 1, device: int = 0,
-                 stream: Optional[int] = None, max_iters: int = 0, arena_bytes: int = 0):
+                 stream: Optional[int] = None, max_iters: int = 0, arena_bytes: int = 0, micro_batch: int = 0):
         self._L = _lib.load()
         o = _lib.Options()
         o.device = device
@@ -96,6 +96,7 @@ class Engine:
         o.batch_size = batch_size
         o.max_iters = max_iters
         o.arena_bytes = arena_bytes
+        o.micro_batch = micro_batch
         self.batch_size = batch_size
         self.semiring = semiring
         h = ctypes.c_void_p()
