@@ -1,15 +1,19 @@
 #!/usr/bin/env python
-"""Benchmark: derived tuples/s of the semi-naive fixpoint on config C2
-(BASELINE.json configs[1]: Pathfinder-shaped 32x32 grids, batch 64 per GPU,
-max-min-prob and diff-max-mult-prob with input-fact gradients).
+"""Benchmark: derived tuples/s of the semi-naive fixpoint.
+
+Default workload = config C2 (BASELINE.json configs[1]: Pathfinder-shaped 32x32
+grids, batch 64 per GPU, max-min-prob and diff-max-mult-prob with input-fact
+gradients).  `--config C1|C3|C4|C5` measures the other BASELINE configs the
+same way (C5 = the 512-sample per-GPU shard of the 4096 batch).
 
 One step = one pass of the whole hot path over one
-batch: ingest (facts already in HBM) -> fixpoint under max-min-prob -> fixpoint
-under diff-max-mult-prob -> witness walk + gradients -> dense dL/dp contraction;
-with N > 1 ranks also all-gather of per-sample outputs and all-reduce of the
-input-fact gradient (NCCL).  Weak scaling: every rank owns 64 samples.
+batch: ingest (facts already in HBM) -> fixpoint under each of the config's
+semirings -> (diff-max-mult) witness walk + gradients -> dense dL/dp
+contraction; with N > 1 ranks also the NCCL all-gather of per-sample output
+records and the all-reduce of the input-fact gradient.  Weak scaling: every
+rank owns its own samples.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lobster|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl lobster|reference]
 
 Prints one JSON line (rank 0).  See DESIGN.md "Measurement".
 """
@@ -30,13 +34,43 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
+from workloads import gen as G  # noqa: E402
 
-BATCH_PER_GPU = 64
-GRID_N = 32
 METRIC = "derived tuples/s"
 UNIT = "tuples/s"
-WORKLOAD = ("C2: Pathfinder-shaped 32x32 lattice connectivity (Fig. 3c program), batch 64 per GPU, "
-            "max-min-prob + diff-max-mult-prob with input-fact gradients")
+
+
+def _rank_batch(make, per_gpu, rank):
+    """This rank's samples (global ids per_gpu*rank ...), pushed with local ids."""
+    samples = list(range(per_gpu * rank, per_gpu * (rank + 1)))
+    w = make(per_gpu * (rank + 1), samples)
+    for f in w.facts.values():
+        if f.sample_ids is not None and "samples" in (w.meta or {}):
+            f.sample_ids = (np.asarray(f.sample_ids) - per_gpu * rank).astype(np.int32)
+    w.batch_size = per_gpu
+    return w
+
+
+CONFIGS = {
+    "C2": dict(per_gpu=64, semirings=[G.MAX_MIN_PROB, G.DIFF_MAX_MULT_PROB], out="endpoints_connected",
+               make=lambda b, s: G.grid_workload(32, b, 2, G.DIFF_MAX_MULT_PROB, samples=s, name="C2"),
+               desc="C2: Pathfinder-shaped 32x32 lattice connectivity (Fig. 3c program), batch 64 per GPU, "
+                    "max-min-prob + diff-max-mult-prob with input-fact gradients"),
+    "C1": dict(per_gpu=1, semirings=[G.ADD_MULT_PROB], out="path",
+               make=lambda b, s: G.c1_workload(G.ADD_MULT_PROB),
+               desc="C1: transitive closure over the 6-node dyadic DAG, add-mult-prob (latency-bound)"),
+    "C3": dict(per_gpu=256, semirings=[G.ADD_MULT_PROB], out="answer",
+               make=lambda b, s: G.c3_workload(G.ADD_MULT_PROB, samples=s, batch=b),
+               desc="C3: CLUTRR-shaped kinship composition, 20 entities x 20 relation types, batch 256 per GPU, "
+                    "add-mult-prob"),
+    "C4": dict(per_gpu=1024, semirings=[G.UNIT], out="reach",
+               make=lambda b, s: G.c4_workload(G.UNIT, samples=s, batch=b),
+               desc="C4: unit reachability over a shared 100k-node / 1M-edge Chung-Lu graph, 1024 sources per GPU"),
+    "C5": dict(per_gpu=512, semirings=[G.DIFF_MAX_MULT_PROB], out="endpoints_connected",
+               make=lambda b, s: G.grid_workload(64, b, 5, G.DIFF_MAX_MULT_PROB, samples=s, name="C5"),
+               desc="C5: 64x64 lattice connectivity, 512 samples per GPU (the 8-GPU shard of the 4096 batch), "
+                    "diff-max-mult-prob with input-fact gradients"),
+}
 
 
 def parse():
@@ -44,6 +78,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="lobster", choices=["lobster", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -106,18 +141,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-# ------------------------------------------------------------------ workload
-def make_batch(rank: int):
-    """This rank's 64 samples (global ids 64*rank ...); pushed with local ids."""
-    samples = list(range(BATCH_PER_GPU * rank, BATCH_PER_GPU * (rank + 1)))
-    w = W.grid_workload(GRID_N, BATCH_PER_GPU * (rank + 1), 2, W.gen.DIFF_MAX_MULT_PROB, samples=samples, name="C2")
-    for f in w.facts.values():
-        if f.sample_ids is not None:
-            f.sample_ids = (f.sample_ids - BATCH_PER_GPU * rank).astype(np.int32)
-    w.batch_size = BATCH_PER_GPU
-    return w
-
-
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -137,41 +160,52 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------ cpu baseline
-def cpu_baseline(threads: int, semiring: int, nsamples: int):
+def cpu_baseline(cfg_name: str, threads: int, sr_index: int = -1, nsamples: int = 0):
+    """The oracle, as it stands, on a bounded sample of the config's workload;
+    one sample per thread.  Returns (tuples, seconds, description)."""
     import oracle
-    w = W.grid_workload(GRID_N, BATCH_PER_GPU, 2, semiring, samples=list(range(nsamples)), name="C2")
+    cfg = CONFIGS[cfg_name]
+    sr = cfg["semirings"][sr_index]
+    n = nsamples or max(1, min(threads, cfg["per_gpu"]))
+    if cfg_name == "C4":
+        n = min(n, 8)
+    w = cfg["make"](cfg["per_gpu"], list(range(n)))
+    if cfg_name == "C1":
+        n = 1
+    reps = 200 if cfg_name == "C1" else 1  # C1 is one 14-tuple problem: repeat it
     t = time.perf_counter()
-    res = oracle.run(w.program, semiring, w.batch_size, w.facts, outputs=["path", "endpoints_connected"],
-                     samples=list(range(nsamples)), threads=threads)
+    for _ in range(reps):
+        res = oracle.run(w.program, sr, w.batch_size, w.facts, samples=list(range(n)), threads=threads)
     dt = time.perf_counter() - t
-    tuples = sum(len(r) for r in res.relations.values())
-    return tuples, dt
+    tuples = reps * sum(len(r) for r in res.relations.values())
+    return tuples, dt, (f"{n} of the {cfg['per_gpu']} {cfg_name} samples under semiring {sr} (one per thread)"
+                        + (f", repeated {reps}x" if reps > 1 else ""))
 
 
 def run_reference(args):
     """--impl reference: the oracle (CPU), as it stands, on a bounded sample of
-    C2 per step; rank 0 only."""
+    the config per step; rank 0 only (other ranks exit without work)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    cfg = CONFIGS[args.config]
     cores = os.cpu_count() or 1
-    nsamp = max(1, min(cores, BATCH_PER_GPU))
-    sr_cycle = [W.gen.MAX_MIN_PROB, W.gen.DIFF_MAX_MULT_PROB]
-    for i in range(args.warmup):
-        cpu_baseline(nsamp, sr_cycle[i % 2], 1)  # warm-up on one sample
-    tot_t, tot_tuples = 0.0, 0
+    threads = max(1, min(cores, cfg["per_gpu"]))
+    nsr = len(cfg["semirings"])
+    for i in range(args.warmup):  # warm-up on one sample
+        cpu_baseline(args.config, 1, i % nsr, 1)
+    tot_t, tot_tuples, desc = 0.0, 0, ""
     for i in range(args.steps):
-        tuples, dt = cpu_baseline(nsamp, sr_cycle[i % 2], nsamp)
+        tuples, dt, desc = cpu_baseline(args.config, threads, i % nsr)
         tot_t += dt
         tot_tuples += tuples
     v = tot_tuples / tot_t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": BATCH_PER_GPU},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nsamp, "kind": "oracle",
-                             "sample": f"{nsamp} of the 64 C2 samples per step (one per thread), semiring "
-                                       f"alternating max-min / diff-max-mult by step"},
+            "data": "synthetic", "config": {"workload": cfg["desc"], "global_batch": cfg["per_gpu"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": desc + "; semirings alternate by step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -183,8 +217,11 @@ def main():
         return run_reference(args)
     import torch
     import torch.distributed as dist
-    from paper_2503_21937_b200 import DIFF_MAX_MULT_PROB, MAX_MIN_PROB, Engine, _lib
+    from paper_2503_21937_b200 import DIFF_MAX_MULT_PROB, Engine, _lib
+    from paper_2503_21937_b200 import dist as D
 
+    cfg = CONFIGS[args.config]
+    per_gpu = cfg["per_gpu"]
     ws, rank, local = dist_env()
     if ws > 1:
         dist.init_process_group("nccl", init_method="env://")
@@ -192,50 +229,48 @@ def main():
     dev = torch.device("cuda", local)
     L = _lib.load()
 
-    w = make_batch(rank)
+    w = _rank_batch(cfg["make"], per_gpu, rank)
     # device-resident inputs (value) and pinned host inputs (e2e)
     dfacts, hfacts, h2d = {}, {}, 0
     for rel, f in w.facts.items():
         cols_d = [torch.as_tensor(c).to(dev) for c in f.cols]
         cols_h = [torch.as_tensor(c).pin_memory() for c in f.cols]
-        s_d = torch.as_tensor(f.sample_ids).to(dev)
-        s_h = torch.as_tensor(f.sample_ids).pin_memory()
+        s_d = None if f.sample_ids is None else torch.as_tensor(f.sample_ids).to(dev)
+        s_h = None if f.sample_ids is None else torch.as_tensor(f.sample_ids).pin_memory()
         p_d = torch.as_tensor(f.probs).to(dev)
         p_h = torch.as_tensor(f.probs).pin_memory()
         dfacts[rel] = W.Facts(cols_d, s_d, p_d)
         hfacts[rel] = W.Facts(cols_h, s_h, p_h)
-        h2d += sum(c.numel() * 4 for c in cols_h) + s_h.numel() * 4 + p_h.numel() * 4
-    h2d *= 2  # pushed once per semiring
+        h2d += sum(c.numel() * 4 for c in cols_h) + (0 if s_h is None else s_h.numel() * 4) + p_h.numel() * 4
+    h2d *= len(cfg["semirings"])  # pushed once per semiring
 
-    engines = {sr: Engine(w.program, sr, batch_size=BATCH_PER_GPU, device=local)
-               for sr in (MAX_MIN_PROB, DIFF_MAX_MULT_PROB)}
+    engines = {sr: Engine(w.program, sr, batch_size=per_gpu, device=local) for sr in cfg["semirings"]}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     nfacts = w.n_facts()
     grad_dense = torch.zeros(nfacts * ws, dtype=torch.float32, device=dev)
+    rel = cfg["out"]
+    arity0 = rel in ("endpoints_connected",)
 
     def step(facts, host_out=False):
         stats, d2h = [], 0
-        grad_dense.zero_()
         for sr, eng in engines.items():
             eng.push_facts(facts)
             stats.append(eng.run())
-        em = engines[DIFF_MAX_MULT_PROB]
-        out_dev = em.output("endpoints_connected", device=True)
-        up = torch.ones(out_dev.n, dtype=torch.float32, device=dev)
-        g = grad_dense[rank * nfacts:(rank + 1) * nfacts]
-        em.backward("endpoints_connected", up, g)
-        rec = torch.zeros(2 * BATCH_PER_GPU, dtype=torch.float32, device=dev)  # per-sample (present, p)
-        if out_dev.n:
-            rec[2 * out_dev.sample_ids.long()] = 1.0
-            rec[2 * out_dev.sample_ids.long() + 1] = out_dev.probs
-        if ws > 1:
-            allrec = torch.empty(ws * rec.numel(), dtype=rec.dtype, device=dev)
-            dist.all_gather_into_tensor(allrec, rec)
-            dist.all_reduce(grad_dense)
+        if DIFF_MAX_MULT_PROB in engines:
+            em = engines[DIFF_MAX_MULT_PROB]
+            out_dev = em.output(rel, device=True)
+            grad_dense.zero_()
+            em.backward(rel, torch.ones(out_dev.n, dtype=torch.float32, device=dev),
+                        grad_dense[rank * nfacts:(rank + 1) * nfacts])
+            if ws > 1:
+                rec = D.arity0_records(out_dev.sample_ids, out_dev.probs, per_gpu, device=dev) if arity0 else \
+                    torch.zeros(2 * per_gpu, device=dev)
+                D.all_gather_records(rec)
+                D.all_reduce_grad(grad_dense)
         if host_out:  # e2e: results back to the host through the C ABI
             for sr, eng in engines.items():
-                o = eng.output("endpoints_connected", device=False)
-                d2h += o.n * 8 + o.sample_offsets.nbytes
+                o = eng.output(rel, device=False)
+                d2h += o.n * 4 * (1 + o.arity) + o.sample_offsets.nbytes
                 if o.probs is not None:
                     d2h += o.probs.nbytes
                 if o.grad_values is not None:
@@ -247,7 +282,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 0)):
         step(dfacts)
     barrier()
 
@@ -280,7 +315,6 @@ def main():
     cands_step = sum(s["candidates"] for s in stats_all[-1])
     ms_step = total_ms / args.steps
     value = tuples_step * ws / (ms_step / 1000.0)
-    # phase breakdown (engine CUDA events, summed over both semirings, last step)
     ph = {k: sum(s[k] for s in stats_all[-1]) for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge", "ms_grad")}
     peak, peak_src = peaks()
     # Dominant kernel: the fused row-centric join + direct ⊕ (join_rows_direct_k).
@@ -288,34 +322,34 @@ def main():
     # (candidate write + re-read for dedup), r = packed key (4 B) + tag bytes;
     # duration = the engine's CUDA events around each launch, on its stream,
     # summed over the timed steps (averaged per launch).
-    last = stats_all  # every timed step
-    fj_l = sum(s["fj_launches"] for st in last for s in st)
-    fj_ms = sum(s["ms_fused_join"] for st in last for s in st)
+    fj_l = sum(s["fj_launches"] for st in stats_all for s in st)
+    fj_ms = sum(s["ms_fused_join"] for st in stats_all for s in st)
     fj_b = sum(s["fj_probe_rows"] * s["fj_row_bytes"] + 2 * s["fj_candidates"] * s["fj_row_bytes"]
-               for st in last for s in st)
-    tr = ncu_traffic()
+               for st in stats_all for s in st)
+    tr = ncu_traffic() if args.config == "C2" else {}
     if fj_l and fj_ms > 0:
         achieved = fj_b / fj_l / (fj_ms / fj_l / 1000.0) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr.get("dram_bytes_per_launch"),
                     "kernel": "join_rows_direct_k (fused count-free join + ⊗ + direct ⊕ into the dense store)",
-                    "launches_per_step": fj_l / len(last), "avg_launch_us": 1000.0 * fj_ms / fj_l,
+                    "launches_per_step": fj_l / len(stats_all), "avg_launch_us": 1000.0 * fj_ms / fj_l,
                     "alg_bytes_per_launch": fj_b / fj_l,
                     "alg_bytes_def": "SURVEY §8(d): |Δ|·r + 2·|C|·r per launch, r = 4 B key + tag (8 B max-mult)",
                     "traffic_source": tr.get("source"), "peak_source": peak_src}
     else:
         bytes_alg = sum(s["bytes_algorithmic"] for s in stats_all[-1])
-        t_alg = sum(ph[k] for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge")) / 1000.0
+        t_alg = max(1e-9, sum(ph[k] for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge")) / 1000.0)
         achieved = bytes_alg / t_alg / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": "fixpoint phases (no fused join launched)", "peak_source": peak_src}
+                    "traffic": None, "kernel": "fixpoint phases (SURVEY §8(d) B_alg / summed phase time)",
+                    "peak_source": peak_src}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": BATCH_PER_GPU * ws, "grid": f"{GRID_N}x{GRID_N}",
+            "config": {"workload": cfg["desc"], "name": args.config, "global_batch": per_gpu * ws,
                        "parallelism": f"dp{ws} (batch sharded, no collective inside the fixpoint)",
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "samples_per_s": BATCH_PER_GPU * ws / (ms_step / 1000.0),
+            "samples_per_s": per_gpu * ws / (ms_step / 1000.0),
             "candidates_per_s": cands_step * ws / (ms_step / 1000.0),
             "tuples_per_step": tuples_step * ws, "rounds_per_step": sum(s["rounds_total"] for s in stats_all[-1]),
             "phases_ms": ph, "gpu_launches": launches, "roofline": roofline}
@@ -324,13 +358,11 @@ def main():
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": e2e_d2h,
                        "ms_per_step": e2e_ms / args.steps}
     line["clocks"] = clk.summary()
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config != "C5":
         cores = os.cpu_count() or 1
-        ns = max(1, min(cores, 16))
-        tuples, dt = cpu_baseline(ns, W.gen.DIFF_MAX_MULT_PROB, ns)
-        line["cpu_baseline"] = {"value": tuples / dt, "unit": UNIT, "cores": ns, "kind": "oracle",
-                                "sample": f"{ns} of the 64 C2 samples under diff-max-mult-prob "
-                                          f"(one sample per thread), {dt:.1f} s wall"}
+        tuples, dt, desc = cpu_baseline(args.config, max(1, min(cores, 16)))
+        line["cpu_baseline"] = {"value": tuples / dt, "unit": UNIT, "cores": max(1, min(cores, 16)),
+                                "kind": "oracle", "sample": f"{desc}, {dt:.1f} s wall"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     for e in engines.values():

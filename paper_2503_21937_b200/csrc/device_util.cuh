@@ -117,6 +117,55 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
   if (app) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
 }
 
+// Batched direct ⊕ for a thread's independent candidates (no pre-reduction).
+// direct_pack: the candidate's value in the store's packed word (unit: the bit
+// within its 32-bit bitmap word).  direct_peek: a plain L2 read of the word —
+// the store only grows (atomicMax / OR), so a stale read is a lower bound and
+// a candidate not above it can never improve the slot.  direct_commit issues
+// the remaining atomics back to back, then marks each slot's first improver
+// dirty (the settled bit of the pre-atomic word says "first this round").
+__device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slot, float t, uint32_t w) {
+  if (semi == S_UNIT) return 1ull << (slot & 31u);
+  if (semi == S_MAXMIN) return (unsigned long long)((f2u(t) + 1u) << 1);
+  return ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
+}
+
+__device__ __forceinline__ unsigned long long direct_peek(int semi, const void* f, uint32_t slot) {
+  if (semi == S_UNIT) return __ldcg(reinterpret_cast<const uint32_t*>(f) + (slot >> 5));
+  if (semi == S_MAXMIN) return __ldcg(reinterpret_cast<const uint32_t*>(f) + slot);
+  return __ldcg(reinterpret_cast<const unsigned long long*>(f) + slot);
+}
+
+template <int N>
+__device__ __forceinline__ void direct_commit(int semi, void* f, uint32_t* dirty, const uint32_t* slotv,
+                                              const unsigned long long* newv, unsigned long long* oldv, bool* live) {
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    if (!live[d]) continue;
+    const unsigned long long v = newv[d];
+    if (semi == S_UNIT) {
+      if (oldv[d] & v) { live[d] = false; continue; }
+      oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(f) + (slotv[d] >> 5), (uint32_t)v);
+    } else if (semi == S_MAXMIN) {
+      if (v <= oldv[d]) { live[d] = false; continue; }
+      oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(f) + slotv[d], (uint32_t)v);
+    } else {
+      if (v <= oldv[d]) { live[d] = false; continue; }
+      oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(f) + slotv[d], v);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    if (!live[d]) continue;
+    const unsigned long long old = oldv[d], v = newv[d];
+    bool first;
+    if (semi == S_UNIT) first = !(old & v);
+    else if (semi == S_MAXMIN) first = old < v && (old == 0ull || (old & 1ull));
+    else first = old < v && (old == 0ull || ((old >> 32) & 1ull));
+    if (first) atomicOr(dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
+  }
+}
+
 inline int grid_for(int64_t n, int threads, int cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;

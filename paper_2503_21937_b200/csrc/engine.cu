@@ -166,6 +166,7 @@ struct Index {
   int64_t nprefix = 0;
   int free_bits = 0, prefix_bits = 0;
   int64_t maxdeg = -1;  // max rows per prefix (static CSR indexes), -1 unknown
+
   bool has_sample = false;
   int sshift = 0, sbits = 0;
   std::vector<int> col_shift, col_bits;
@@ -1164,7 +1165,7 @@ struct Ctx {
     uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
     {
       Phase ph(this, 2);
-      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 1), st);
+      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 2), st);
       kcheck("seg reduce");
     }
     uint64_t* flags = arena.get<uint64_t>(nu);
@@ -1363,7 +1364,7 @@ struct Ctx {
     uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
     {
       Phase ph(this, 2);
-      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 1), st);
+      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 2), st);
       kcheck("seg reduce");
     }
     uint64_t* flags = arena.get<uint64_t>(nu);

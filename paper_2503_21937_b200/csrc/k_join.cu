@@ -61,15 +61,6 @@ constexpr int WT = 2048;    // output slots per CTA (8 per thread)
 constexpr int WROWS = 2048; // probe-row offsets staged in shared memory
 constexpr int SPT = WT / 256;
 
-__device__ __forceinline__ int smem_row(const int64_t* s, int n, int64_t o) {
-  int lo = 0, hi = n;  // largest i with s[i] <= o
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (s[mid] <= o) lo = mid + 1; else hi = mid;
-  }
-  return lo - 1;
-}
-
 // ⊗ in body order over T = [ptag[0..npt-1], btag] (reading 9).  Fast path:
 // one probe tag followed by the build tag (every linear TC-shaped rule).
 __device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int64_t row, int64_t j) {
@@ -82,50 +73,77 @@ __device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int64_t row, 
   return t;
 }
 
+// Largest r in [lo, hi) with offs[r] <= o (offs non-decreasing, offs[lo] <= o),
+// found by the whole CTA: each round 256 threads probe 256 evenly spaced rows
+// and __syncthreads_count narrows the range 256x (3 rounds for 10^7 rows)
+// instead of one thread walking ~24 dependent loads while the CTA waits.
+__device__ __forceinline__ int64_t coop_row(const int64_t* __restrict__ offs, int64_t o, int64_t lo, int64_t hi) {
+  while (hi - lo > 1) {
+    const int64_t stride = (hi - lo + 255) >> 8;
+    const int64_t idx = lo + (int64_t)threadIdx.x * stride;
+    const int c = __syncthreads_count(idx < hi && __ldg(offs + idx) <= o);
+    const int64_t nlo = lo + (int64_t)(c - 1) * stride;
+    hi = nlo + stride < hi ? nlo + stride : hi;
+    lo = nlo;
+  }
+  return lo;
+}
+
 template <typename PK, typename OK>
 __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int64_t* __restrict__ offs,
                                                     const int64_t* __restrict__ start, int64_t total) {
-  __shared__ int64_t soff[WROWS];
-  __shared__ int64_t r0s, r1s;
+  // the tile's probe rows, staged: row start relative to the tile (only row 0
+  // can start before it: clamped to -1), build-index delta start - offs (so a
+  // slot's build row is j = sdel + o) and the probe key
+  __shared__ int32_t soff[WROWS];
+  __shared__ int64_t sdel[WROWS];
+  __shared__ PK spk[WROWS];
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   OK* __restrict__ okey = reinterpret_cast<OK*>(jp.okey);
   const int64_t o0 = (int64_t)blockIdx.x * WT;
   if (o0 >= total) return;
   const int64_t o1 = (o0 + WT < total ? o0 + WT : total) - 1;
-  if (threadIdx.x == 0) {
-    r0s = upper_bound_m1_i64(offs, jp.np, o0);
-    r1s = upper_bound_m1_i64(offs, jp.np, o1);
-  }
-  __syncthreads();
-  const int64_t r0 = r0s, r1 = r1s;
+  const int64_t r0 = coop_row(offs, o0, 0, jp.np);
+  const int64_t r1 = coop_row(offs, o1, r0, jp.np);
   const int nrows = (int)(r1 - r0 + 1);
   const bool staged = r1 - r0 + 1 <= WROWS;
   if (staged)
-    for (int i = threadIdx.x; i < nrows; i += blockDim.x) soff[i] = offs[r0 + i];
+    for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
+      const int64_t of = offs[r0 + i];
+      soff[i] = of < o0 ? -1 : (int32_t)(of - o0);
+      sdel[i] = start[r0 + i] - of;
+      spk[i] = pkey[r0 + i];
+    }
   __syncthreads();
   // phase 1: resolve every slot of this thread (independent loads in flight)
   int64_t rowv[SPT], jv[SPT];
+  PK pkv[SPT];
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     const int64_t o = o0 + threadIdx.x + k * 256;
     rowv[k] = -1;
     if (o > o1) continue;
-    int64_t row, base;
     if (staged) {
-      const int r = smem_row(soff, nrows, o);
-      row = r0 + r;
-      base = soff[r];
+      const int32_t lo32 = (int32_t)(o - o0);
+      int lo = 0, hi = nrows;  // largest i with soff[i] <= o - o0
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (soff[mid] <= lo32) lo = mid + 1; else hi = mid;
+      }
+      rowv[k] = r0 + lo - 1;
+      jv[k] = sdel[lo - 1] + o;
+      pkv[k] = spk[lo - 1];
     } else {
       int64_t lo = r0, hi = r1 + 1;
       while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
         if (offs[mid] <= o) lo = mid + 1; else hi = mid;
       }
-      row = lo - 1;
-      base = offs[row];
+      const int64_t row = lo - 1;
+      rowv[k] = row;
+      jv[k] = start[row] + (o - offs[row]);
+      pkv[k] = pkey[row];
     }
-    rowv[k] = row;
-    jv[k] = o - base;
   }
   uint64_t keyv[SPT];
   float tv[SPT];
@@ -136,9 +154,8 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
     okv[k] = false;
     if (rowv[k] < 0) continue;
     const int64_t row = rowv[k];
-    const int64_t j = start[row] + jv[k];
-    jv[k] = j;
-    const uint64_t pk = (uint64_t)pkey[row];
+    const int64_t j = jv[k];
+    const uint64_t pk = (uint64_t)pkv[k];
     const uint64_t bk = jp.bkey[j];
     bool ok = true;
     for (int e = 0; e < jp.nfeq; ++e) {
@@ -161,36 +178,20 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
   }
   // phase 2: emit
   if (jp.direct) {  // fused A5-A8: ⊕ straight into the direct-mapped store
-    if (!jp.aggregate && jp.semi != S_UNIT) {
-      // issue all of this thread's atomics before consuming any result
+    if (!jp.aggregate) {
+      // stale-read filter, then this thread's remaining atomics back to back
       unsigned long long oldv[SPT], newv[SPT];
+      uint32_t slotv[SPT];
+      bool live[SPT];
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        newv[k] = 0ull;
-        oldv[k] = ~0ull;
-        if (rowv[k] < 0 || !okv[k]) continue;
-        const uint32_t slot = (uint32_t)keyv[k];
-        if (jp.semi == S_MAXMIN) {
-          const uint32_t v = (f2u(tv[k]) + 1u) << 1;
-          newv[k] = v;
-          oldv[k] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slot, v);
-        } else {
-          const unsigned long long v = ((unsigned long long)(f2u(tv[k]) + 1u) << 33) | (unsigned long long)(~wv[k]);
-          newv[k] = v;
-          oldv[k] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slot, v);
-        }
+        live[k] = rowv[k] >= 0 && okv[k];
+        if (!live[k]) continue;
+        slotv[k] = (uint32_t)keyv[k];
+        newv[k] = direct_pack(jp.semi, slotv[k], tv[k], wv[k]);
+        oldv[k] = direct_peek(jp.semi, jp.fdir, slotv[k]);
       }
-      // the unique first improver of a slot marks it dirty (no shared counter)
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        const unsigned long long old = oldv[k], v = newv[k];
-        const bool settled_or_absent =
-            jp.semi == S_MAXMIN ? (old == 0ull || (old & 1ull)) : (old == 0ull || ((old >> 32) & 1ull));
-        if (rowv[k] >= 0 && okv[k] && old < v && settled_or_absent) {
-          const uint32_t slot = (uint32_t)keyv[k];
-          atomicOr(jp.dirty + (slot >> 5), 1u << (slot & 31u));
-        }
-      }
+      direct_commit<SPT>(jp.semi, jp.fdir, jp.dirty, slotv, newv, oldv, live);
     } else {
 #pragma unroll
       for (int k = 0; k < SPT; ++k)
@@ -255,8 +256,16 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // static CSR index has <= MAXDEG rows, e.g. lattice edges: 4).  One thread per
 // probe row: coalesced probe key / tag loads, its matches unrolled, all
 // atomics issued before any result is consumed.  No count / scan / host sync.
+// One thread per probe row, <= MAXDEG candidates each.  Measured on C2 and
+// rejected: two rows per thread (152 vs 101 us per launch: fewer resident
+// warps for the same requests in flight), phase A/B through the generic
+// direct_pack/peek/commit helpers (+5%), a fixed-width ELL copy of the build
+// index replacing boff -> bkey (+3%: boff hits L1).
+#ifndef FJ_MINB
+#define FJ_MINB 6
+#endif
 template <typename PK, int MAXDEG>
-__global__ void __launch_bounds__(256, (MAXDEG <= 4) ? 6 : 4) join_rows_direct_k(const JoinPlan jp,
+__global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_direct_k(const JoinPlan jp,
                                                           unsigned long long* __restrict__ ncand) {
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   uint32_t mycount = 0;

@@ -126,9 +126,12 @@ __global__ void edb_reduce_k(const uint64_t* __restrict__ key, const float* __re
 // U = segmented ⊕ of sorted candidates (A7).  Segment boundaries come from
 // the head flags' scan (pos); uend[u] = one past the last element of segment u.
 // Short segments: one thread each, left-to-right.  Long segments (> LONG_SEG,
-// e.g. the per-sample `endpoints_connected()` groups of ~1M candidates): one
-// CTA each, strided partials combined by a fixed-shape tree (deterministic).
+// e.g. a C3 kinship head's per-round contributions): one warp each.  Huge
+// segments (> HUGE_SEG, e.g. the per-sample `endpoints_connected()` groups of
+// ~1M candidates): one CTA each.  Warp/CTA partials are strided folds combined
+// by a fixed-shape tree, so the result is deterministic.
 constexpr int LONG_SEG = 64;
+constexpr int HUGE_SEG = 4096;
 
 template <typename K>
 __global__ void seg_ends_k(const K* __restrict__ key, const uint32_t* __restrict__ pos, int64_t n,
@@ -193,8 +196,9 @@ __global__ void seg_reduce_short_k(const K* __restrict__ key, const void* __rest
     const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
     ukey[u] = key[s];
     if constexpr (SEMI == S_UNIT) continue;
-    if (e - s > LONG_SEG) {
-      longs[atomicAdd(nlong, 1u)] = (uint32_t)u;
+    if (e - s > LONG_SEG) {  // warp list from the front, CTA list from the back
+      if (e - s > HUGE_SEG) longs[nu - 1 - atomicAdd(nlong + 1, 1u)] = (uint32_t)u;
+      else longs[atomicAdd(nlong, 1u)] = (uint32_t)u;
       continue;
     }
     Acc a = acc_load<SEMI>(valv, s);
@@ -204,25 +208,53 @@ __global__ void seg_reduce_short_k(const K* __restrict__ key, const void* __rest
 }
 
 template <int SEMI>
-__global__ void __launch_bounds__(256) seg_reduce_long_k(const void* __restrict__ valv,
+__device__ __forceinline__ Acc acc_shfl_down(Acc a, int off) {
+  Acc b;
+  b.s = __shfl_down_sync(0xffffffffu, a.s, off);
+  b.p = __shfl_down_sync(0xffffffffu, a.p, off);
+  b.w = __shfl_down_sync(0xffffffffu, a.w, off);
+  return b;
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256) seg_reduce_warp_k(const void* __restrict__ valv,
                                                          const uint32_t* __restrict__ uend,
                                                          const uint32_t* __restrict__ nlong,
                                                          const uint32_t* __restrict__ longs, float* __restrict__ up,
                                                          uint32_t* __restrict__ uw) {
-  __shared__ Acc part[256];
-  const uint32_t nl = *nlong;
-  for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+  const uint32_t nl = nlong[0];
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nl; q += nw) {
     const uint32_t u = longs[q];
     const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
-    // thread t folds elements s+t, s+t+256, ... in order (every long segment
-    // has more than 256 > LONG_SEG elements or at least LONG_SEG+1: guard)
-    Acc a = acc_load<SEMI>(valv, s + threadIdx.x < e ? s + threadIdx.x : s);
+    // lane t folds s+t, s+t+32, ... in order (e - s > LONG_SEG >= 32)
+    Acc a = acc_load<SEMI>(valv, s + lane);
+    for (int64_t j = s + lane + 32; j < e; j += 32) a = acc_join<SEMI>(a, acc_load<SEMI>(valv, j));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) a = acc_join<SEMI>(a, acc_shfl_down<SEMI>(a, off));
+    if (lane == 0) acc_store<SEMI>(a, u, up, uw);
+  }
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256) seg_reduce_long_k(const void* __restrict__ valv,
+                                                         const uint32_t* __restrict__ uend,
+                                                         const uint32_t* __restrict__ nlong, int64_t nu,
+                                                         const uint32_t* __restrict__ longs, float* __restrict__ up,
+                                                         uint32_t* __restrict__ uw) {
+  __shared__ Acc part[256];
+  const uint32_t nl = nlong[1];
+  for (uint32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+    const uint32_t u = longs[nu - 1 - q];
+    const int64_t s = u ? (int64_t)uend[u - 1] : 0, e = uend[u];
+    // thread t folds elements s+t, s+t+256, ... in order (e - s > HUGE_SEG >= 256)
+    Acc a = acc_load<SEMI>(valv, s + threadIdx.x);
     for (int64_t j = s + threadIdx.x + 256; j < e; j += 256) a = acc_join<SEMI>(a, acc_load<SEMI>(valv, j));
     part[threadIdx.x] = a;
     __syncthreads();
-    const int cnt = (int)((e - s) < 256 ? (e - s) : 256);
     for (int d = 1; d < 256; d <<= 1) {  // fixed pairwise tree over the thread partials
-      if ((threadIdx.x % (2 * d)) == 0 && threadIdx.x + d < cnt)
+      if ((threadIdx.x % (2 * d)) == 0)
         part[threadIdx.x] = acc_join<SEMI>(part[threadIdx.x], part[threadIdx.x + d]);
       __syncthreads();
     }
@@ -649,9 +681,9 @@ void seg_reduce_impl(const K* key, const void* val, const uint32_t* pos, int64_t
                      float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st) {
   if (n <= 0 || nu <= 0) return;
   uint32_t* uend = scratch;            // nu
-  uint32_t* nlong = scratch + nu;      // 1
-  uint32_t* longs = scratch + nu + 1;  // nu
-  cudaMemsetAsync(nlong, 0, 4, st);
+  uint32_t* nlong = scratch + nu;      // 2: [0] warp list, [1] CTA list
+  uint32_t* longs = scratch + nu + 2;  // nu: warp list from the front, CTA list from the back
+  cudaMemsetAsync(nlong, 0, 8, st);
   note_launch();
   seg_ends_k<K><<<grid_for(n, 256), 256, 0, st>>>(key, pos, n, uend);
   const int g = grid_for(nu, 256);
@@ -670,12 +702,22 @@ void seg_reduce_impl(const K* key, const void* val, const uint32_t* pos, int64_t
       seg_reduce_short_k<K, S_MAXMULT><<<g, 256, 0, st>>>(key, val, uend, nu, ukey, up, uw, nlong, longs);
       break;
   }
-  const int gl = 148 * 4;
+  const int gw = grid_for((nu + 7) / 8, 1, 148 * 8), gl = 148 * 4;
+  note_launch();
   note_launch();
   switch (semi) {
-    case S_MAXMIN: seg_reduce_long_k<S_MAXMIN><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
-    case S_ADDMULT: seg_reduce_long_k<S_ADDMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
-    default: seg_reduce_long_k<S_MAXMULT><<<gl, 256, 0, st>>>(val, uend, nlong, longs, up, uw); break;
+    case S_MAXMIN:
+      seg_reduce_warp_k<S_MAXMIN><<<gw, 256, 0, st>>>(val, uend, nlong, longs, up, uw);
+      seg_reduce_long_k<S_MAXMIN><<<gl, 256, 0, st>>>(val, uend, nlong, nu, longs, up, uw);
+      break;
+    case S_ADDMULT:
+      seg_reduce_warp_k<S_ADDMULT><<<gw, 256, 0, st>>>(val, uend, nlong, longs, up, uw);
+      seg_reduce_long_k<S_ADDMULT><<<gl, 256, 0, st>>>(val, uend, nlong, nu, longs, up, uw);
+      break;
+    default:
+      seg_reduce_warp_k<S_MAXMULT><<<gw, 256, 0, st>>>(val, uend, nlong, longs, up, uw);
+      seg_reduce_long_k<S_MAXMULT><<<gl, 256, 0, st>>>(val, uend, nlong, nu, longs, up, uw);
+      break;
   }
 }
 

@@ -89,6 +89,7 @@ struct JoinPlan {
   void* fdir;               // u32 bitmap (unit) / u32 packed (max-min) / u64 packed (max-mult)
   uint32_t* dirty;          // bitmap: slots improved this round
   int aggregate;            // warp pre-reduction of equal slots (narrow heads)
+
 };
 
 // Direct ⊕ (idempotent semirings on a direct-mapped store): F[slot] holds
@@ -220,6 +221,7 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
 // max_p (off[p+1] - off[p]) -> atomicMax into *out
 void launch_max_degree(const int64_t* off, int64_t nprefix, unsigned long long* out, cudaStream_t st);
 
+
 // ---- index build (A1) ----
 // re-key rows: out = Σ moves(key) ; tags copied
 void launch_rekey(const uint64_t* key, int64_t n, const Move* mv, int nmv, uint64_t* out, cudaStream_t st);
@@ -228,7 +230,7 @@ void launch_build_offsets(const uint64_t* key, int64_t n, int free_bits, int64_t
 
 // ---- dedup (A6-A7) and merge/diff (A8-A9) ----
 // U = segmented ⊕ over sorted candidates (vals: u32 p bits or u64 p|w<<32)
-// scratch: 2*nu + 1 uint32 words
+// scratch: 2*nu + 2 uint32 words
 void launch_seg_reduce(const uint64_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,
                        uint64_t* ukey, float* up, uint32_t* uw, uint32_t* scratch, cudaStream_t st);
 void launch_seg_reduce(const uint32_t* key, const void* val, const uint32_t* pos, int64_t n, int64_t nu, int semi,

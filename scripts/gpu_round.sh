@@ -9,5 +9,6 @@ smoke) python __graft_entry__.py --smoke 2>&1 | tail -3 ;;
 bench) timeout 900 python bench.py --steps 3 --warmup 2 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json ;;
 prof) python scripts/profile_c2.py 3,1 2>&1 | tail -3 ;;
 ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_c2.py 3 > /dev/null 2>&1; wc -l gpurun_out/launches.csv ;;
+configs) for c in C2 C1 C3 C4 C5; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -2 gpurun_out/bench_$c.err; cut -c1-400 gpurun_out/bench_$c.json; done ;;
 esac
 done
