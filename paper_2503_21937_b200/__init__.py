@@ -16,5 +16,5 @@ from .engine import Engine, LobsterError, RelationOutput  # noqa: F401
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    from .build import build as _b
+    from ._build import build as _b
     return _b(force=force, verbose=verbose)

@@ -1,6 +1,6 @@
 """In-tree build of liblobster.so for sm_100a (nvcc; no JIT cache).
 
-    python -m paper_2503_21937_b200.build        # or __graft_entry__.build()
+    python -m paper_2503_21937_b200._build        # or __graft_entry__.build()
 """
 from __future__ import annotations
 

@@ -59,7 +59,7 @@ def load():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2503_21937_b200.build` "
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2503_21937_b200._build` "
                            "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     vp = ctypes.c_void_p

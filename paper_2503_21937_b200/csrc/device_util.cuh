@@ -122,8 +122,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
 // within its 32-bit bitmap word).  direct_peek: a plain L2 read of the word —
 // the store only grows (atomicMax / OR), so a stale read is a lower bound and
 // a candidate not above it can never improve the slot.  direct_commit issues
-// the remaining atomics back to back, then marks each slot's first improver
-// dirty (the settled bit of the pre-atomic word says "first this round").
+// the remaining updates and dirty bits as fire-and-forget reductions.
 __device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slot, float t, uint32_t w) {
   if (semi == S_UNIT) return 1ull << (slot & 31u);
   if (semi == S_MAXMIN) return (unsigned long long)((f2u(t) + 1u) << 1);
@@ -138,31 +137,26 @@ __device__ __forceinline__ unsigned long long direct_peek(int semi, const void* 
 
 template <int N>
 __device__ __forceinline__ void direct_commit(int semi, void* f, uint32_t* dirty, const uint32_t* slotv,
-                                              const unsigned long long* newv, unsigned long long* oldv, bool* live) {
+                                              const unsigned long long* newv, const unsigned long long* oldv,
+                                              const bool* live) {
+  // v > the (stale) read >= the slot's round-start value: the slot ends the
+  // round strictly above its settled value, so it is in Δ' — RED the value and
+  // the dirty bit without waiting for the atomic's old value.
 #pragma unroll
   for (int d = 0; d < N; ++d) {
     if (!live[d]) continue;
     const unsigned long long v = newv[d];
     if (semi == S_UNIT) {
-      if (oldv[d] & v) { live[d] = false; continue; }
-      oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(f) + (slotv[d] >> 5), (uint32_t)v);
+      if (oldv[d] & v) continue;
+      atomicOr(reinterpret_cast<uint32_t*>(f) + (slotv[d] >> 5), (uint32_t)v);
     } else if (semi == S_MAXMIN) {
-      if (v <= oldv[d]) { live[d] = false; continue; }
-      oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(f) + slotv[d], (uint32_t)v);
+      if (v <= oldv[d]) continue;
+      atomicMax(reinterpret_cast<uint32_t*>(f) + slotv[d], (uint32_t)v);
     } else {
-      if (v <= oldv[d]) { live[d] = false; continue; }
-      oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(f) + slotv[d], v);
+      if (v <= oldv[d]) continue;
+      atomicMax(reinterpret_cast<unsigned long long*>(f) + slotv[d], v);
     }
-  }
-#pragma unroll
-  for (int d = 0; d < N; ++d) {
-    if (!live[d]) continue;
-    const unsigned long long old = oldv[d], v = newv[d];
-    bool first;
-    if (semi == S_UNIT) first = !(old & v);
-    else if (semi == S_MAXMIN) first = old < v && (old == 0ull || (old & 1ull));
-    else first = old < v && (old == 0ull || ((old >> 32) & 1ull));
-    if (first) atomicOr(dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
+    atomicOr(dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
   }
 }
 

@@ -114,10 +114,10 @@ struct RelState {
   bool out_dev_ready = false, out_host_ready = false;
   DBuf<int32_t> o_sid, o_cols;
   DBuf<int64_t> o_soff;
-  std::vector<int32_t> h_sid, h_cols;
-  std::vector<float> h_p;
-  std::vector<int64_t> h_soff, h_goff, h_gfid;
-  std::vector<float> h_gval;
+  HBuf<int32_t> h_sid, h_cols;
+  HBuf<float> h_p;
+  HBuf<int64_t> h_soff, h_goff, h_gfid;
+  HBuf<float> h_gval;
   std::vector<const int32_t*> col_ptrs;
   bool has_grad = false;
   DBuf<int64_t> goff, gfid;

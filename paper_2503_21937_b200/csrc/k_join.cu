@@ -318,31 +318,27 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
         oldv[d] = __ldcg(reinterpret_cast<const unsigned long long*>(jp.fdir) + slot);
       }
     }
-    // phase B: atomics only for candidates above the stale bound
+    // phase B: fire-and-forget reductions (RED, no return) for candidates above
+    // the stale bound.  The read is >= the slot's value at round start (slots
+    // only grow; earlier kernels' writes are visible), so v > read means the
+    // slot ends the round strictly above its settled value: it IS in Δ' and
+    // its dirty bit is set unconditionally (idempotent OR) — no need to learn
+    // from the atomic's old value who improved first.
 #pragma unroll
     for (int d = 0; d < MAXDEG; ++d) {
       if (!live[d]) continue;
       const unsigned long long v = newv[d];
       if (jp.semi == S_UNIT) {
-        if (oldv[d] & v) { live[d] = false; continue; }
-        oldv[d] = atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
+        if (oldv[d] & v) continue;
+        atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
       } else if (jp.semi == S_MAXMIN) {
-        if (v <= oldv[d]) { live[d] = false; continue; }
-        oldv[d] = atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
+        if (v <= oldv[d]) continue;
+        atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
       } else {
-        if (v <= oldv[d]) { live[d] = false; continue; }
-        oldv[d] = atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], v);
+        if (v <= oldv[d]) continue;
+        atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], v);
       }
-    }
-#pragma unroll
-    for (int d = 0; d < MAXDEG; ++d) {
-      if (!live[d]) continue;
-      const unsigned long long old = oldv[d], v = newv[d];
-      bool first;
-      if (jp.semi == S_UNIT) first = !(old & v);
-      else if (jp.semi == S_MAXMIN) first = old < v && (old == 0ull || (old & 1ull));
-      else first = old < v && (old == 0ull || ((old >> 32) & 1ull));
-      if (first) atomicOr(jp.dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
+      atomicOr(jp.dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
     }
   }
   mycount = __reduce_add_sync(0xffffffffu, mycount);
