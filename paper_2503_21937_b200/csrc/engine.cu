@@ -14,9 +14,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -103,6 +105,8 @@ struct RelState {
   DevMem dirf;          // direct store words
   DBuf<uint32_t> dirty;  // bitmap of the slots improved this round
   DBuf<unsigned long long> dctr;  // |Δ'| counter of the single-pass extraction
+  DBuf<uint32_t> ndev;             // |Δ'| of the last extraction (device)
+  bool async = false;              // rounds run without a host sync: Δ size lives in ndev
   int64_t cand_bound = 0;         // upper bound on slots dirtied this round
   DBuf<float> dfp;
   DBuf<uint32_t> dfw, dfbits, dkey32, ckey32, ckey32b;
@@ -140,6 +144,7 @@ struct RelState {
     for (auto* b : {&fid, &o_sid, &o_cols}) b->bind(st);
     for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
     dctr.bind(st);
+    ndev.bind(st);
     for (auto& c : in.cols) c.bind(st);
     for (auto& c : acc_col) c.bind(st);
     acc_sid.bind(st);
@@ -208,7 +213,8 @@ struct Ctx {
   int max_iters = 100000;
   int32_t batch_cur = 1;  // samples of the (micro-)batch being evaluated
   bool micro = false;     // the last run was split into sample chunks
-  int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line
+  int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line, 2: + rounds
+  std::vector<std::array<int64_t, 4>> trace;  // per round: first event index, fused probe rows, |Δ'|, stratum
   double host_ms[8] = {};
   struct HostTimer {  // accumulates host wall time of a scope (diagnostics)
     double& acc;
@@ -272,6 +278,9 @@ struct Ctx {
     if (d_ncand) cudaFree(d_ncand);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (hbuf) cudaFreeHost(hbuf);
+    if (hring) cudaFreeHost(hring);
+    for (auto e : ring_ev)
+      if (e) cudaEventDestroy(e);
   }
 
   // --------------------------------------------------------------- create
@@ -683,6 +692,7 @@ struct Ctx {
 
   // Evaluate one rule (variant) and append its candidates to the head's buffer.
   void eval_rule(const Rule& R, const std::vector<Version>& ver, int start) {
+    round_other++;  // moved to round_fused if this evaluation takes the fused direct join
     const int na = (int)R.body.size();
     const int nv = (int)R.var_names.size();
     RelState& H = *rels[R.head_rel];
@@ -963,16 +973,21 @@ struct Ctx {
           jp.tag_order[1] = (int8_t)(start < ai ? 1 : 0);
         }
         direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate);
+        if (rels[A0.rel]->async) jp.np_dev = rels[A0.rel]->ndev.ptr();
         merge_moves(jp.prem, jp.nprem);
         merge_moves(jp.om, jp.nom);
         merge_moves(jp.wm, jp.nwm);
         {
           Phase ph(this, 5);
-          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand + 1, st);
+          // async: Δ size unknown here; grid from the last size the host saw (any grid is
+          // correct: the kernel strides over the device-side count)
+          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand + 1, st, jp.np_dev ? 8 * async_nd0 + 1 : jp.np);
           kcheck("join rows direct");
         }
         stats.fj_launches++;
-        stats.fj_probe_rows += T.n;
+        round_other--;
+        round_fused++;
+        if (!H.async) stats.fj_probe_rows += T.n;
         H.nc += T.n;  // candidates counted on the device (d_ncand[1])
         H.cand_bound += T.n * ix->maxdeg;
         return;
@@ -1247,6 +1262,7 @@ struct Ctx {
       S.dirf.reserve(bytes);
       launch_direct_fill(S.dirf.get(), ns, semi, st);
       S.dirty.reserve((ns + 31) / 32);
+      S.ndev.reserve(1);
       S.dctr.reserve(1);
       cuda_check(cudaMemsetAsync(S.dctr.ptr(), 0, 8, st), "memset");
       S.cand_bound = 0;
@@ -1278,25 +1294,25 @@ struct Ctx {
   int64_t settle_direct(RelState& S) {
     const int64_t nc = S.nc;
     S.nc = 0;
-    if (nc == 0) { S.nd = 0; return 0; }
+    if (nc == 0 && !S.async) { S.nd = 0; return 0; }
     const int64_t nw = (S.nslots + 31) / 32;
-    const int64_t cap = std::min<int64_t>(std::max<int64_t>(S.cand_bound, 1), S.nslots);
+    const int64_t cap = S.async ? S.nslots : std::min<int64_t>(std::max<int64_t>(S.cand_bound, 1), S.nslots);
     S.cand_bound = 0;
     S.dkey32.reserve(cap);
     if (semi != S_UNIT) S.dp.reserve(cap);
     if (semi == S_MAXMULT) S.dw.reserve(cap);
-    const int64_t ntiles = (nw + 31) / 32;  // warp chunks of 32 words
-    uint32_t* tcnt = arena.get<uint32_t>(ntiles);
-    uint32_t* tbase = arena.get<uint32_t>(ntiles + 1);
-    {  // Δ' in slot order: chunk popcounts -> scan -> extract; dirty bits cleared, slots re-settled
+    {  // Δ' in slot order (two launches); dirty bits cleared, slots re-settled
       Phase ph(this, 3);
-      launch_dirty_chunk_count(S.dirty.ptr(), nw, tcnt, st);
-      exclusive_scan<uint32_t>(tcnt, tbase, ntiles, tbase + ntiles, arena.alloc(scan_tmp_bytes<uint32_t>(ntiles)), st);
-      launch_direct_extract_warp(S.dirf.get(), S.dirty.ptr(), tbase, nw, semi, S.dkey32.ptr(),
-                                 semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr, st);
+      launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
+                             semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr,
+                             arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(), st);
       kcheck("direct extract");
     }
-    const int64_t nd = (int64_t)read_dev(tbase + ntiles);
+    if (S.async) {  // |Δ'| stays on the device: the next join reads it, the host polls it later
+      S.nd = S.nslots;
+      return -1;
+    }
+    const int64_t nd = (int64_t)read_dev(S.ndev.ptr());
     stats.bytes_algorithmic += bytes_round_direct(nc, nd);
     S.nd = nd;
     return nd;
@@ -1577,6 +1593,66 @@ struct Ctx {
   }
 
   // one (micro-)batch: every stratum to fixpoint; returns 1 if max_iters was hit
+  // Async rounds (direct strata): ring of pinned |Δ'| slots, one event per slot.
+  static constexpr int ARING = 64, AREL = 8, ALAG = 6;
+  uint32_t* hring = nullptr;
+  cudaEvent_t ring_ev[ARING] = {};
+  int round_fused = 0, round_other = 0;
+  int64_t async_nd0 = 0;  // Δ rows probed by the first async round
+  int async_nrel = 0;     // relations of the async stratum (ring entries per round)
+
+  // Δ buffers must hold every slot (sizes are no longer known on the host)
+  bool async_ok(const std::vector<int>& strat) {
+    if (getenv("LOBSTER_SYNC_ROUNDS")) return false;
+    size_t need = 0;
+    for (int r : strat) {
+      RelState& S = *rels[r];
+      if (!S.direct) return false;
+      const size_t row = 4 + (semi == S_UNIT ? 0 : 4) + (semi == S_MAXMULT ? 4 : 0);
+      if (S.dkey32.bytes() < (size_t)S.nslots * 4) need += (size_t)S.nslots * row;
+    }
+    if (need) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if ((double)need > 0.4 * (double)fr) return false;
+    }
+    if (!hring) {
+      cuda_check(cudaMallocHost(&hring, ARING * AREL * 4), "cudaMallocHost");
+      for (auto& e : ring_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    return true;
+  }
+
+  // Consume finished rounds from the ring (all of them if `all`, else block only on
+  // rounds more than ALAG behind).  Returns the first round whose Σ|Δ'| is 0, or 0.
+  int64_t drain_async(std::deque<int>& pending, size_t trace_base, bool all) {
+    const int newest = pending.empty() ? 0 : pending.back();
+    while (!pending.empty()) {
+      const int pr = pending.front();
+      const int slot = pr % ARING;
+      if (all || newest - pr >= ALAG) {
+        cuda_check(cudaEventSynchronize(ring_ev[slot]), "event sync");
+      } else {
+        const cudaError_t q = cudaEventQuery(ring_ev[slot]);
+        if (q == cudaErrorNotReady) break;
+        cuda_check(q, "event query");
+      }
+      pending.pop_front();
+      int64_t sum = 0;
+      for (int q = 0; q < async_nrel; ++q) sum += hring[slot * AREL + q];
+      const int64_t probe = async_nd0;
+      async_nd0 = sum;  // Δ' of this round = probe rows of the next
+      stats.fj_probe_rows += probe;
+      stats.bytes_algorithmic += bytes_round_direct(probe, sum);
+      if (log_level >= 2 && trace_base + pr - 1 < trace.size()) {
+        trace[trace_base + pr - 1][1] = probe;
+        trace[trace_base + pr - 1][2] = sum;
+      }
+      if (sum == 0) return pr;
+    }
+    return 0;
+  }
+
   int64_t run_strata() {
     int64_t round_cap_hit = 0;
     for (size_t si = 0; si < prog.strata.size(); ++si) {
@@ -1592,11 +1668,22 @@ struct Ctx {
         choose_store(S);
       }
       int rounds = 0;
-      bool first = true;
+      bool first = true, first_round = true, async = false;
+      int64_t done = 0;
+      std::deque<int> pending;
+      const size_t trace_base = trace.size();
+      async_nd0 = 0;
       for (;;) {
-        if (rounds >= max_iters) { round_cap_hit = 1; break; }
+        if (rounds >= max_iters) {
+          if (async && (done = drain_async(pending, trace_base, true)) > 0) { rounds = (int)done; break; }
+          round_cap_hit = 1;
+          break;
+        }
         rounds++;
         arena.reset();
+        const int64_t probe0 = stats.fj_probe_rows;
+        if (log_level >= 2) trace.push_back({(int64_t)ev.size(), 0, 0, (int64_t)si});
+        round_fused = round_other = 0;
         HostTimer ht_rules(host_ms[1]);
         for (const Rule& R : prog.rules) {
           if (!local.count(R.head_rel)) continue;
@@ -1635,7 +1722,36 @@ struct Ctx {
           HostTimer ht(host_ms[2]);
           for (int r : strat) changed += settle(r);
         }
+        if (async) {  // |Δ'| of this round -> pinned ring; poll earlier rounds without stalling the GPU
+          const int slot = rounds % ARING;
+          for (size_t q = 0; q < strat.size(); ++q)
+            cuda_check(cudaMemcpyAsync(hring + slot * AREL + q, rels[strat[q]]->ndev.ptr(), 4, cudaMemcpyDeviceToHost, st),
+                       "D2H");
+          cuda_check(cudaEventRecord(ring_ev[slot], st), "event");
+          pending.push_back(rounds);
+          if ((done = drain_async(pending, trace_base, false)) > 0) { rounds = (int)done; break; }
+          continue;
+        }
+        if (log_level >= 2) { trace.back()[1] = stats.fj_probe_rows - probe0; trace.back()[2] = changed; }
         if (changed == 0) break;
+        // every recursive rule took the fused direct join in this (non-seed) round: later
+        // rounds need no host-side sizes, so they are issued without a sync (lagged stop test)
+        if (!first_round && round_other == 0 && round_fused > 0 && strat.size() <= (size_t)AREL && async_ok(strat)) {
+          async = true;
+          async_nrel = (int)strat.size();
+          for (int r : strat) rels[r]->async = true;
+          for (int r : strat) async_nd0 += rels[r]->nd;
+        }
+        first_round = false;
+      }
+      if (async) {
+        sync();
+        if (log_level >= 2 && trace.size() > trace_base + rounds) trace.resize(trace_base + rounds);
+        for (int r : strat) {
+          rels[r]->async = false;
+          rels[r]->nd = 0;
+        }
+        pending.clear();
       }
       HostTimer ht(host_ms[3]);
       for (int r : strat)
@@ -1669,6 +1785,20 @@ struct Ctx {
         default: stats.ms_grad += m; break;
       }
     }
+    if (log_level >= 2) {  // per-round trace: probe rows, |Δ'|, GPU ms of join / settle phases
+      for (size_t t = 0; t < trace.size(); ++t) {
+        const size_t e0 = (size_t)trace[t][0], e1 = t + 1 < trace.size() ? (size_t)trace[t + 1][0] : ev.size();
+        double pj = 0, pm = 0;
+        for (size_t q = e0; q < e1 && q < ev.size(); ++q) {
+          float m = 0;
+          cudaEventElapsedTime(&m, ev[q].second.first, ev[q].second.second);
+          if (ev[q].first == 0 || ev[q].first == 5) pj += m; else pm += m;
+        }
+        fprintf(stderr, "[lobster] round %4zu stratum %lld probe %10lld delta' %10lld join %8.1f us settle %8.1f us\n", t,
+                (long long)trace[t][3], (long long)trace[t][1], (long long)trace[t][2], pj * 1e3, pm * 1e3);
+      }
+    }
+    trace.clear();
     ran = true;
     arena.reset();
     if (log_level >= 1)

@@ -12,6 +12,8 @@
 //
 // Probe / output keys are u32 or u64 (template PK / OK): relations whose
 // packed key fits 31 bits move half the key bytes.
+#include <algorithm>
+
 #include "device_util.cuh"
 
 namespace lob {
@@ -255,31 +257,52 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // Row-centric fused join + direct ⊕ for bounded fan-out (every prefix of the
 // static CSR index has <= MAXDEG rows, e.g. lattice edges: 4).  One thread per
 // probe row: coalesced probe key / tag loads, its matches unrolled, all
-// atomics issued before any result is consumed.  No count / scan / host sync.
-// One thread per probe row, <= MAXDEG candidates each.  Measured on C2 and
-// rejected: two rows per thread (152 vs 101 us per launch: fewer resident
-// warps for the same requests in flight), phase A/B through the generic
-// direct_pack/peek/commit helpers (+5%), a fixed-width ELL copy of the build
-// index replacing boff -> bkey (+3%: boff hits L1).
+// updates issued before any result is consumed.  No count / scan / host sync.
+// Specialised on the semiring and on the longest move list (NM: 2, 4 or MAXM
+// bit moves for prefix / slot / witness) — the generic kernel was 3.7k SASS
+// instructions and stalled on instruction fetch (ncu: 21% no_instruction).
+// Measured on C2 and rejected: two rows per thread (152 vs 101 us per launch:
+// fewer resident warps for the same requests in flight), a fixed-width ELL
+// copy of the build index replacing boff -> bkey (+3%: boff hits L1).
 #ifndef FJ_MINB
 #define FJ_MINB 6
 #endif
-template <typename PK, int MAXDEG>
+template <int NM>
+__device__ __forceinline__ uint64_t moves_n(const Move* mv, int n, uint64_t a, uint64_t b) {
+  uint64_t o = 0;
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    if (i < n) {
+      const Move m = mv[i];
+      const uint64_t s = m.src ? b : a;
+      o |= ((s >> m.sshift) & ((1ull << m.bits) - 1ull)) << m.dshift;
+    }
+  }
+  return o;
+}
+
+template <typename PK, int MAXDEG, int SEMI, int NM>
 __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_direct_k(const JoinPlan jp,
                                                           unsigned long long* __restrict__ ncand) {
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   uint32_t mycount = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < jp.np;
+  int64_t np = jp.np;
+  if (jp.np_dev) {
+    const int64_t nd = (int64_t)*jp.np_dev;
+    np = nd < np ? nd : np;
+  }
+  const int ncmp = jp.ncmp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np;
        i += (int64_t)gridDim.x * blockDim.x) {
     const PK pkr = pkey[i];
     if (pkr == dead<PK>()) continue;
     const uint64_t pk = (uint64_t)pkr;
-    const uint64_t pre = probe_prefix(jp, pk);
+    const uint64_t pre = jp.cprefix | moves_n<NM>(jp.prem, jp.nprem, pk, 0);
     if (pre >= (uint64_t)jp.nprefix) continue;
     const int64_t lo = jp.boff[pre];
     const int n = (int)(jp.boff[pre + 1] - lo);
     mycount += (uint32_t)n;
-    const float pt = jp.semi != S_UNIT ? jp.ptag[0][i] : 1.0f;
+    const float pt = SEMI != S_UNIT ? jp.ptag[0][i] : 1.0f;
     unsigned long long oldv[MAXDEG], newv[MAXDEG];
     uint32_t slotv[MAXDEG];
     bool live[MAXDEG];
@@ -293,27 +316,27 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
       if (d >= n) continue;
       const uint64_t bk = jp.bkey[lo + d];
       bool ok = true;
-      for (int c = 0; c < jp.ncmp; ++c) {
+      for (int c = 0; c < ncmp; ++c) {
         const int64_t a = operand_value(jp.cmp[c].a, pk, bk);
         const int64_t b = operand_value(jp.cmp[c].b, pk, bk);
         ok &= jp.cmp[c].neq ? (a != b) : (a == b);
       }
       if (!ok) continue;
-      const uint32_t slot = (uint32_t)(jp.cout | apply_moves(jp.om, jp.nom, pk, bk));
+      const uint32_t slot = (uint32_t)(jp.cout | moves_n<NM>(jp.om, jp.nom, pk, bk));
       slotv[d] = slot;
       live[d] = true;
-      if (jp.semi == S_UNIT) {
+      if (SEMI == S_UNIT) {
         newv[d] = 1u << (slot & 31u);
         oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + (slot >> 5));
         continue;
       }
       const float bt = jp.btag[lo + d];
-      const float t = jp.tag_order[0] == 0 ? otimes(jp.semi, pt, bt) : otimes(jp.semi, bt, pt);
-      if (jp.semi == S_MAXMIN) {
+      const float t = jp.tag_order[0] == 0 ? otimes(SEMI, pt, bt) : otimes(SEMI, bt, pt);
+      if (SEMI == S_MAXMIN) {
         newv[d] = (f2u(t) + 1u) << 1;
         oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
       } else {
-        const uint32_t w = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
+        const uint32_t w = jp.wconst | (uint32_t)moves_n<NM>(jp.wm, jp.nwm, pk, bk);
         newv[d] = ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
         oldv[d] = __ldcg(reinterpret_cast<const unsigned long long*>(jp.fdir) + slot);
       }
@@ -328,10 +351,10 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
     for (int d = 0; d < MAXDEG; ++d) {
       if (!live[d]) continue;
       const unsigned long long v = newv[d];
-      if (jp.semi == S_UNIT) {
+      if (SEMI == S_UNIT) {
         if (oldv[d] & v) continue;
         atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
-      } else if (jp.semi == S_MAXMIN) {
+      } else if (SEMI == S_MAXMIN) {
         if (v <= oldv[d]) continue;
         atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
       } else {
@@ -454,16 +477,31 @@ void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* s
   else join_write_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(jp, offs, start, total);
 }
 
-void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st) {
+template <typename PK, int SEMI, int NM>
+static void launch_rows_direct_t(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st, int g) {
+  if (maxdeg <= 4) join_rows_direct_k<PK, 4, SEMI, NM><<<g, 256, 0, st>>>(jp, ncand);
+  else join_rows_direct_k<PK, 8, SEMI, NM><<<g, 256, 0, st>>>(jp, ncand);
+}
+template <int SEMI>
+static void launch_rows_direct_s(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st, int g) {
+  const int nm = std::max(jp.nprem, std::max(jp.nom, jp.nwm));
+  if (!jp.pk32) launch_rows_direct_t<uint64_t, SEMI, MAXM>(jp, maxdeg, ncand, st, g);
+  else if (nm <= 2) launch_rows_direct_t<uint32_t, SEMI, 2>(jp, maxdeg, ncand, st, g);
+  else if (nm <= 4) launch_rows_direct_t<uint32_t, SEMI, 4>(jp, maxdeg, ncand, st, g);
+  else launch_rows_direct_t<uint32_t, SEMI, MAXM>(jp, maxdeg, ncand, st, g);
+}
+
+void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st,
+                             int64_t np_hint) {
   if (jp.np <= 0) return;
-  const int g = grid_for(jp.np, 256);
+  // device-sized Δ: at most one wave of resident CTAs (grid-stride), at least 2 per SM
+  int g = grid_for(np_hint, 256);
+  if (jp.np_dev) g = std::max(148 * 2, std::min(g, 148 * ((maxdeg <= 4) ? FJ_MINB : 4)));
   note_launch();
-  if (jp.pk32) {
-    if (maxdeg <= 4) join_rows_direct_k<uint32_t, 4><<<g, 256, 0, st>>>(jp, ncand);
-    else join_rows_direct_k<uint32_t, 8><<<g, 256, 0, st>>>(jp, ncand);
-  } else {
-    if (maxdeg <= 4) join_rows_direct_k<uint64_t, 4><<<g, 256, 0, st>>>(jp, ncand);
-    else join_rows_direct_k<uint64_t, 8><<<g, 256, 0, st>>>(jp, ncand);
+  switch (jp.semi) {
+    case S_UNIT: launch_rows_direct_s<S_UNIT>(jp, maxdeg, ncand, st, g); break;
+    case S_MAXMIN: launch_rows_direct_s<S_MAXMIN>(jp, maxdeg, ncand, st, g); break;
+    default: launch_rows_direct_s<S_MAXMULT>(jp, maxdeg, ncand, st, g); break;
   }
 }
 

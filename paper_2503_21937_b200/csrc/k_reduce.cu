@@ -624,6 +624,175 @@ __global__ void __launch_bounds__(256) direct_extract_warp_k(void* __restrict__ 
   }
 }
 
+// Dirty bitmap -> Δ' in slot order in two launches (replaces the per-chunk
+// count, scan and extraction above: three plus the scan's).  CTA tile = 2048
+// bitmap words, 8 per lane in warp-strided chunks of 32 (each chunk load is one
+// 128-B line per warp).  Launch 1 counts the set bits of every tile and of every
+// group of 8 tiles; launch 2 gives each tile its base as the sum of the group
+// counts before it plus the tile counts of its own group before it (a parallel
+// block reduction: no serial chain across tiles, unlike a decoupled look-back
+// when every tile of a small grid is resident at once), then writes the tile's
+// Δ' rows.
+constexpr int LB_WPT = 8;   // bitmap words per lane
+constexpr int LB_U = 4;     // Δ' rows per lane in flight
+constexpr int LB_TILE = 256 * LB_WPT;
+constexpr int LB_GROUP = 8;  // tiles per group (one counting CTA, one tile per warp)
+
+__global__ void __launch_bounds__(256) dirty_group_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
+                                                           int64_t nt, uint32_t* __restrict__ tcnt,
+                                                           uint32_t* __restrict__ gsum) {
+  __shared__ uint32_t wt[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = (int64_t)blockIdx.x * LB_GROUP + warp;
+  uint32_t c = 0;
+  if (tile < nt) {
+    const int64_t w0 = tile * LB_TILE;
+    if (w0 + LB_TILE <= nw) {
+#pragma unroll
+      for (int i = 0; i < LB_TILE / 128; ++i) {  // 16 B per lane, 512 B per warp load
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(dirty + w0) + i * 32 + lane);
+        c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+      }
+    } else {
+      for (int64_t w = w0 + lane; w < nw; w += 32) c += __popc(__ldcg(dirty + w));
+    }
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) {
+    wt[warp] = c;
+    if (tile < nt) tcnt[tile] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t g = 0;
+    for (int k = 0; k < 8; ++k) g += wt[k];
+    gsum[blockIdx.x] = g;
+  }
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
+                                                         int64_t nw, uint32_t* __restrict__ dkey,
+                                                         float* __restrict__ dp, uint32_t* __restrict__ dw,
+                                                         const uint32_t* __restrict__ tcnt,
+                                                         const uint32_t* __restrict__ gsum,
+                                                         uint32_t* __restrict__ total) {
+  __shared__ uint32_t wtot[8];
+  __shared__ uint32_t wpre[8];
+  __shared__ uint32_t s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t w0 = tile * LB_TILE + (int64_t)warp * (32 * LB_WPT);
+  uint32_t m[LB_WPT];
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < LB_WPT; ++j) {
+    const int64_t w = w0 + j * 32 + lane;
+    m[j] = w < nw ? __ldcg(dirty + w) : 0u;
+    c += __popc(m[j]);
+  }
+  // tile base: groups before this tile's group + this group's earlier tiles
+  const int64_t grp = tile / LB_GROUP;
+  uint32_t pre = 0;
+  for (int64_t i = threadIdx.x; i < grp; i += 256) pre += gsum[i];
+  if (threadIdx.x < (unsigned)(tile - grp * LB_GROUP)) pre += tcnt[grp * LB_GROUP + threadIdx.x];
+  pre = __reduce_add_sync(0xffffffffu, pre);
+  const uint32_t wsum = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) {
+    wtot[warp] = wsum;
+    wpre[warp] = pre;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t own = lane < 8 ? wtot[lane] : 0u;
+    uint32_t inc = own;
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    const uint32_t prefix = __reduce_add_sync(0xffffffffu, lane < 8 ? wpre[lane] : 0u);
+    const uint32_t agg = __shfl_sync(0xffffffffu, inc, 7);
+    if (lane == 0) {
+      s_base = prefix;
+      if (tile == (int64_t)gridDim.x - 1) *total = prefix + agg;
+    }
+    __syncwarp();
+    if (lane < 8) wtot[lane] = inc - own;
+  }
+  __syncthreads();
+  uint32_t base = s_base + wtot[warp];
+#pragma unroll 1
+  for (int j = 0; j < LB_WPT; ++j) {
+    const uint32_t mm = m[j];
+    const uint32_t cnt = __popc(mm);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (!tot) continue;
+    const int64_t wbase = w0 + j * 32;
+    if (mm) dirty[wbase + lane] = 0u;
+    // bits spread evenly over the lanes, LB_U per lane per batch: every slot
+    // read of a batch is issued before any dependent store (memory-level
+    // parallelism; the loop is latency-bound otherwise)
+    for (uint32_t kb = 0; kb < tot; kb += 32 * LB_U) {
+      uint32_t slotv[LB_U];
+      bool act[LB_U];
+#pragma unroll
+      for (int u = 0; u < LB_U; ++u) {
+        const uint32_t k = kb + u * 32 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, inc, lo + step - 1);
+          if (v <= k) lo += step;
+        }
+        const uint32_t wm = __shfl_sync(0xffffffffu, mm, lo);
+        const uint32_t wex = __shfl_sync(0xffffffffu, inc - cnt, lo);
+        act[u] = k < tot;
+        slotv[u] = act[u] ? (uint32_t)((wbase + lo) * 32 + __fns(wm, 0, (int)(k - wex) + 1)) : 0u;
+      }
+      if (SEMI == S_MAXMIN) {
+        uint32_t v[LB_U];
+#pragma unroll
+        for (int u = 0; u < LB_U; ++u)
+          if (act[u]) v[u] = __ldcg(reinterpret_cast<const uint32_t*>(f) + slotv[u]);
+#pragma unroll
+        for (int u = 0; u < LB_U; ++u) {
+          if (!act[u]) continue;
+          const uint32_t o = base + kb + u * 32 + lane;
+          __stcg(reinterpret_cast<uint32_t*>(f) + slotv[u], v[u] | 1u);  // settle (each slot once: no atomic)
+          dkey[o] = slotv[u];
+          dp[o] = u2f((v[u] >> 1) - 1u);
+        }
+      } else if (SEMI == S_MAXMULT) {
+        unsigned long long v[LB_U];
+#pragma unroll
+        for (int u = 0; u < LB_U; ++u)
+          if (act[u]) v[u] = __ldcg(reinterpret_cast<const unsigned long long*>(f) + slotv[u]);
+#pragma unroll
+        for (int u = 0; u < LB_U; ++u) {
+          if (!act[u]) continue;
+          const uint32_t o = base + kb + u * 32 + lane;
+          __stcg(reinterpret_cast<unsigned long long*>(f) + slotv[u], v[u] | (1ull << 32));
+          dkey[o] = slotv[u];
+          dp[o] = u2f((uint32_t)(v[u] >> 33) - 1u);
+          dw[o] = ~(uint32_t)v[u];
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < LB_U; ++u)
+          if (act[u]) dkey[base + kb + u * 32 + lane] = slotv[u];
+      }
+    }
+    base += tot;
+  }
+}
+
 // popcount of each 1024-word tile of the dirty bitmap
 __global__ void __launch_bounds__(256) dirty_tile_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
                                                           uint32_t* __restrict__ tcnt) {
@@ -840,6 +1009,26 @@ void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   note_launch();
   direct_extract1_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(f, dirty, nwords, semi, dkey, dp, dw,
                                                                                  counter, tile_base);
+}
+int64_t direct_extract2_scratch(int64_t nwords) {
+  const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
+  return nt + (nt + LB_GROUP - 1) / LB_GROUP;
+}
+void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
+                            uint32_t* dw, uint32_t* scratch, uint32_t* total, cudaStream_t st) {
+  if (nwords <= 0) return;
+  const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
+  const int64_t ng = (nt + LB_GROUP - 1) / LB_GROUP;
+  uint32_t* tcnt = scratch;
+  uint32_t* gsum = scratch + nt;
+  note_launch();
+  dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
+  note_launch();
+  switch (semi) {
+    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
+    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
+    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
+  }
 }
 void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st) {
   if (nwords <= 0) return;

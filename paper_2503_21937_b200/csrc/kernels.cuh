@@ -48,6 +48,7 @@ struct JoinPlan {
   const void* pkey;         // u32 or u64 keys (pk32)
   int8_t pk32, ok32;
   int64_t np;
+  const uint32_t* np_dev;   // nullable: probe rows = min(np, *np_dev) (Δ size left on the device)
   const float* ptag[MAXT];
   int npt;
   // build lookup
@@ -217,7 +218,9 @@ void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* s
                        cudaStream_t st);
 void launch_project(const ProjectPlan& pp, cudaStream_t st);
 // fused row-centric join + direct ⊕ (bounded fan-out <= 8 per prefix); adds |C| to *ncand
-void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st);
+// With jp.np_dev (Δ size on the device) the grid is persistent.
+void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st,
+                             int64_t np_hint);
 // max_p (off[p+1] - off[p]) -> atomicMax into *out
 void launch_max_degree(const int64_t* off, int64_t nprefix, unsigned long long* out, cudaStream_t st);
 
@@ -263,6 +266,11 @@ void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tc
 void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st);
 void launch_direct_extract_warp(void* f, uint32_t* dirty, const uint32_t* cbase, int64_t nwords, int semi,
                                 uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
+// two launches (tile / group counts, then bases + rows): dirty bitmap -> Δ' in slot order,
+// dirty bits cleared, slots re-settled; |Δ'| -> *total (device).  scratch: direct_extract2_scratch u32
+int64_t direct_extract2_scratch(int64_t nwords);
+void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
+                            uint32_t* dw, uint32_t* scratch, uint32_t* total, cudaStream_t st);
 // dirty bitmap -> per-word popcounts (scan them), then Δ' in slot order
 void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st);
 void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
