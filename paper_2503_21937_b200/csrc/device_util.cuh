@@ -16,7 +16,9 @@ template <typename K>
 __device__ __forceinline__ constexpr K dead() { return ~K(0); }
 
 // Moves are merged host-side (adjacent fields with the same shift delta become
-// one move), so the common case has <= 4 moves: a short predicated loop.
+// one move), so the common case has <= 4 moves: a short predicated unrolled
+// loop; longer lists take a rolled loop (keeps the kernels' code small: the
+// unrolled MAXM path blew join_write_k up to 17.7k SASS instructions).
 __device__ __forceinline__ uint64_t apply_moves(const Move* mv, int n, uint64_t a, uint64_t b) {
   uint64_t o = 0;
   if (n <= 4) {
@@ -30,13 +32,11 @@ __device__ __forceinline__ uint64_t apply_moves(const Move* mv, int n, uint64_t 
     }
     return o;
   }
-#pragma unroll
-  for (int i = 0; i < MAXM; ++i) {
-    if (i < n) {
-      const Move m = mv[i];
-      const uint64_t s = m.src ? b : a;
-      o |= ((s >> m.sshift) & ((1ull << m.bits) - 1ull)) << m.dshift;
-    }
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const Move m = mv[i];
+    const uint64_t s = m.src ? b : a;
+    o |= ((s >> m.sshift) & ((1ull << m.bits) - 1ull)) << m.dshift;
   }
   return o;
 }

@@ -65,13 +65,14 @@ constexpr int SPT = WT / 256;
 
 // ⊗ in body order over T = [ptag[0..npt-1], btag] (reading 9).  Fast path:
 // one probe tag followed by the build tag (every linear TC-shaped rule).
-__device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int64_t row, int64_t j) {
+__device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int semi, int64_t row, int64_t j) {
   if (jp.npt == 1 && jp.ntag == 2) {
     const float a = jp.ptag[0][row], b = jp.btag[j];
-    return jp.tag_order[0] == 0 ? otimes(jp.semi, a, b) : otimes(jp.semi, b, a);
+    return jp.tag_order[0] == 0 ? otimes(semi, a, b) : otimes(semi, b, a);
   }
   float t = tag_at(jp, jp.tag_order[0], row, j);
-  for (int k = 1; k < jp.ntag; ++k) t = otimes(jp.semi, t, tag_at(jp, jp.tag_order[k], row, j));
+#pragma unroll 1
+  for (int k = 1; k < jp.ntag; ++k) t = otimes(semi, t, tag_at(jp, jp.tag_order[k], row, j));
   return t;
 }
 
@@ -91,9 +92,17 @@ __device__ __forceinline__ int64_t coop_row(const int64_t* __restrict__ offs, in
   return lo;
 }
 
-template <typename PK, typename OK>
+// MODE (compile time, keeps each variant's code small): JW_INTER = intermediate
+// rows (final_step 0), JW_CAND = candidates (semiring at run time), JW_DIRECT +
+// semiring = direct ⊕ into the dense store.
+constexpr int JW_INTER = 0, JW_CAND = 1, JW_DIRECT = 2;
+
+template <typename PK, typename OK, int MODE>
 __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int64_t* __restrict__ offs,
                                                     const int64_t* __restrict__ start, int64_t total) {
+  constexpr bool FINAL = MODE != JW_INTER;
+  constexpr bool DIRECT = MODE >= JW_DIRECT;
+  const int semi = DIRECT ? MODE - JW_DIRECT : jp.semi;
   // the tile's probe rows, staged: row start relative to the tile (only row 0
   // can start before it: clamped to -1), build-index delta start - offs (so a
   // slot's build row is j = sdel + o) and the probe key
@@ -173,13 +182,13 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
     keyv[k] = jp.cout | apply_moves(jp.om, jp.nom, pk, bk);
     tv[k] = 1.0f;
     wv[k] = 0;
-    if (jp.final_step && jp.semi != S_UNIT) {
-      tv[k] = candidate_tag(jp, row, j);
-      if (jp.semi == S_MAXMULT) wv[k] = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
+    if (FINAL && semi != S_UNIT) {
+      tv[k] = candidate_tag(jp, semi, row, j);
+      if (semi == S_MAXMULT) wv[k] = jp.wconst | (uint32_t)apply_moves(jp.wm, jp.nwm, pk, bk);
     }
   }
   // phase 2: emit
-  if (jp.direct) {  // fused A5-A8: ⊕ straight into the direct-mapped store
+  if constexpr (DIRECT) {  // fused A5-A8: ⊕ straight into the direct-mapped store
     if (!jp.aggregate) {
       // stale-read filter, then this thread's remaining atomics back to back
       unsigned long long oldv[SPT], newv[SPT];
@@ -190,31 +199,32 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
         live[k] = rowv[k] >= 0 && okv[k];
         if (!live[k]) continue;
         slotv[k] = (uint32_t)keyv[k];
-        newv[k] = direct_pack(jp.semi, slotv[k], tv[k], wv[k]);
-        oldv[k] = direct_peek(jp.semi, jp.fdir, slotv[k]);
+        newv[k] = direct_pack(semi, slotv[k], tv[k], wv[k]);
+        oldv[k] = direct_peek(semi, jp.fdir, slotv[k]);
       }
-      direct_commit<SPT>(jp.semi, jp.fdir, jp.dirty, slotv, newv, oldv, live);
+      direct_commit<SPT>(semi, jp.fdir, jp.dirty, slotv, newv, oldv, live);
     } else {
 #pragma unroll
       for (int k = 0; k < SPT; ++k)
         if (rowv[k] >= 0 && okv[k])
-          direct_oplus(jp.semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate);
+          direct_oplus(semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate);
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (rowv[k] < 0) continue;
-    const int64_t o = o0 + threadIdx.x + k * 256;
-    okey[o] = okv[k] ? (OK)keyv[k] : dead<OK>();
-    if (jp.semi == S_UNIT) continue;
-    if (jp.final_step) {
-      if (jp.semi == S_MAXMULT) jp.oval64[o] = (uint64_t)f2u(tv[k]) | ((uint64_t)wv[k] << 32);
-      else jp.oval32[o] = f2u(tv[k]);
-    } else {
-      const int64_t row = rowv[k];
-      for (int q = 0; q < jp.npt; ++q) jp.otag[q][o] = jp.ptag[q][row];
-      jp.otag[jp.npt][o] = jp.btag ? jp.btag[jv[k]] : 1.0f;
+    for (int k = 0; k < SPT; ++k) {
+      if (rowv[k] < 0) continue;
+      const int64_t o = o0 + threadIdx.x + k * 256;
+      okey[o] = okv[k] ? (OK)keyv[k] : dead<OK>();
+      if (semi == S_UNIT) continue;
+      if constexpr (FINAL) {
+        if (semi == S_MAXMULT) jp.oval64[o] = (uint64_t)f2u(tv[k]) | ((uint64_t)wv[k] << 32);
+        else jp.oval32[o] = f2u(tv[k]);
+      } else {
+        const int64_t row = rowv[k];
+#pragma unroll 1
+        for (int q = 0; q < jp.npt; ++q) jp.otag[q][o] = jp.ptag[q][row];
+        jp.otag[jp.npt][o] = jp.btag ? jp.btag[jv[k]] : 1.0f;
+      }
     }
   }
 }
@@ -263,7 +273,8 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // instructions and stalled on instruction fetch (ncu: 21% no_instruction).
 // Measured on C2 and rejected: two rows per thread (152 vs 101 us per launch:
 // fewer resident warps for the same requests in flight), a fixed-width ELL
-// copy of the build index replacing boff -> bkey (+3%: boff hits L1).
+// copy of the build index replacing boff -> bkey (+3%: boff hits L1), a
+// software pipeline prefetching row i+stride's key and CSR range (+22%).
 #ifndef FJ_MINB
 #define FJ_MINB 6
 #endif
@@ -466,15 +477,25 @@ void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaS
   else join_count_k<uint64_t><<<grid_for(jp.np, 256), 256, 0, st>>>(jp, count, start);
 }
 
+template <typename PK, typename OK>
+static void launch_join_write_t(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
+                                unsigned g, cudaStream_t st) {
+  if (!jp.final_step) join_write_k<PK, OK, JW_INTER><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else if (!jp.direct) join_write_k<PK, OK, JW_CAND><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else if (jp.semi == S_UNIT) join_write_k<PK, OK, JW_DIRECT + S_UNIT><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else if (jp.semi == S_MAXMIN) join_write_k<PK, OK, JW_DIRECT + S_MAXMIN><<<g, 256, 0, st>>>(jp, offs, start, total);
+  else join_write_k<PK, OK, JW_DIRECT + S_MAXMULT><<<g, 256, 0, st>>>(jp, offs, start, total);
+}
+
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
                        cudaStream_t st) {
   if (total <= 0) return;
   const unsigned g = (unsigned)((total + WT - 1) / WT);
   note_launch();
-  if (jp.pk32 && jp.ok32) join_write_k<uint32_t, uint32_t><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else if (jp.pk32) join_write_k<uint32_t, uint64_t><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else if (jp.ok32) join_write_k<uint64_t, uint32_t><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else join_write_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(jp, offs, start, total);
+  if (jp.pk32 && jp.ok32) launch_join_write_t<uint32_t, uint32_t>(jp, offs, start, total, g, st);
+  else if (jp.pk32) launch_join_write_t<uint32_t, uint64_t>(jp, offs, start, total, g, st);
+  else if (jp.ok32) launch_join_write_t<uint64_t, uint32_t>(jp, offs, start, total, g, st);
+  else launch_join_write_t<uint64_t, uint64_t>(jp, offs, start, total, g, st);
 }
 
 template <typename PK, int SEMI, int NM>
