@@ -1072,7 +1072,7 @@ struct Ctx {
         Phase ph(this, 0);
         merge_moves(jp.om, jp.nom);
         merge_moves(jp.wm, jp.nwm);
-        launch_join_write(jp, offs, start_, total, st);
+        launch_join_write(jp, offs, start_, total, arena.get<int64_t>(join_write_tiles(total) + 1), st);
         kcheck("join write");
       }
       if (last) {

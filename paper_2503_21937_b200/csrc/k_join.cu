@@ -76,55 +76,78 @@ __device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int semi, int
   return t;
 }
 
-// Largest r in [lo, hi) with offs[r] <= o (offs non-decreasing, offs[lo] <= o),
-// found by the whole CTA: each round 256 threads probe 256 evenly spaced rows
-// and __syncthreads_count narrows the range 256x (3 rounds for 10^7 rows)
-// instead of one thread walking ~24 dependent loads while the CTA waits.
-__device__ __forceinline__ int64_t coop_row(const int64_t* __restrict__ offs, int64_t o, int64_t lo, int64_t hi) {
-  while (hi - lo > 1) {
-    const int64_t stride = (hi - lo + 255) >> 8;
-    const int64_t idx = lo + (int64_t)threadIdx.x * stride;
-    const int c = __syncthreads_count(idx < hi && __ldg(offs + idx) <= o);
-    const int64_t nlo = lo + (int64_t)(c - 1) * stride;
-    hi = nlo + stride < hi ? nlo + stride : hi;
-    lo = nlo;
-  }
-  return lo;
-}
-
 // MODE (compile time, keeps each variant's code small): JW_INTER = intermediate
 // rows (final_step 0), JW_CAND = candidates (semiring at run time), JW_DIRECT +
 // semiring = direct ⊕ into the dense store.
 constexpr int JW_INTER = 0, JW_CAND = 1, JW_DIRECT = 2;
 
+// Tile -> first probe row: row i owns output slots [offs[i], offs[i+1]); every
+// tile whose first slot t*WT falls in that range starts at row i.  One pass
+// over the offsets (coalesced) instead of a per-CTA search of them.
+__global__ void tile_rows_k(const int64_t* __restrict__ offs, int64_t np, int64_t total, int64_t ntiles,
+                            int64_t* __restrict__ tile_row) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = offs[i], b = i + 1 < np ? offs[i + 1] : total;
+    for (int64_t t = (a + WT - 1) / WT; t * WT < b; ++t) tile_row[t] = i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) tile_row[ntiles] = np - 1;
+}
+
 template <typename PK, typename OK, int MODE>
 __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int64_t* __restrict__ offs,
-                                                    const int64_t* __restrict__ start, int64_t total) {
+                                                    const int64_t* __restrict__ start, int64_t total,
+                                                    const int64_t* __restrict__ tile_row) {
   constexpr bool FINAL = MODE != JW_INTER;
   constexpr bool DIRECT = MODE >= JW_DIRECT;
   const int semi = DIRECT ? MODE - JW_DIRECT : jp.semi;
-  // the tile's probe rows, staged: row start relative to the tile (only row 0
-  // can start before it: clamped to -1), build-index delta start - offs (so a
-  // slot's build row is j = sdel + o) and the probe key
-  __shared__ int32_t soff[WROWS];
+  // the tile's probe rows, staged: build-index delta start - offs (so a slot's
+  // build row is j = sdel + o) and the probe key; srow[k] = the tile-local row
+  // of output slot o0 + k, by scattering each row's index to its first slot
+  // and an inclusive max-scan over the tile (no per-slot binary search)
+  __shared__ int32_t srow[WT];
   __shared__ int64_t sdel[WROWS];
   __shared__ PK spk[WROWS];
+  __shared__ int32_t wmax[8];
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   OK* __restrict__ okey = reinterpret_cast<OK*>(jp.okey);
   const int64_t o0 = (int64_t)blockIdx.x * WT;
   if (o0 >= total) return;
   const int64_t o1 = (o0 + WT < total ? o0 + WT : total) - 1;
-  const int64_t r0 = coop_row(offs, o0, 0, jp.np);
-  const int64_t r1 = coop_row(offs, o1, r0, jp.np);
+  // r1 may overshoot by rows that start after the tile (harmless: they own no slot here)
+  const int64_t r0 = tile_row[blockIdx.x];
+  const int64_t r1 = tile_row[blockIdx.x + 1];
   const int nrows = (int)(r1 - r0 + 1);
   const bool staged = r1 - r0 + 1 <= WROWS;
-  if (staged)
+  if (staged) {
+#pragma unroll
+    for (int q = 0; q < SPT; ++q) srow[threadIdx.x + q * 256] = (threadIdx.x + q * 256) == 0 ? 0 : -1;
+    __syncthreads();
     for (int i = threadIdx.x; i < nrows; i += blockDim.x) {
       const int64_t of = offs[r0 + i];
-      soff[i] = of < o0 ? -1 : (int32_t)(of - o0);
+      if (of >= o0 && of - o0 < WT) atomicMax(&srow[of - o0], i);  // equal offsets: the last row owns the slots
       sdel[i] = start[r0 + i] - of;
       spk[i] = pkey[r0 + i];
     }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int v[SPT];
+    int m = -1;
+#pragma unroll
+    for (int q = 0; q < SPT; ++q) {
+      m = max(m, srow[threadIdx.x * SPT + q]);
+      v[q] = m;
+    }
+    int inc = m;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) inc = max(inc, __shfl_up_sync(0xffffffffu, inc, d));
+    if (lane == 31) wmax[warp] = inc;
+    int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = -1;
+    __syncthreads();
+    for (int q = 0; q < warp; ++q) ex = max(ex, wmax[q]);
+#pragma unroll
+    for (int q = 0; q < SPT; ++q) srow[threadIdx.x * SPT + q] = max(v[q], ex);
+  }
   __syncthreads();
   // phase 1: resolve every slot of this thread (independent loads in flight)
   int64_t rowv[SPT], jv[SPT];
@@ -135,15 +158,10 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
     rowv[k] = -1;
     if (o > o1) continue;
     if (staged) {
-      const int32_t lo32 = (int32_t)(o - o0);
-      int lo = 0, hi = nrows;  // largest i with soff[i] <= o - o0
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (soff[mid] <= lo32) lo = mid + 1; else hi = mid;
-      }
-      rowv[k] = r0 + lo - 1;
-      jv[k] = sdel[lo - 1] + o;
-      pkv[k] = spk[lo - 1];
+      const int li = srow[threadIdx.x + k * 256];
+      rowv[k] = r0 + li;
+      jv[k] = sdel[li] + o;
+      pkv[k] = spk[li];
     } else {
       int64_t lo = r0, hi = r1 + 1;
       while (lo < hi) {
@@ -203,8 +221,8 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
         oldv[k] = direct_peek(semi, jp.fdir, slotv[k]);
       }
       direct_commit<SPT>(semi, jp.fdir, jp.dirty, slotv, newv, oldv, live);
-    } else {
-#pragma unroll
+    } else {  // narrow heads (rare): warp pre-aggregation, rolled to keep the code small
+#pragma unroll 1
       for (int k = 0; k < SPT; ++k)
         if (rowv[k] >= 0 && okv[k])
           direct_oplus(semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate);
@@ -479,23 +497,29 @@ void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaS
 
 template <typename PK, typename OK>
 static void launch_join_write_t(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
-                                unsigned g, cudaStream_t st) {
-  if (!jp.final_step) join_write_k<PK, OK, JW_INTER><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else if (!jp.direct) join_write_k<PK, OK, JW_CAND><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else if (jp.semi == S_UNIT) join_write_k<PK, OK, JW_DIRECT + S_UNIT><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else if (jp.semi == S_MAXMIN) join_write_k<PK, OK, JW_DIRECT + S_MAXMIN><<<g, 256, 0, st>>>(jp, offs, start, total);
-  else join_write_k<PK, OK, JW_DIRECT + S_MAXMULT><<<g, 256, 0, st>>>(jp, offs, start, total);
+                                unsigned g, int64_t* tile_row, cudaStream_t st) {
+  int64_t* tr = tile_row;
+  if (!jp.final_step) join_write_k<PK, OK, JW_INTER><<<g, 256, 0, st>>>(jp, offs, start, total, tr);
+  else if (!jp.direct) join_write_k<PK, OK, JW_CAND><<<g, 256, 0, st>>>(jp, offs, start, total, tr);
+  else if (jp.semi == S_UNIT) join_write_k<PK, OK, JW_DIRECT + S_UNIT><<<g, 256, 0, st>>>(jp, offs, start, total, tr);
+  else if (jp.semi == S_MAXMIN) join_write_k<PK, OK, JW_DIRECT + S_MAXMIN><<<g, 256, 0, st>>>(jp, offs, start, total, tr);
+  else join_write_k<PK, OK, JW_DIRECT + S_MAXMULT><<<g, 256, 0, st>>>(jp, offs, start, total, tr);
 }
 
+int64_t join_write_tiles(int64_t total) { return (total + WT - 1) / WT; }
+
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
-                       cudaStream_t st) {
+                       int64_t* tile_row, cudaStream_t st) {
   if (total <= 0) return;
-  const unsigned g = (unsigned)((total + WT - 1) / WT);
+  const int64_t nt = join_write_tiles(total);
+  const unsigned g = (unsigned)nt;
   note_launch();
-  if (jp.pk32 && jp.ok32) launch_join_write_t<uint32_t, uint32_t>(jp, offs, start, total, g, st);
-  else if (jp.pk32) launch_join_write_t<uint32_t, uint64_t>(jp, offs, start, total, g, st);
-  else if (jp.ok32) launch_join_write_t<uint64_t, uint32_t>(jp, offs, start, total, g, st);
-  else launch_join_write_t<uint64_t, uint64_t>(jp, offs, start, total, g, st);
+  tile_rows_k<<<grid_for(jp.np, 256), 256, 0, st>>>(offs, jp.np, total, nt, tile_row);
+  note_launch();
+  if (jp.pk32 && jp.ok32) launch_join_write_t<uint32_t, uint32_t>(jp, offs, start, total, g, tile_row, st);
+  else if (jp.pk32) launch_join_write_t<uint32_t, uint64_t>(jp, offs, start, total, g, tile_row, st);
+  else if (jp.ok32) launch_join_write_t<uint64_t, uint32_t>(jp, offs, start, total, g, tile_row, st);
+  else launch_join_write_t<uint64_t, uint64_t>(jp, offs, start, total, g, tile_row, st);
 }
 
 template <typename PK, int SEMI, int NM>

@@ -214,8 +214,10 @@ void launch_edb_reduce(const uint64_t* key, const float* p, const int32_t* fid, 
 
 // ---- join (A3-A5) ----
 void launch_join_count(const JoinPlan& jp, int64_t* count, int64_t* start, cudaStream_t st);
+// tile_row: join_write_tiles(total) + 1 int64 scratch
+int64_t join_write_tiles(int64_t total);
 void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* start, int64_t total,
-                       cudaStream_t st);
+                       int64_t* tile_row, cudaStream_t st);
 void launch_project(const ProjectPlan& pp, cudaStream_t st);
 // fused row-centric join + direct ⊕ (bounded fan-out <= 8 per prefix); adds |C| to *ncand
 // With jp.np_dev (Δ size on the device) the grid is persistent.
