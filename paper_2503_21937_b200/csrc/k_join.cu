@@ -397,66 +397,163 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
   if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
 }
 
-template <typename PK, typename OK>
+// MODE: LC_CAND = candidates (semiring at run time), LC_DIRECT + semiring =
+// direct ⊕ into the dense store (compile time: small code, no semiring branches).
+constexpr int LC_CAND = 0, LC_DIRECT = 1;
+
+// One probe row of a lookup chain: filters, point lookups, ⊗ in body order,
+// witness and head key.  Returns whether the row yields a candidate.
+template <typename PK>
+__device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pkr, int64_t i, float& t, uint32_t& w,
+                                           uint64_t& key) {
+  bool ok = pkr != dead<PK>();
+  const uint64_t pk = (uint64_t)pkr;
+#pragma unroll 1
+  for (int c = 0; c < lp.ncmp; ++c) {
+    const int64_t a = operand_value(lp.cmp[c].a, pk, 0);
+    const int64_t b = operand_value(lp.cmp[c].b, pk, 0);
+    ok &= lp.cmp[c].neq ? (a != b) : (a == b);
+  }
+  float tags[MAXL + 1];
+  tags[0] = (semi != S_UNIT && lp.ptag && ok) ? lp.ptag[i] : 1.0f;
+#pragma unroll
+  for (int l = 0; l < MAXL; ++l) {
+    tags[l + 1] = 1.0f;
+    if (l >= lp.nlk || !ok) continue;
+    const Lookup& L = lp.lk[l];
+    const uint64_t pre = L.cprefix | apply_moves(L.prem, L.nprem, pk, 0);
+    int64_t j = -1;
+    if (L.boff) {
+      if (pre < (uint64_t)L.nprefix) {
+        const int64_t b0 = L.boff[pre];
+        if (L.boff[pre + 1] > b0) j = b0;
+      }
+    } else {
+      const int64_t q = lower_bound_u64(L.bkey, L.nb, pre);
+      if (q < L.nb && L.bkey[q] == pre) j = q;
+    }
+    if (j < 0) ok = false;
+    else if (semi != S_UNIT && L.btag) tags[l + 1] = L.btag[j];
+  }
+  t = 1.0f;
+  w = 0;
+  if (ok && semi != S_UNIT) {
+    auto pick = [&](int idx) {
+      float r = tags[0];
+#pragma unroll
+      for (int k = 1; k <= MAXL; ++k)
+        if (k == idx) r = tags[k];
+      return r;
+    };
+    t = pick(lp.tag_order[0]);
+#pragma unroll 1
+    for (int k = 1; k < lp.ntag; ++k) t = otimes(semi, t, pick(lp.tag_order[k]));
+    if (semi == S_MAXMULT) w = lp.wconst | (uint32_t)apply_moves(lp.wm, lp.nwm, pk, 0);
+  }
+  key = lp.cout | apply_moves(lp.om, lp.nom, pk, 0);
+  return ok;
+}
+
+template <int SEMI>
+__device__ __forceinline__ unsigned long long agg_pack(float p, uint32_t w) {
+  if (SEMI == S_MAXMIN) return (unsigned long long)((f2u(p) + 1u) << 1);
+  if (SEMI == S_MAXMULT) return ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
+  return 1ull;
+}
+
+// warp max of the lanes' packed values, one atomic for the warp's slot
+template <int SEMI>
+__device__ __forceinline__ void agg_flush(void* f, uint32_t* dirty, uint32_t slot, unsigned long long v) {
+  if (SEMI == S_MAXMIN) {
+    const uint32_t m = __reduce_max_sync(0xffffffffu, (uint32_t)v);
+    if ((threadIdx.x & 31) == 0 && m) {
+      const uint32_t old = atomicMax(reinterpret_cast<uint32_t*>(f) + slot, m);
+      if (old < m && (old == 0u || (old & 1u))) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
+    }
+  } else if (SEMI == S_MAXMULT) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, d);
+      v = u > v ? u : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v) {
+      const unsigned long long old = atomicMax(reinterpret_cast<unsigned long long*>(f) + slot, v);
+      if (old < v && (old == 0ull || ((old >> 32) & 1ull))) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
+    }
+  } else {
+    if (__any_sync(0xffffffffu, v != 0ull) && (threadIdx.x & 31) == 0) {
+      const uint32_t bit = 1u << (slot & 31u);
+      const uint32_t old = atomicOr(reinterpret_cast<uint32_t*>(f) + (slot >> 5), bit);
+      if (!(old & bit)) atomicOr(dirty + (slot >> 5), bit);
+    }
+  }
+}
+
+template <typename PK, typename OK, int MODE>
 __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsigned long long* __restrict__ ncand) {
+  constexpr bool DIRECT = MODE >= LC_DIRECT;
+  constexpr int SEMI_C = DIRECT ? MODE - LC_DIRECT : -1;
+  const int semi = DIRECT ? SEMI_C : lp.semi;
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(lp.pkey);
   OK* __restrict__ okey = reinterpret_cast<OK*>(lp.okey);
   uint32_t mycount = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lp.np;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const PK pkr = pkey[i];
-    bool ok = pkr != dead<PK>();
-    const uint64_t pk = (uint64_t)pkr;
-    for (int c = 0; c < lp.ncmp; ++c) {
-      const int64_t a = operand_value(lp.cmp[c].a, pk, 0);
-      const int64_t b = operand_value(lp.cmp[c].b, pk, 0);
-      ok &= lp.cmp[c].neq ? (a != b) : (a == b);
-    }
-    float tags[MAXL + 1];
-    tags[0] = (lp.semi != S_UNIT && lp.ptag) ? lp.ptag[i] : 1.0f;
-#pragma unroll
-    for (int l = 0; l < MAXL; ++l) {
-      if (l >= lp.nlk) break;
-      tags[l + 1] = 1.0f;
-      if (!ok) continue;
-      const Lookup& L = lp.lk[l];
-      const uint64_t pre = L.cprefix | apply_moves(L.prem, L.nprem, pk, 0);
-      int64_t j = -1;
-      if (L.boff) {
-        if (pre < (uint64_t)L.nprefix && L.boff[pre + 1] > L.boff[pre]) j = L.boff[pre];
-      } else {
-        const int64_t q = lower_bound_u64(L.bkey, L.nb, pre);
-        if (q < L.nb && L.bkey[q] == pre) j = q;
+  if (DIRECT && lp.aggregate) {
+    // Narrow head (e.g. endpoints_connected(): ~1M candidates per slot, rows
+    // sorted by sample): each warp walks a contiguous chunk 32 rows at a time
+    // and keeps a per-lane running max while all its live rows aim at one
+    // slot; one warp reduction + one atomic per (warp, slot) segment instead
+    // of one per 32 rows (same-address atomics serialise in L2).
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t chunk = ((lp.np + nwarps - 1) / nwarps + 31) & ~(int64_t)31;
+    const int64_t r0 = wid * chunk, r1 = r0 + chunk < lp.np ? r0 + chunk : lp.np;
+    uint32_t cur = 0xffffffffu;
+    unsigned long long run = 0;
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int64_t i = base + (threadIdx.x & 31);
+      const PK pkr = i < r1 ? pkey[i] : dead<PK>();
+      float t;
+      uint32_t w;
+      uint64_t key;
+      const bool ok = lookup_row<PK>(lp, SEMI_C, pkr, i, t, w, key);
+      if (ok) ++mycount;
+      const uint32_t slot = (uint32_t)key;
+      const unsigned act = __ballot_sync(0xffffffffu, ok);
+      if (!act) continue;
+      const uint32_t s0 = __shfl_sync(0xffffffffu, slot, __ffs(act) - 1);
+      const bool uniform = __all_sync(0xffffffffu, !ok || slot == s0);
+      if (uniform && s0 == cur) {
+        const unsigned long long v = ok ? agg_pack<SEMI_C>(t, w) : 0ull;
+        run = v > run ? v : run;
+        continue;
       }
-      if (j < 0) ok = false;
-      else if (lp.semi != S_UNIT && L.btag) tags[l + 1] = L.btag[j];
+      if (cur != 0xffffffffu) agg_flush<SEMI_C>(lp.fdir, lp.dirty, cur, run);
+      run = 0;
+      cur = 0xffffffffu;
+      if (uniform) {
+        cur = s0;
+        run = ok ? agg_pack<SEMI_C>(t, w) : 0ull;
+      } else if (ok) {
+        direct_oplus(SEMI_C, lp.fdir, slot, t, w, lp.dirty, 1);
+      }
     }
-    float t = 1.0f;
-    uint32_t w = 0;
-    if (ok && lp.semi != S_UNIT) {
-      float v[MAXL + 1];
-#pragma unroll
-      for (int k = 0; k <= MAXL; ++k) v[k] = tags[k];
-      auto pick = [&](int idx) {
-        float r = v[0];
-#pragma unroll
-        for (int k = 1; k <= MAXL; ++k)
-          if (k == idx) r = v[k];
-        return r;
-      };
-      t = pick(lp.tag_order[0]);
-      for (int k = 1; k < lp.ntag; ++k) t = otimes(lp.semi, t, pick(lp.tag_order[k]));
-      if (lp.semi == S_MAXMULT) w = lp.wconst | (uint32_t)apply_moves(lp.wm, lp.nwm, pk, 0);
+    if (cur != 0xffffffffu) agg_flush<SEMI_C>(lp.fdir, lp.dirty, cur, run);
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lp.np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float t;
+      uint32_t w;
+      uint64_t key;
+      const bool ok = lookup_row<PK>(lp, semi, pkey[i], i, t, w, key);
+      if (ok) ++mycount;
+      if constexpr (DIRECT) {
+        if (ok) direct_oplus(SEMI_C, lp.fdir, (uint32_t)key, t, w, lp.dirty, 0);
+      } else {
+        okey[i] = ok ? (OK)key : dead<OK>();
+        if (semi == S_MAXMULT) lp.oval64[i] = (uint64_t)f2u(t) | ((uint64_t)w << 32);
+        else if (semi != S_UNIT) lp.oval32[i] = f2u(t);
+      }
     }
-    const uint64_t key = lp.cout | apply_moves(lp.om, lp.nom, pk, 0);
-    if (ok) ++mycount;
-    if (lp.direct) {
-      if (ok) direct_oplus(lp.semi, lp.fdir, (uint32_t)key, t, w, lp.dirty, lp.aggregate);
-      continue;
-    }
-    okey[i] = ok ? (OK)key : dead<OK>();
-    if (lp.semi == S_MAXMULT) lp.oval64[i] = (uint64_t)f2u(t) | ((uint64_t)w << 32);
-    else if (lp.semi != S_UNIT) lp.oval32[i] = f2u(t);
   }
   mycount = __reduce_add_sync(0xffffffffu, mycount);
   if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
@@ -550,14 +647,22 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
   }
 }
 
+template <typename PK, typename OK>
+static void launch_lookup_chain_t(const LookupPlan& lp, unsigned long long* ncand, int g, cudaStream_t st) {
+  if (!lp.direct) lookup_chain_k<PK, OK, LC_CAND><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.semi == S_UNIT) lookup_chain_k<PK, OK, LC_DIRECT + S_UNIT><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.semi == S_MAXMIN) lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMIN><<<g, 256, 0, st>>>(lp, ncand);
+  else lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMULT><<<g, 256, 0, st>>>(lp, ncand);
+}
+
 void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaStream_t st) {
   if (lp.np <= 0) return;
   const int g = grid_for(lp.np, 256);
   note_launch();
-  if (lp.pk32 && lp.ok32) lookup_chain_k<uint32_t, uint32_t><<<g, 256, 0, st>>>(lp, ncand);
-  else if (lp.pk32) lookup_chain_k<uint32_t, uint64_t><<<g, 256, 0, st>>>(lp, ncand);
-  else if (lp.ok32) lookup_chain_k<uint64_t, uint32_t><<<g, 256, 0, st>>>(lp, ncand);
-  else lookup_chain_k<uint64_t, uint64_t><<<g, 256, 0, st>>>(lp, ncand);
+  if (lp.pk32 && lp.ok32) launch_lookup_chain_t<uint32_t, uint32_t>(lp, ncand, g, st);
+  else if (lp.pk32) launch_lookup_chain_t<uint32_t, uint64_t>(lp, ncand, g, st);
+  else if (lp.ok32) launch_lookup_chain_t<uint64_t, uint32_t>(lp, ncand, g, st);
+  else launch_lookup_chain_t<uint64_t, uint64_t>(lp, ncand, g, st);
 }
 
 __global__ void max_degree_k(const int64_t* __restrict__ off, int64_t np, unsigned long long* __restrict__ out) {
