@@ -63,12 +63,16 @@ class _CudaArray:
         self._owner = owner
 
 
-def _np_view(ptr, n, dtype):
+def _np_view(ptr, n, dtype, copy=True):
     if n == 0 or not ptr:
         return np.zeros(0, dtype=dtype)
     ct = {np.int32: ctypes.c_int32, np.int64: ctypes.c_int64, np.float32: ctypes.c_float}[dtype]
     arr = (ct * n).from_address(ptr)
-    return np.frombuffer(arr, dtype=dtype, count=n).copy()
+    v = np.frombuffer(arr, dtype=dtype, count=n)
+    if copy:
+        return v.copy()
+    v.flags.writeable = False
+    return v
 
 
 @dataclass
@@ -166,21 +170,29 @@ class Engine:
         return int(self._L.lobster_num_facts(self._h))
 
     # ---------------------------------------------------------------- output
-    def output(self, relation: str, device: bool = False) -> RelationOutput:
+    def output(self, relation: str, device: bool = False, copy: bool = True) -> RelationOutput:
+        """device=False: numpy arrays of the host copy (lobster_output_get where=0).  With
+        copy=False they are read-only views of the context's pinned buffers — no extra host
+        copy — valid until the next push / run / close (the C ABI's lifetime rule)."""
         o = _lib.Output()
         self._check(self._L.lobster_output_get(self._h, relation.encode(), 1 if device else 0, ctypes.byref(o)))
         n, ar = int(o.n), int(o.arity)
         if not device:
-            cols = np.stack([_np_view(o.columns[c], n, np.int32) for c in range(ar)]) if ar else np.zeros((0, n), np.int32)
-            out = RelationOutput(n, ar, _np_view(o.sample_ids, n, np.int32), cols,
-                                 _np_view(o.probs, n, np.float32) if self.semiring != _lib.UNIT else None,
-                                 _np_view(o.sample_offsets, self.batch_size + 1, np.int64))
+            if ar and not copy:  # columns are one arity x n block in the context's buffer
+                cols = _np_view(o.columns[0], ar * n, np.int32, False).reshape(ar, n)
+            elif ar:
+                cols = np.stack([_np_view(o.columns[c], n, np.int32) for c in range(ar)])
+            else:
+                cols = np.zeros((0, n), np.int32)
+            out = RelationOutput(n, ar, _np_view(o.sample_ids, n, np.int32, copy), cols,
+                                 _np_view(o.probs, n, np.float32, copy) if self.semiring != _lib.UNIT else None,
+                                 _np_view(o.sample_offsets, self.batch_size + 1, np.int64, copy))
             if o.grad_offsets or (self.semiring == _lib.DIFF_MAX_MULT_PROB and n == 0 and o.grad_offsets is not None):
-                goff = _np_view(o.grad_offsets, n + 1, np.int64) if n else np.zeros(1, np.int64)
+                goff = _np_view(o.grad_offsets, n + 1, np.int64, copy) if n else np.zeros(1, np.int64)
                 ng = int(goff[-1]) if n else 0
                 out.grad_offsets = goff
-                out.grad_fact_ids = _np_view(o.grad_fact_ids, ng, np.int64)
-                out.grad_values = _np_view(o.grad_values, ng, np.float32)
+                out.grad_fact_ids = _np_view(o.grad_fact_ids, ng, np.int64, copy)
+                out.grad_values = _np_view(o.grad_values, ng, np.float32, copy)
             return out
         import torch
         dev = torch.device("cuda", torch.cuda.current_device())
