@@ -1300,11 +1300,11 @@ struct Ctx {
     S.cand_bound = 0;
     S.dkey32.reserve(cap);
     if (semi != S_UNIT) S.dp.reserve(cap);
-    if (semi == S_MAXMULT) S.dw.reserve(cap);
-    {  // Δ' in slot order (two launches); dirty bits cleared, slots re-settled
+    {  // Δ' in slot order (two launches); dirty bits cleared, slots re-settled.  Joins read
+       // Δ keys and p only (a candidate's witness comes from its own body), so no Δ' witness.
       Phase ph(this, 3);
       launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
-                             semi != S_UNIT ? S.dp.ptr() : nullptr, semi == S_MAXMULT ? S.dw.ptr() : nullptr,
+                             semi != S_UNIT ? S.dp.ptr() : nullptr, nullptr,
                              arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(), st);
       kcheck("direct extract");
     }
@@ -1608,7 +1608,7 @@ struct Ctx {
     for (int r : strat) {
       RelState& S = *rels[r];
       if (!S.direct) return false;
-      const size_t row = 4 + (semi == S_UNIT ? 0 : 4) + (semi == S_MAXMULT ? 4 : 0);
+      const size_t row = 4 + (semi == S_UNIT ? 0 : 4);
       if (S.dkey32.bytes() < (size_t)S.nslots * 4) need += (size_t)S.nslots * row;
     }
     if (need) {

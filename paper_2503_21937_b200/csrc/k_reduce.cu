@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
           __stcg(reinterpret_cast<unsigned long long*>(f) + slotv[u], v[u] | (1ull << 32));
           dkey[o] = slotv[u];
           dp[o] = u2f((uint32_t)(v[u] >> 33) - 1u);
-          dw[o] = ~(uint32_t)v[u];
+          if (dw) dw[o] = ~(uint32_t)v[u];
         }
       } else {
 #pragma unroll

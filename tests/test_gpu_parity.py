@@ -278,6 +278,40 @@ def test_iteration_cap():
     assert e.value.status == _lib.E_ITER_CAP
 
 
+@pytest.mark.parametrize("sr", [1, 3])
+def test_iteration_cap_async_rounds(sr, monkeypatch):
+    """The cap stops the asynchronous (device-sized) rounds at exactly max_iters:
+    the readable state equals the host-synchronised engine's at the same cap."""
+    from paper_2503_21937_b200 import Engine, LobsterError, _lib
+    w = W.c2_workload(semiring=sr, n=8, batch=3)
+    outs = []
+    for sync in (False, True):
+        if sync:
+            monkeypatch.setenv("LOBSTER_SYNC_ROUNDS", "1")
+        eng = Engine(w.program, sr, batch_size=w.batch_size, max_iters=9)
+        eng.push_facts(w.facts)
+        with pytest.raises(LobsterError) as e:
+            eng.run()
+        assert e.value.status == _lib.E_ITER_CAP
+        o = eng.output("path")
+        outs.append((o.sample_ids.copy(), o.cols.copy(), o.probs.copy()))
+    (s0, c0, p0), (s1, c1, p1) = outs
+    assert np.array_equal(s0, s1) and np.array_equal(c0, c1)
+    assert np.array_equal(p0.view(np.uint32), p1.view(np.uint32))
+
+
+def test_host_output_views():
+    """output(copy=False): read-only views of the pinned host copy, equal to the copies."""
+    w = W.c2_workload(semiring=3, n=6, batch=3)
+    eng, _, _ = engine_run(w)
+    a = eng.output("path")
+    b = eng.output("path", copy=False)
+    assert not b.probs.flags.writeable
+    assert np.array_equal(a.sample_ids, b.sample_ids) and np.array_equal(a.cols, b.cols)
+    assert np.array_equal(a.probs, b.probs) and np.array_equal(a.sample_offsets, b.sample_offsets)
+    assert np.array_equal(a.grad_offsets, b.grad_offsets) if a.grad_offsets is not None else b.grad_offsets is None
+
+
 def test_rerun_new_database():
     """A push after a run starts a new database (header contract)."""
     w1 = W.c2_workload(semiring=1, n=5, batch=2)
@@ -292,11 +326,12 @@ def test_rerun_new_database():
     assert_parity(eng, res, "path", 1)
 
 
-@pytest.mark.parametrize("env", ["LOBSTER_SORTED_STORE", "LOBSTER_SORT_DEDUP"])
+@pytest.mark.parametrize("env", ["LOBSTER_SORTED_STORE", "LOBSTER_SORT_DEDUP", "LOBSTER_SYNC_ROUNDS"])
 @pytest.mark.parametrize("sr", [0, 1, 3])
 def test_store_paths_match(sr, env, monkeypatch):
     """Every relation-store path (merge-based sorted store; dense store with
-    radix sort + segmented ⊕; default dense direct ⊕) matches the oracle."""
+    radix sort + segmented ⊕; default dense direct ⊕, with host-synchronised
+    rounds as well as the default asynchronous ones) matches the oracle."""
     monkeypatch.setenv(env, "1")
     w = W.c2_workload(semiring=sr, n=8, batch=5)
     eng, stats, res = run_both(w, outputs=["path", "endpoints_connected"])
