@@ -70,6 +70,12 @@ __device__ __forceinline__ int64_t upper_bound_m1_i64(const int64_t* __restrict_
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 
+// max-min direct-store word: fp32 bits of p (p >= 0: order-preserving) + 1, 0 =
+// absent.  No settled bit: an equal p is never an improvement (no witness to
+// tie-break), so a slot is only rewritten when p strictly grows.
+__device__ __forceinline__ uint32_t mm_word(float p) { return f2u(p) + 1u; }
+__device__ __forceinline__ float mm_p(uint32_t v) { return u2f(v - 1u); }
+
 // ⊗: one IEEE fp32 op, no contraction (reading 9)
 __device__ __forceinline__ float otimes(int semi, float a, float b) {
   if (semi == S_MAXMIN) return a < b ? a : b;
@@ -90,7 +96,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
     const uint32_t old = atomicOr(reinterpret_cast<uint32_t*>(f) + (slot >> 5), bit);
     app = !(old & bit);
   } else if (semi == S_MAXMIN) {
-    uint32_t v = (f2u(p) + 1u) << 1;
+    uint32_t v = mm_word(p);
     bool lead = true;
     if (aggregate) {
       cg::coalesced_group part = cg::labeled_partition(cg::coalesced_threads(), (int)slot);
@@ -99,7 +105,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
     }
     if (lead) {
       const uint32_t old = atomicMax(reinterpret_cast<uint32_t*>(f) + slot, v);
-      app = old < v && (old == 0u || (old & 1u));
+      app = old < v;  // any improvement marks the slot (idempotent OR)
     }
   } else {
     unsigned long long v = ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
@@ -125,7 +131,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
 // the remaining updates and dirty bits as fire-and-forget reductions.
 __device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slot, float t, uint32_t w) {
   if (semi == S_UNIT) return 1ull << (slot & 31u);
-  if (semi == S_MAXMIN) return (unsigned long long)((f2u(t) + 1u) << 1);
+  if (semi == S_MAXMIN) return (unsigned long long)mm_word(t);
   return ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
 }
 

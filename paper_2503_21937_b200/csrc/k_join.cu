@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
       const float bt = jp.btag[lo + d];
       const float t = jp.tag_order[0] == 0 ? otimes(SEMI, pt, bt) : otimes(SEMI, bt, pt);
       if (SEMI == S_MAXMIN) {
-        newv[d] = (f2u(t) + 1u) << 1;
+        newv[d] = mm_word(t);
         oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
       } else {
         const uint32_t w = jp.wconst | (uint32_t)moves_n<NM>(jp.wm, jp.nwm, pk, bk);
@@ -456,7 +456,7 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
 
 template <int SEMI>
 __device__ __forceinline__ unsigned long long agg_pack(float p, uint32_t w) {
-  if (SEMI == S_MAXMIN) return (unsigned long long)((f2u(p) + 1u) << 1);
+  if (SEMI == S_MAXMIN) return (unsigned long long)mm_word(p);
   if (SEMI == S_MAXMULT) return ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
   return 1ull;
 }
@@ -468,7 +468,7 @@ __device__ __forceinline__ void agg_flush(void* f, uint32_t* dirty, uint32_t slo
     const uint32_t m = __reduce_max_sync(0xffffffffu, (uint32_t)v);
     if ((threadIdx.x & 31) == 0 && m) {
       const uint32_t old = atomicMax(reinterpret_cast<uint32_t*>(f) + slot, m);
-      if (old < m && (old == 0u || (old & 1u))) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
+      if (old < m) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
     }
   } else if (SEMI == S_MAXMULT) {
 #pragma unroll

@@ -441,186 +441,12 @@ __device__ __forceinline__ void direct_decode(const void* f, int semi, int64_t s
   } else if (semi == S_MAXMIN) {
     const uint32_t v = reinterpret_cast<const uint32_t*>(f)[slot];
     present = v != 0u;
-    p = u2f((v >> 1) - 1u);
+    p = mm_p(v);
   } else {
     const unsigned long long v = reinterpret_cast<const unsigned long long*>(f)[slot];
     present = v != 0ull;
     p = u2f((uint32_t)(v >> 33) - 1u);
     w = ~(uint32_t)v;
-  }
-}
-
-// dirty bitmap -> Δ': per-word popcounts, exclusive scan, then each word's set
-// bits are written in slot order (Δ' sorted by key), re-settled and cleared.
-__global__ void direct_dirty_count_k(const uint32_t* __restrict__ dirty, int64_t nw, uint32_t* __restrict__ cnt) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
-    cnt[i] = __popc(dirty[i]);
-}
-
-__global__ void direct_dirty_extract_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
-                                       const uint32_t* __restrict__ pos, int64_t nw, int semi,
-                                       uint32_t* __restrict__ dkey, float* __restrict__ dp,
-                                       uint32_t* __restrict__ dw) {
-  for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t m = dirty[wi];
-    if (!m) continue;
-    dirty[wi] = 0u;
-    uint32_t o = pos[wi];
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1u;
-      const uint32_t slot = (uint32_t)(wi * 32 + b);
-      dkey[o] = slot;
-      if (semi == S_MAXMIN) {
-        uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
-        const uint32_t v = *a;
-        *a = v | 1u;
-        dp[o] = u2f((v >> 1) - 1u);
-      } else if (semi == S_MAXMULT) {
-        unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
-        const unsigned long long v = *a;
-        *a = v | (1ull << 32);
-        dp[o] = u2f((uint32_t)(v >> 33) - 1u);
-        dw[o] = ~(uint32_t)v;
-      }
-      ++o;
-    }
-  }
-}
-
-// Single pass: each CTA tile = 1024 dirty words (4 consecutive per thread,
-// one 16-B load), block scan of popcounts, one global atomic per tile for the
-// output base.  Slots come out sorted within a tile (tiles in any order;
-// results do not depend on Δ order under idempotent ⊕).
-__global__ void __launch_bounds__(256) direct_extract1_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
-                                                         int64_t nw, int semi, uint32_t* __restrict__ dkey,
-                                                         float* __restrict__ dp, uint32_t* __restrict__ dw,
-                                                         unsigned long long* __restrict__ counter,
-                                                         const uint32_t* __restrict__ tile_base) {
-  // A tile is 4 sub-tiles of 256 words, one word per thread (short serial bit
-  // loops); tile bases come from the scanned tile popcounts (slot order).
-  __shared__ uint32_t wsum[8];
-  __shared__ uint32_t s_run;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  (void)counter;
-  for (int64_t base = (int64_t)blockIdx.x * 1024; base < nw; base += (int64_t)gridDim.x * 1024) {
-    if (threadIdx.x == 0) s_run = tile_base[base / 1024];
-    __syncthreads();
-#pragma unroll 1
-    for (int k = 0; k < 4; ++k) {
-      const int64_t w = base + k * 256 + threadIdx.x;
-      uint32_t m = w < nw ? dirty[w] : 0u;
-      const uint32_t c = __popc(m);
-      uint32_t inc = c;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += u;
-      }
-      if (lane == 31) wsum[warp] = inc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t t = s_run;
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t x = wsum[j];
-          wsum[j] = t;
-          t += x;
-        }
-        s_run = t;
-      }
-      __syncthreads();
-      uint32_t o = wsum[warp] + inc - c;
-      __syncthreads();  // wsum reused by the next sub-tile
-      if (!m) continue;
-      dirty[w] = 0u;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1u;
-        const uint32_t slot = (uint32_t)(w * 32 + b);
-        dkey[o] = slot;
-        if (semi == S_MAXMIN) {  // settle: each slot appears once here, no atomic needed
-          uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
-          const uint32_t v = __ldcg(a);
-          __stcg(a, v | 1u);
-          dp[o] = u2f((v >> 1) - 1u);
-        } else if (semi == S_MAXMULT) {
-          unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
-          const unsigned long long v = __ldcg(a);
-          __stcg(a, v | (1ull << 32));
-          dp[o] = u2f((uint32_t)(v >> 33) - 1u);
-          dw[o] = ~(uint32_t)v;
-        }
-        ++o;
-      }
-    }
-  }
-}
-
-// Warp-granular variant (no block barriers): chunk = 32 words, one per lane.
-__global__ void __launch_bounds__(256) dirty_chunk_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
-                                                           uint32_t* __restrict__ ccnt) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nchunks = (nw + 31) / 32;
-  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks;
-       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t w = c * 32 + lane;
-    const uint32_t n = __reduce_add_sync(0xffffffffu, w < nw ? (uint32_t)__popc(dirty[w]) : 0u);
-    if (lane == 0) ccnt[c] = n;
-  }
-}
-
-__global__ void __launch_bounds__(256) direct_extract_warp_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
-                                                             const uint32_t* __restrict__ cbase, int64_t nw, int semi,
-                                                             uint32_t* __restrict__ dkey, float* __restrict__ dp,
-                                                             uint32_t* __restrict__ dw) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nchunks = (nw + 31) / 32;
-  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks;
-       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t w = c * 32 + lane;
-    uint32_t m = w < nw ? dirty[w] : 0u;
-    const uint32_t cnt = __popc(m);
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += u;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    if (!total) continue;
-    if (m) dirty[w] = 0u;
-    const uint32_t base = cbase[c];
-    // the chunk's set bits are spread evenly over the lanes: lane handles bit
-    // k = lane, lane+32, ...; its word = first lane whose inclusive count > k
-    for (uint32_t kb = 0; kb < total; kb += 32) {  // warp-uniform trip count (shuffles below)
-      const uint32_t k = kb + lane;
-      const bool act = k < total;
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {  // branch-free search over the 32 inclusive counts
-        const uint32_t v = __shfl_sync(0xffffffffu, inc, lo + step - 1);
-        if (v <= k) lo += step;
-      }
-      const uint32_t wm = __shfl_sync(0xffffffffu, m, lo);
-      const uint32_t wex = __shfl_sync(0xffffffffu, inc - cnt, lo);
-      if (!act) continue;
-      const uint32_t bit = __fns(wm, 0, (int)(k - wex) + 1);
-      const uint32_t slot = (uint32_t)((c * 32 + lo) * 32 + bit);
-      const uint32_t o = base + k;
-      dkey[o] = slot;
-      if (semi == S_MAXMIN) {  // settle: each slot appears once here, no atomic needed
-        uint32_t* a = reinterpret_cast<uint32_t*>(f) + slot;
-        const uint32_t v = __ldcg(a);
-        __stcg(a, v | 1u);
-        dp[o] = u2f((v >> 1) - 1u);
-      } else if (semi == S_MAXMULT) {
-        unsigned long long* a = reinterpret_cast<unsigned long long*>(f) + slot;
-        const unsigned long long v = __ldcg(a);
-        __stcg(a, v | (1ull << 32));
-        dp[o] = u2f((uint32_t)(v >> 33) - 1u);
-        dw[o] = ~(uint32_t)v;
-      }
-    }
   }
 }
 
@@ -765,9 +591,8 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
         for (int u = 0; u < LB_U; ++u) {
           if (!act[u]) continue;
           const uint32_t o = base + kb + u * 32 + lane;
-          __stcg(reinterpret_cast<uint32_t*>(f) + slotv[u], v[u] | 1u);  // settle (each slot once: no atomic)
-          dkey[o] = slotv[u];
-          dp[o] = u2f((v[u] >> 1) - 1u);
+          dkey[o] = slotv[u];  // no settle: max-min words carry no tie state
+          dp[o] = mm_p(v[u]);
         }
       } else if (SEMI == S_MAXMULT) {
         unsigned long long v[LB_U];
@@ -793,32 +618,6 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   }
 }
 
-// popcount of each 1024-word tile of the dirty bitmap
-__global__ void __launch_bounds__(256) dirty_tile_count_k(const uint32_t* __restrict__ dirty, int64_t nw,
-                                                          uint32_t* __restrict__ tcnt) {
-  const int64_t ntiles = (nw + 1023) / 1024;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t w0 = t * 1024 + threadIdx.x * 4;
-    uint32_t c = 0;
-    if (w0 + 3 < nw) {
-      const uint4 m = *reinterpret_cast<const uint4*>(dirty + w0);
-      c = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
-    } else {
-      for (int k = 0; k < 4; ++k)
-        if (w0 + k < nw) c += __popc(dirty[w0 + k]);
-    }
-    c = __reduce_add_sync(0xffffffffu, c);
-    __shared__ uint32_t ws[8];
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t s = 0;
-      for (int k = 0; k < 8; ++k) s += ws[k];
-      tcnt[t] = s;
-    }
-    __syncthreads();
-  }
-}
 
 __global__ void direct_present_k(const void* __restrict__ f, int64_t n, int semi, uint32_t* __restrict__ flag) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1003,13 +802,6 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st) {
                                       : (size_t)nslots * (semi == S_MAXMULT ? 8 : 4);
   cudaMemsetAsync(f, 0, bytes, st);
 }
-void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
-                            uint32_t* dw, unsigned long long* counter, const uint32_t* tile_base, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  direct_extract1_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(f, dirty, nwords, semi, dkey, dp, dw,
-                                                                                 counter, tile_base);
-}
 int64_t direct_extract2_scratch(int64_t nwords) {
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   return nt + (nt + LB_GROUP - 1) / LB_GROUP;
@@ -1029,34 +821,6 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
     case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
     default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
   }
-}
-void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  dirty_chunk_count_k<<<grid_for((nwords + 31) / 32 * 32, 256), 256, 0, st>>>(dirty, nwords, ccnt);
-}
-void launch_direct_extract_warp(void* f, uint32_t* dirty, const uint32_t* cbase, int64_t nwords, int semi,
-                                uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  direct_extract_warp_k<<<grid_for((nwords + 31) / 32 * 32, 256), 256, 0, st>>>(f, dirty, cbase, nwords, semi, dkey,
-                                                                               dp, dw);
-}
-void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  dirty_tile_count_k<<<grid_for((nwords + 1023) / 1024, 1, 148 * 8), 256, 0, st>>>(dirty, nwords, tcnt);
-}
-void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  direct_dirty_count_k<<<grid_for(nwords, 256), 256, 0, st>>>(dirty, nwords, cnt);
-}
-void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
-                                 uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st) {
-  if (nwords <= 0) return;
-  note_launch();
-  direct_dirty_extract_k<<<grid_for(nwords, 256), 256, 0, st>>>(f, dirty, pos, nwords, semi, dkey, dp, dw);
 }
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
   if (nslots <= 0) return;

@@ -94,13 +94,18 @@ struct JoinPlan {
 };
 
 // Direct ⊕ (idempotent semirings on a direct-mapped store): F[slot] holds
-//   max-min : (pbits + 1) << 1 | settled
+//   unit    : one bit per slot
+//   max-min : pbits + 1                       (0 = absent)
 //   max-mult: (pbits + 1) << 33 | settled << 32 | ~w
 // so one atomicMax per candidate computes "larger p wins; on equal p the
-// existing (settled) tag wins, then the smaller witness" (readings 8a, 8b).
-// The unique thread whose atomic lifts a settled or absent slot sets the
-// slot's bit in the round's dirty bitmap; the epilogue compacts the bitmap in
-// slot order into Δ' (sorted, deterministic) and re-settles those slots.
+// existing (settled) tag wins, then the smaller witness" (readings 8a, 8b);
+// max-min has no witness, so an equal p is simply no change.  A candidate is
+// applied only if it beats a plain (stale) read of the slot, which is a lower
+// bound of the slot at round start; such a candidate makes the slot end the
+// round above its round-start value, so it sets the slot's bit in the round's
+// dirty bitmap (idempotent OR, fire-and-forget).  The epilogue compacts the
+// bitmap in slot order into Δ' (sorted, deterministic) and, under max-mult,
+// re-settles those slots.
 
 // Single-atom rule (projection): rows of one relation -> candidates.
 struct ProjectPlan {
@@ -255,28 +260,13 @@ void launch_dense_present(const float* fp, const uint32_t* fbits, int64_t nslots
                           cudaStream_t st);
 void launch_dense_compact(const float* fp, const uint32_t* fw, const uint32_t* fbits, const uint32_t* pos,
                           int64_t nslots, int semi, uint64_t* key, float* p, uint32_t* w, cudaStream_t st);
-// direct ⊕ store: zero-fill, list -> Δ' (+ re-settle), present flags, compaction
+// direct ⊕ store: zero-fill, present flags, compaction
 void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
-// single-pass dirty bitmap -> Δ' (tile-sorted); *counter += |Δ'|; dkey/dp/dw
-// must hold every slot that can be dirty this round
-// tile_base (scanned per-1024-word popcounts, see launch_dirty_tile_count) gives
-// slot-sorted Δ'; null = bases from an atomic counter (tiles unordered)
-void launch_direct_extract1(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
-                            uint32_t* dw, unsigned long long* counter, const uint32_t* tile_base, cudaStream_t st);
-void launch_dirty_tile_count(const uint32_t* dirty, int64_t nwords, uint32_t* tcnt, cudaStream_t st);
-// warp-granular: per-32-word chunk popcounts (scan them) -> Δ' in slot order, no block barriers
-void launch_dirty_chunk_count(const uint32_t* dirty, int64_t nwords, uint32_t* ccnt, cudaStream_t st);
-void launch_direct_extract_warp(void* f, uint32_t* dirty, const uint32_t* cbase, int64_t nwords, int semi,
-                                uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
 // two launches (tile / group counts, then bases + rows): dirty bitmap -> Δ' in slot order,
-// dirty bits cleared, slots re-settled; |Δ'| -> *total (device).  scratch: direct_extract2_scratch u32
+// dirty bits cleared, max-mult slots re-settled; |Δ'| -> *total (device).  scratch: direct_extract2_scratch u32
 int64_t direct_extract2_scratch(int64_t nwords);
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, uint32_t* scratch, uint32_t* total, cudaStream_t st);
-// dirty bitmap -> per-word popcounts (scan them), then Δ' in slot order
-void launch_direct_dirty_count(const uint32_t* dirty, int64_t nwords, uint32_t* cnt, cudaStream_t st);
-void launch_direct_dirty_extract(void* f, uint32_t* dirty, const uint32_t* pos, int64_t nwords, int semi,
-                                 uint32_t* dkey, float* dp, uint32_t* dw, cudaStream_t st);
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st);
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
                            uint32_t* w, cudaStream_t st);
