@@ -76,6 +76,12 @@ __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 __device__ __forceinline__ uint32_t mm_word(float p) { return f2u(p) + 1u; }
 __device__ __forceinline__ float mm_p(uint32_t v) { return u2f(v - 1u); }
 
+// max-mult direct-store word (kernels.cuh MxEnc)
+__device__ __forceinline__ unsigned long long mx_word(float p, uint32_t w, const MxEnc& e) {
+  return ((unsigned long long)(f2u(p) + 1u) << 34) | e.stamp | ((unsigned long long)(~w) & e.wmask);
+}
+__device__ __forceinline__ float mx_p(unsigned long long v) { return u2f((uint32_t)(v >> 34) - 1u); }
+
 // ⊗: one IEEE fp32 op, no contraction (reading 9)
 __device__ __forceinline__ float otimes(int semi, float a, float b) {
   if (semi == S_MAXMIN) return a < b ? a : b;
@@ -88,7 +94,7 @@ __device__ __forceinline__ float otimes(int semi, float a, float b) {
 // to each of 64 slots) lanes of a warp aiming at the same slot are pre-reduced
 // (match + shuffle tree) so one atomic per (warp, slot) reaches L2.
 __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, float p, uint32_t w, uint32_t* dirty,
-                                             int aggregate) {
+                                             int aggregate, const MxEnc& mx) {
   namespace cg = cooperative_groups;
   bool app = false;
   if (semi == S_UNIT) {
@@ -108,7 +114,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
       app = old < v;  // any improvement marks the slot (idempotent OR)
     }
   } else {
-    unsigned long long v = ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
+    unsigned long long v = mx_word(p, w, mx);
     bool lead = true;
     if (aggregate) {
       cg::coalesced_group part = cg::labeled_partition(cg::coalesced_threads(), (int)slot);
@@ -117,7 +123,7 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
     }
     if (lead) {
       const unsigned long long old = atomicMax(reinterpret_cast<unsigned long long*>(f) + slot, v);
-      app = old < v && (old == 0ull || ((old >> 32) & 1ull));
+      app = old < v;
     }
   }
   if (app) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
@@ -129,10 +135,11 @@ __device__ __forceinline__ void direct_oplus(int semi, void* f, uint32_t slot, f
 // the store only grows (atomicMax / OR), so a stale read is a lower bound and
 // a candidate not above it can never improve the slot.  direct_commit issues
 // the remaining updates and dirty bits as fire-and-forget reductions.
-__device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slot, float t, uint32_t w) {
+__device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slot, float t, uint32_t w,
+                                                          const MxEnc& mx) {
   if (semi == S_UNIT) return 1ull << (slot & 31u);
   if (semi == S_MAXMIN) return (unsigned long long)mm_word(t);
-  return ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
+  return mx_word(t, w, mx);
 }
 
 __device__ __forceinline__ unsigned long long direct_peek(int semi, const void* f, uint32_t slot) {

@@ -107,6 +107,11 @@ struct RelState {
   DBuf<unsigned long long> dctr;  // |Δ'| counter of the single-pass extraction
   DBuf<uint32_t> ndev;             // |Δ'| of the last extraction (device)
   bool async = false;              // rounds run without a host sync: Δ size lives in ndev
+  // max-mult direct words (kernels.cuh MxEnc): witness field WB = wrb + wT bits,
+  // round stamps in the SB = 34 - WB bits above it when they hold every round
+  int wT = 0, wrb = 0, wWB = 0;
+  bool stamp_mode = false;
+  unsigned long long smax = 0;
   int64_t cand_bound = 0;         // upper bound on slots dirtied this round
   DBuf<float> dfp;
   DBuf<uint32_t> dfw, dfbits, dkey32, ckey32, ckey32b;
@@ -823,7 +828,7 @@ struct Ctx {
             if (tag_atoms[q] == k) lp.tag_order[k] = (int8_t)q;
       }
       if (H.direct) {
-        direct_target(H, lp.direct, lp.fdir, lp.dirty, lp.aggregate);
+        direct_target(H, lp.direct, lp.fdir, lp.dirty, lp.aggregate, lp.mx);
       } else {
         reserve_candidates(H, H.nc + T.n);
         lp.ok32 = H.dense;
@@ -862,7 +867,7 @@ struct Ctx {
       pp.semi = semi;
       witness_moves(R, T, nullptr, pp.wm, pp.nwm, pp.wconst);
       if (H.direct) {
-        direct_target(H, pp.direct, pp.fdir, pp.dirty, pp.aggregate);
+        direct_target(H, pp.direct, pp.fdir, pp.dirty, pp.aggregate, pp.mx);
       } else {
         reserve_candidates(H, H.nc + T.n);
         pp.okey = cand_key(H);
@@ -972,7 +977,7 @@ struct Ctx {
           jp.tag_order[0] = (int8_t)(start < ai ? 0 : 1);
           jp.tag_order[1] = (int8_t)(start < ai ? 1 : 0);
         }
-        direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate);
+        direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate, jp.mx);
         if (rels[A0.rel]->async) jp.np_dev = rels[A0.rel]->ndev.ptr();
         merge_moves(jp.prem, jp.nprem);
         merge_moves(jp.om, jp.nom);
@@ -1022,7 +1027,7 @@ struct Ctx {
           }
         }
         if (H.direct) {
-          direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate);
+          direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate, jp.mx);
         } else {
           reserve_candidates(H, H.nc + total);
           jp.ok32 = H.dense;
@@ -1112,7 +1117,10 @@ struct Ctx {
     wconst = 0;
     if (semi != S_MAXMULT) return;
     const int rb = rule_bits[R.head_rel];
-    if (rb) wconst = (uint32_t)R.local_index << (32 - rb);
+    // direct max-mult heads store the compressed witness (rule index just above
+    // the variable fields, kernels.cuh MxEnc); other stores the 32-bit layout
+    const RelState& H = *rels[R.head_rel];
+    if (rb) wconst = (uint32_t)R.local_index << (H.direct ? H.wT : 32 - rb);
     const size_t ri = (size_t)R.global_index;
     for (size_t i = 0; i < R.nonhead.size(); ++i) {
       const int v = R.nonhead[i];
@@ -1224,7 +1232,7 @@ struct Ctx {
     if (semi == S_MAXMULT) S.w.reserve(n);
     if (S.direct)
       launch_direct_compact(S.dirf.get(), pos, ns, semi, S.key.ptr(), semi != S_UNIT ? S.p.ptr() : nullptr,
-                            semi == S_MAXMULT ? S.w.ptr() : nullptr, st);
+                            semi == S_MAXMULT ? S.w.ptr() : nullptr, mx_wmask(S), S.wT, S.wrb, st);
     else
       launch_dense_compact(S.dfp.ptr(), S.dfw.ptr(), S.dfbits.ptr(), pos, ns, semi, S.key.ptr(),
                            semi != S_UNIT ? S.p.ptr() : nullptr, semi == S_MAXMULT ? S.w.ptr() : nullptr, st);
@@ -1237,14 +1245,35 @@ struct Ctx {
   // B^new / B^old index is needed) and the slot array fits half of free HBM.
   // direct ⊕ target for `n` more candidates of head H this round: dlist must
   // hold every slot improved so far (<= candidates so far) plus n.
-  void direct_target(RelState& H, int& direct, void*& f, uint32_t*& dirty, int& aggregate) {
+  void direct_target(RelState& H, int& direct, void*& f, uint32_t*& dirty, int& aggregate, MxEnc& mx) {
     direct = 1;
     aggregate = (H.L.total - H.L.sbits) <= 8 ? 1 : 0;  // narrow head: many candidates per slot
     f = H.dirf.get();
     dirty = H.dirty.ptr();
+    mx.wmask = mx_wmask(H);
+    mx.stamp = H.stamp_mode ? (H.smax - (unsigned long long)cur_round) << H.wWB : 0ull;
   }
 
-  void choose_store(RelState& S) {
+  static unsigned long long mx_wmask(const RelState& S) { return S.wWB >= 64 ? ~0ull : (1ull << S.wWB) - 1ull; }
+
+  // max-mult direct word layout of head relation r: widest variable field of its
+  // rules (wT), rule-index bits (wrb); stamps when 2^(34 - WB) - 1 exceeds max_iters
+  void mx_layout(int r, RelState& S) {
+    S.wT = 0;
+    for (const Rule& R : prog.rules) {
+      if (R.head_rel != r) continue;
+      int tot = 0;
+      for (int b : wbits[(size_t)R.global_index]) tot += b;
+      S.wT = std::max(S.wT, tot);
+    }
+    S.wrb = rule_bits[r];
+    S.wWB = S.wT + S.wrb;
+    const int sb = 34 - S.wWB;
+    S.smax = (1ull << sb) - 1ull;
+    S.stamp_mode = !getenv("LOBSTER_NO_STAMPS") && S.smax > (unsigned long long)max_iters + 1;
+  }
+
+  void choose_store(RelState& S, int r) {
     S.dense = false;
     S.direct = false;
     if (S.build_local || S.L.total > 30 || force_sorted) return;
@@ -1259,6 +1288,7 @@ struct Ctx {
       }
       S.dense = S.direct = true;
       S.nslots = ns;
+      if (semi == S_MAXMULT) mx_layout(r, S);
       S.dirf.reserve(bytes);
       launch_direct_fill(S.dirf.get(), ns, semi, st);
       S.dirty.reserve((ns + 31) / 32);
@@ -1305,7 +1335,8 @@ struct Ctx {
       Phase ph(this, 3);
       launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
                              semi != S_UNIT ? S.dp.ptr() : nullptr, nullptr,
-                             arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(), st);
+                             arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(),
+                             semi == S_MAXMULT && !S.stamp_mode ? S.smax << S.wWB : 0ull, mx_wmask(S), st);
       kcheck("direct extract");
     }
     if (S.async) {  // |Δ'| stays on the device: the next join reads it, the host polls it later
@@ -1598,6 +1629,7 @@ struct Ctx {
   uint32_t* hring = nullptr;
   cudaEvent_t ring_ev[ARING] = {};
   int round_fused = 0, round_other = 0;
+  int cur_round = 0;      // round of the stratum being issued (max-mult stamps)
   int64_t async_nd0 = 0;  // Δ rows probed by the first async round
   int async_nrel = 0;     // relations of the async stratum (ring entries per round)
 
@@ -1665,7 +1697,7 @@ struct Ctx {
         if (semi != S_UNIT) S.p.reserve(1);
         if (semi == S_MAXMULT) S.w.reserve(1);
         HostTimer hts(host_ms[4]);
-        choose_store(S);
+        choose_store(S, r);
       }
       int rounds = 0;
       bool first = true, first_round = true, async = false;
@@ -1680,6 +1712,7 @@ struct Ctx {
           break;
         }
         rounds++;
+        cur_round = rounds;
         arena.reset();
         const int64_t probe0 = stats.fj_probe_rows;
         if (log_level >= 2) trace.push_back({(int64_t)ev.size(), 0, 0, (int64_t)si});

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
         live[k] = rowv[k] >= 0 && okv[k];
         if (!live[k]) continue;
         slotv[k] = (uint32_t)keyv[k];
-        newv[k] = direct_pack(semi, slotv[k], tv[k], wv[k]);
+        newv[k] = direct_pack(semi, slotv[k], tv[k], wv[k], jp.mx);
         oldv[k] = direct_peek(semi, jp.fdir, slotv[k]);
       }
       direct_commit<SPT>(semi, jp.fdir, jp.dirty, slotv, newv, oldv, live);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
 #pragma unroll 1
       for (int k = 0; k < SPT; ++k)
         if (rowv[k] >= 0 && okv[k])
-          direct_oplus(semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate);
+          direct_oplus(semi, jp.fdir, (uint32_t)keyv[k], tv[k], wv[k], jp.dirty, jp.aggregate, jp.mx);
     }
   } else {
 #pragma unroll
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
       if (ok) {
         const float t = (pp.semi != S_UNIT && pp.tag) ? pp.tag[i] : 1.0f;
         const uint32_t w = pp.semi == S_MAXMULT ? (pp.wconst | (uint32_t)apply_moves(pp.wm, pp.nwm, k, 0)) : 0u;
-        direct_oplus(pp.semi, pp.fdir, (uint32_t)hk, t, w, pp.dirty, pp.aggregate);
+        direct_oplus(pp.semi, pp.fdir, (uint32_t)hk, t, w, pp.dirty, pp.aggregate, pp.mx);
       }
       continue;
     }
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
         oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
       } else {
         const uint32_t w = jp.wconst | (uint32_t)moves_n<NM>(jp.wm, jp.nwm, pk, bk);
-        newv[d] = ((unsigned long long)(f2u(t) + 1u) << 33) | (unsigned long long)(~w);
+        newv[d] = mx_word(t, w, jp.mx);
         oldv[d] = __ldcg(reinterpret_cast<const unsigned long long*>(jp.fdir) + slot);
       }
     }
@@ -455,9 +455,9 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
 }
 
 template <int SEMI>
-__device__ __forceinline__ unsigned long long agg_pack(float p, uint32_t w) {
+__device__ __forceinline__ unsigned long long agg_pack(float p, uint32_t w, const MxEnc& mx) {
   if (SEMI == S_MAXMIN) return (unsigned long long)mm_word(p);
-  if (SEMI == S_MAXMULT) return ((unsigned long long)(f2u(p) + 1u) << 33) | (unsigned long long)(~w);
+  if (SEMI == S_MAXMULT) return mx_word(p, w, mx);
   return 1ull;
 }
 
@@ -478,7 +478,7 @@ __device__ __forceinline__ void agg_flush(void* f, uint32_t* dirty, uint32_t slo
     }
     if ((threadIdx.x & 31) == 0 && v) {
       const unsigned long long old = atomicMax(reinterpret_cast<unsigned long long*>(f) + slot, v);
-      if (old < v && (old == 0ull || ((old >> 32) & 1ull))) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
+      if (old < v) atomicOr(dirty + (slot >> 5), 1u << (slot & 31u));
     }
   } else {
     if (__any_sync(0xffffffffu, v != 0ull) && (threadIdx.x & 31) == 0) {
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       const uint32_t s0 = __shfl_sync(0xffffffffu, slot, __ffs(act) - 1);
       const bool uniform = __all_sync(0xffffffffu, !ok || slot == s0);
       if (uniform && s0 == cur) {
-        const unsigned long long v = ok ? agg_pack<SEMI_C>(t, w) : 0ull;
+        const unsigned long long v = ok ? agg_pack<SEMI_C>(t, w, lp.mx) : 0ull;
         run = v > run ? v : run;
         continue;
       }
@@ -532,9 +532,9 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       cur = 0xffffffffu;
       if (uniform) {
         cur = s0;
-        run = ok ? agg_pack<SEMI_C>(t, w) : 0ull;
+        run = ok ? agg_pack<SEMI_C>(t, w, lp.mx) : 0ull;
       } else if (ok) {
-        direct_oplus(SEMI_C, lp.fdir, slot, t, w, lp.dirty, 1);
+        direct_oplus(SEMI_C, lp.fdir, slot, t, w, lp.dirty, 1, lp.mx);
       }
     }
     if (cur != 0xffffffffu) agg_flush<SEMI_C>(lp.fdir, lp.dirty, cur, run);
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       const bool ok = lookup_row<PK>(lp, semi, pkey[i], i, t, w, key);
       if (ok) ++mycount;
       if constexpr (DIRECT) {
-        if (ok) direct_oplus(SEMI_C, lp.fdir, (uint32_t)key, t, w, lp.dirty, 0);
+        if (ok) direct_oplus(SEMI_C, lp.fdir, (uint32_t)key, t, w, lp.dirty, 0, lp.mx);
       } else {
         okey[i] = ok ? (OK)key : dead<OK>();
         if (semi == S_MAXMULT) lp.oval64[i] = (uint64_t)f2u(t) | ((uint64_t)w << 32);

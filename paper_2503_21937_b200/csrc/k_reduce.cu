@@ -431,8 +431,10 @@ __global__ void dense_compact_k(const float* __restrict__ fp, const uint32_t* __
 }
 
 // ------------------------------------------------------ direct ⊕ store ----
+// wmask / wT / wrb: max-mult witness field and its decompression (kernels.cuh MxEnc):
+// wc = rule << wT | vars  ->  w = rule << (32 - wrb) | vars
 __device__ __forceinline__ void direct_decode(const void* f, int semi, int64_t slot, bool& present, float& p,
-                                              uint32_t& w) {
+                                              uint32_t& w, unsigned long long wmask = 0, int wT = 0, int wrb = 0) {
   present = false;
   p = 0.0f;
   w = 0;
@@ -445,8 +447,10 @@ __device__ __forceinline__ void direct_decode(const void* f, int semi, int64_t s
   } else {
     const unsigned long long v = reinterpret_cast<const unsigned long long*>(f)[slot];
     present = v != 0ull;
-    p = u2f((uint32_t)(v >> 33) - 1u);
-    w = ~(uint32_t)v;
+    p = mx_p(v);
+    const unsigned long long wc = ~v & wmask;
+    const unsigned long long vars = wc & ((1ull << wT) - 1ull);
+    w = (uint32_t)(wrb ? (((wc >> wT) << (32 - wrb)) | vars) : vars);
   }
 }
 
@@ -502,7 +506,8 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
                                                          float* __restrict__ dp, uint32_t* __restrict__ dw,
                                                          const uint32_t* __restrict__ tcnt,
                                                          const uint32_t* __restrict__ gsum,
-                                                         uint32_t* __restrict__ total) {
+                                                         uint32_t* __restrict__ total, unsigned long long restamp,
+                                                         unsigned long long wmask) {
   __shared__ uint32_t wtot[8];
   __shared__ uint32_t wpre[8];
   __shared__ uint32_t s_base;
@@ -603,10 +608,10 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
         for (int u = 0; u < LB_U; ++u) {
           if (!act[u]) continue;
           const uint32_t o = base + kb + u * 32 + lane;
-          __stcg(reinterpret_cast<unsigned long long*>(f) + slotv[u], v[u] | (1ull << 32));
+          if (restamp) __stcg(reinterpret_cast<unsigned long long*>(f) + slotv[u], v[u] | restamp);
           dkey[o] = slotv[u];
-          dp[o] = u2f((uint32_t)(v[u] >> 33) - 1u);
-          if (dw) dw[o] = ~(uint32_t)v[u];
+          dp[o] = mx_p(v[u]);
+          if (dw) dw[o] = (uint32_t)(~v[u] & wmask);
         }
       } else {
 #pragma unroll
@@ -630,12 +635,13 @@ __global__ void direct_present_k(const void* __restrict__ f, int64_t n, int semi
 }
 
 __global__ void direct_compact_k(const void* __restrict__ f, const uint32_t* __restrict__ pos, int64_t n, int semi,
-                                 uint64_t* __restrict__ key, float* __restrict__ p, uint32_t* __restrict__ w) {
+                                 uint64_t* __restrict__ key, float* __restrict__ p, uint32_t* __restrict__ w,
+                                 unsigned long long wmask, int wT, int wrb) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     bool pr;
     float pp;
     uint32_t ww;
-    direct_decode(f, semi, i, pr, pp, ww);
+    direct_decode(f, semi, i, pr, pp, ww, wmask, wT, wrb);
     if (!pr) continue;
     const uint32_t o = pos[i];
     key[o] = (uint64_t)i;
@@ -807,7 +813,8 @@ int64_t direct_extract2_scratch(int64_t nwords) {
   return nt + (nt + LB_GROUP - 1) / LB_GROUP;
 }
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
-                            uint32_t* dw, uint32_t* scratch, uint32_t* total, cudaStream_t st) {
+                            uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
+                            unsigned long long wmask, cudaStream_t st) {
   if (nwords <= 0) return;
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   const int64_t ng = (nt + LB_GROUP - 1) / LB_GROUP;
@@ -817,9 +824,9 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
   note_launch();
   switch (semi) {
-    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
-    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
-    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total); break;
+    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
+    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
+    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
   }
 }
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
@@ -828,10 +835,10 @@ void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* fl
   direct_present_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, nslots, semi, flag);
 }
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
-                           uint32_t* w, cudaStream_t st) {
+                           uint32_t* w, unsigned long long wmask, int wT, int wrb, cudaStream_t st) {
   if (nslots <= 0) return;
   note_launch();
-  direct_compact_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, pos, nslots, semi, key, p, w);
+  direct_compact_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, pos, nslots, semi, key, p, w, wmask, wT, wrb);
 }
 void launch_dense_present(const float* fp, const uint32_t* fbits, int64_t nslots, int semi, uint32_t* flag,
                           cudaStream_t st) {

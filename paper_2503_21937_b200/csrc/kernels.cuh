@@ -19,6 +19,18 @@ constexpr int MAXC = 4;    // max comparisons applied in one join step
 
 enum Semi : int { S_UNIT = 0, S_MAXMIN = 1, S_ADDMULT = 2, S_MAXMULT = 3 };
 
+// max-mult direct-store word: (pbits + 1) << 34 | stamp << WB | ~wc (WB bits).
+// wc is the witness in compressed layout (rule index << T | variables, T = the
+// widest variable field of the relation's rules; order-preserving), WB = rule
+// bits + T.  stamp = SMAX - round (SB = 34 - WB bits): on equal p an older
+// round's value wins (reading 8a) without rewriting slots; when SB cannot hold
+// every round, candidates take stamp 0 and Δ' extraction re-stamps SMAX
+// (a "settled" bit).  MxEnc: the per-launch constants.
+struct MxEnc {
+  unsigned long long stamp;  // stamp << WB for this round's candidates
+  unsigned long long wmask;  // (1 << WB) - 1
+};
+
 // counts every kernel launch of this library (lobster_kernel_launches)
 void note_launch();
 
@@ -90,22 +102,23 @@ struct JoinPlan {
   void* fdir;               // u32 bitmap (unit) / u32 packed (max-min) / u64 packed (max-mult)
   uint32_t* dirty;          // bitmap: slots improved this round
   int aggregate;            // warp pre-reduction of equal slots (narrow heads)
+  MxEnc mx;                 // max-mult word constants
 
 };
 
 // Direct ⊕ (idempotent semirings on a direct-mapped store): F[slot] holds
 //   unit    : one bit per slot
 //   max-min : pbits + 1                       (0 = absent)
-//   max-mult: (pbits + 1) << 33 | settled << 32 | ~w
+//   max-mult: (pbits + 1) << 34 | stamp << WB | ~wc   (MxEnc)
 // so one atomicMax per candidate computes "larger p wins; on equal p the
-// existing (settled) tag wins, then the smaller witness" (readings 8a, 8b);
+// older round's tag wins, then the smaller witness" (readings 8a, 8b);
 // max-min has no witness, so an equal p is simply no change.  A candidate is
 // applied only if it beats a plain (stale) read of the slot, which is a lower
 // bound of the slot at round start; such a candidate makes the slot end the
 // round above its round-start value, so it sets the slot's bit in the round's
 // dirty bitmap (idempotent OR, fire-and-forget).  The epilogue compacts the
-// bitmap in slot order into Δ' (sorted, deterministic) and, under max-mult,
-// re-settles those slots.
+// bitmap in slot order into Δ' (sorted, deterministic) and, under max-mult
+// without round stamps, re-stamps those slots.
 
 // Single-atom rule (projection): rows of one relation -> candidates.
 struct ProjectPlan {
@@ -129,6 +142,7 @@ struct ProjectPlan {
   void* fdir;
   uint32_t* dirty;
   int aggregate;
+  MxEnc mx;
 };
 
 // Lookup chain: probe rows whose variables cover the whole rule; every other
@@ -172,6 +186,7 @@ struct LookupPlan {
   void* fdir;
   uint32_t* dirty;
   int aggregate;
+  MxEnc mx;
 };
 void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaStream_t st);
 
@@ -265,11 +280,14 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
 // two launches (tile / group counts, then bases + rows): dirty bitmap -> Δ' in slot order,
 // dirty bits cleared, max-mult slots re-settled; |Δ'| -> *total (device).  scratch: direct_extract2_scratch u32
 int64_t direct_extract2_scratch(int64_t nwords);
+// restamp (max-mult): OR-ed into every Δ' slot word (0 = none)
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
-                            uint32_t* dw, uint32_t* scratch, uint32_t* total, cudaStream_t st);
+                            uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
+                            unsigned long long wmask, cudaStream_t st);
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st);
+// wT / wrb: witness decompression (variable field width, rule-index bits)
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
-                           uint32_t* w, cudaStream_t st);
+                           uint32_t* w, unsigned long long wmask, int wT, int wrb, cudaStream_t st);
 // classify U against F: flags (u64: lo = in Δ', hi = new); pos (F index or -1)
 void launch_diff(const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu,
                  const uint64_t* fkey, const float* fp, int64_t nf, int semi, uint64_t* flags, int64_t* pos,
