@@ -173,6 +173,8 @@ struct Index {
   DBuf<float> own_p, tmp_p;
   DBuf<int64_t> off;
   const int64_t* offp = nullptr;
+  DBuf<uint4> rec;                 // fan-out <= 4: per-prefix 32-B records (kernels.cuh JoinPlan::brec)
+  const uint4* recp = nullptr;
   int64_t nprefix = 0;
   int free_bits = 0, prefix_bits = 0;
   int64_t maxdeg = -1;  // max rows per prefix (static CSR indexes), -1 unknown
@@ -634,6 +636,7 @@ struct Ctx {
       int64_t* off;
       if (persistent) {
         ix.off.bind(st);
+        ix.rec.bind(st);
         ix.off.reserve(ix.nprefix + 1);
         off = ix.off.ptr();
       } else {
@@ -647,6 +650,15 @@ struct Ctx {
         cuda_check(cudaMemsetAsync(d, 0, 8, st), "memset");
         launch_max_degree(off, ix.nprefix, d, st);
         ix.maxdeg = (int64_t)read_dev(d);
+        // fan-out <= 4 with index keys < 2^31: one 32-B record per prefix (keys + tags in one
+        // sector) replaces the offsets -> keys -> tags loads of the fused join
+        ix.recp = nullptr;
+        if (ix.maxdeg <= 4 && ix.prefix_bits + ix.free_bits <= 31 && !getenv("LOBSTER_NO_REC")) {
+          ix.rec.reserve(2 * ix.nprefix);
+          launch_build_rec4(off, ix.key, ix.p, ix.nprefix, ix.rec.ptr(), st);
+          kcheck("rec4");
+          ix.recp = ix.rec.ptr();
+        }
       }
     }
   }
@@ -979,6 +991,7 @@ struct Ctx {
         }
         direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate, jp.mx);
         if (rels[A0.rel]->async) jp.np_dev = rels[A0.rel]->ndev.ptr();
+        if (ix->maxdeg <= 4 && jp.pk32) jp.brec = ix->recp;
         merge_moves(jp.prem, jp.nprem);
         merge_moves(jp.om, jp.nom);
         merge_moves(jp.wm, jp.nwm);

@@ -310,7 +310,7 @@ __device__ __forceinline__ uint64_t moves_n(const Move* mv, int n, uint64_t a, u
   return o;
 }
 
-template <typename PK, int MAXDEG, int SEMI, int NM>
+template <typename PK, int MAXDEG, int SEMI, int NM, bool REC>
 __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_direct_k(const JoinPlan jp,
                                                           unsigned long long* __restrict__ ncand) {
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
@@ -328,8 +328,23 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
     const uint64_t pk = (uint64_t)pkr;
     const uint64_t pre = jp.cprefix | moves_n<NM>(jp.prem, jp.nprem, pk, 0);
     if (pre >= (uint64_t)jp.nprefix) continue;
-    const int64_t lo = jp.boff[pre];
-    const int n = (int)(jp.boff[pre + 1] - lo);
+    // build rows of the prefix: CSR range, or (REC) one 32-B record = one sector
+    int64_t lo = 0;
+    int n = 0;
+    uint32_t rk[REC ? 4 : 1];
+    float rt[REC ? 4 : 1];
+    if constexpr (REC) {
+      const uint4 kk = __ldg(jp.brec + 2 * pre);
+      rk[0] = kk.x; rk[1] = kk.y; rk[2] = kk.z; rk[3] = kk.w;
+      n = (kk.x != ~0u) + (kk.y != ~0u) + (kk.z != ~0u) + (kk.w != ~0u);
+      if (SEMI != S_UNIT) {
+        const uint4 tt = __ldg(jp.brec + 2 * pre + 1);
+        rt[0] = u2f(tt.x); rt[1] = u2f(tt.y); rt[2] = u2f(tt.z); rt[3] = u2f(tt.w);
+      }
+    } else {
+      lo = jp.boff[pre];
+      n = (int)(jp.boff[pre + 1] - lo);
+    }
     mycount += (uint32_t)n;
     const float pt = SEMI != S_UNIT ? jp.ptag[0][i] : 1.0f;
     unsigned long long oldv[MAXDEG], newv[MAXDEG];
@@ -343,7 +358,15 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
     for (int d = 0; d < MAXDEG; ++d) {
       live[d] = false;
       if (d >= n) continue;
-      const uint64_t bk = jp.bkey[lo + d];
+      uint64_t bk;
+      float bt = 1.0f;
+      if constexpr (REC) {
+        bk = rk[d];
+        if (SEMI != S_UNIT) bt = rt[d];
+      } else {
+        bk = jp.bkey[lo + d];
+        if (SEMI != S_UNIT) bt = jp.btag[lo + d];
+      }
       bool ok = true;
       for (int c = 0; c < ncmp; ++c) {
         const int64_t a = operand_value(jp.cmp[c].a, pk, bk);
@@ -359,7 +382,6 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
         oldv[d] = __ldcg(reinterpret_cast<const uint32_t*>(jp.fdir) + (slot >> 5));
         continue;
       }
-      const float bt = jp.btag[lo + d];
       const float t = jp.tag_order[0] == 0 ? otimes(SEMI, pt, bt) : otimes(SEMI, bt, pt);
       if (SEMI == S_MAXMIN) {
         newv[d] = mm_word(t);
@@ -621,8 +643,9 @@ void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* s
 
 template <typename PK, int SEMI, int NM>
 static void launch_rows_direct_t(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st, int g) {
-  if (maxdeg <= 4) join_rows_direct_k<PK, 4, SEMI, NM><<<g, 256, 0, st>>>(jp, ncand);
-  else join_rows_direct_k<PK, 8, SEMI, NM><<<g, 256, 0, st>>>(jp, ncand);
+  if (maxdeg <= 4 && jp.brec) join_rows_direct_k<PK, 4, SEMI, NM, true><<<g, 256, 0, st>>>(jp, ncand);
+  else if (maxdeg <= 4) join_rows_direct_k<PK, 4, SEMI, NM, false><<<g, 256, 0, st>>>(jp, ncand);
+  else join_rows_direct_k<PK, 8, SEMI, NM, false><<<g, 256, 0, st>>>(jp, ncand);
 }
 template <int SEMI>
 static void launch_rows_direct_s(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st, int g) {
@@ -663,6 +686,29 @@ void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaSt
   else if (lp.pk32) launch_lookup_chain_t<uint32_t, uint64_t>(lp, ncand, g, st);
   else if (lp.ok32) launch_lookup_chain_t<uint64_t, uint32_t>(lp, ncand, g, st);
   else launch_lookup_chain_t<uint64_t, uint64_t>(lp, ncand, g, st);
+}
+
+__global__ void build_rec4_k(const int64_t* __restrict__ off, const uint64_t* __restrict__ key,
+                             const float* __restrict__ tag, int64_t np, uint4* __restrict__ rec) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = off[p];
+    const int n = (int)(off[p + 1] - lo);
+    uint32_t k[4], t[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      k[d] = d < n ? (uint32_t)key[lo + d] : ~0u;
+      t[d] = d < n && tag ? __float_as_uint(tag[lo + d]) : 0u;
+    }
+    rec[2 * p] = make_uint4(k[0], k[1], k[2], k[3]);
+    rec[2 * p + 1] = make_uint4(t[0], t[1], t[2], t[3]);
+  }
+}
+
+void launch_build_rec4(const int64_t* off, const uint64_t* key, const float* tag, int64_t nprefix, uint4* rec,
+                       cudaStream_t st) {
+  if (nprefix <= 0) return;
+  note_launch();
+  build_rec4_k<<<grid_for(nprefix, 256), 256, 0, st>>>(off, key, tag, nprefix, rec);
 }
 
 __global__ void max_degree_k(const int64_t* __restrict__ off, int64_t np, unsigned long long* __restrict__ out) {

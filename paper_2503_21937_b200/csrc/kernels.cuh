@@ -72,6 +72,7 @@ struct JoinPlan {
   int64_t nb;
   const int64_t* boff;      // CSR offsets over the prefix domain, or null (binary search)
   int64_t nprefix;          // entries of boff minus one
+  const uint4* brec;        // nullable: per prefix one 32-B record {u32 key[4] (~0 = none), f32 tag[4]}
   int free_bits;            // bits below the prefix in the index key
   // repeated free variables: value at shift a must equal value at shift b (build key)
   int nfeq;
@@ -243,6 +244,9 @@ void launch_project(const ProjectPlan& pp, cudaStream_t st);
 // With jp.np_dev (Δ size on the device) the grid is persistent.
 void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st,
                              int64_t np_hint);
+// fan-out <= 4 and index keys < 2^31: per-prefix 32-B records (one sector: keys, tags)
+void launch_build_rec4(const int64_t* off, const uint64_t* key, const float* tag, int64_t nprefix, uint4* rec,
+                       cudaStream_t st);
 // max_p (off[p+1] - off[p]) -> atomicMax into *out
 void launch_max_degree(const int64_t* off, int64_t nprefix, unsigned long long* out, cudaStream_t st);
 
