@@ -222,6 +222,13 @@ struct Ctx {
   bool micro = false;     // the last run was split into sample chunks
   int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line, 2: + rounds
   std::vector<std::array<int64_t, 4>> trace;  // per round: first event index, fused probe rows, |Δ'|, stratum
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;  // LOBSTER_LOG>=1: GPU timeline sections of a run
+  void mark(const char* what) {
+    if (log_level < 1) return;
+    cudaEvent_t e = get_event();
+    cudaEventRecord(e, st);
+    marks.push_back({what, e});
+  }
   double host_ms[8] = {};
   struct HostTimer {  // accumulates host wall time of a scope (diagnostics)
     double& acc;
@@ -1485,8 +1492,10 @@ struct Ctx {
     cuda_check(cudaMemsetAsync(d_ncand, 0, 16, st), "memset");
     ev.clear();
     ev_used = 0;
+    marks.clear();
     cudaEvent_t t0 = get_event();
     cudaEventRecord(t0, st);
+    mark("start");
     for (auto& r : rels) {
       r->out_dev_ready = r->out_host_ready = false;
       r->has_grad = false;
@@ -1498,6 +1507,7 @@ struct Ctx {
       HostTimer ht(host_ms[0]);
       ingest_domains();
     }
+    mark("domains");
     // Micro-batching (SURVEY §5 memory planner): samples are independent
     // databases, so the fixpoint runs over sample ranges whose
     // packed keys fit the direct-mapped store; `output` relations are
@@ -1518,6 +1528,7 @@ struct Ctx {
         static_idx.clear();
         ingest_chunk(micro ? s0 : 0, micro ? s1 : B);
       }
+      mark("ingest");
       round_cap_hit = run_strata();
       for (size_t r = 0; r < prog.rels.size(); ++r)
         if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
@@ -1526,6 +1537,7 @@ struct Ctx {
         HostTimer htg(host_ms[5]);
         gradients();
       }
+      mark("gradients");
       if (micro) collect_outputs(s0);
     }
     batch_cur = B;
@@ -1712,6 +1724,7 @@ struct Ctx {
         HostTimer hts(host_ms[4]);
         choose_store(S, r);
       }
+      mark("store setup");
       int rounds = 0;
       bool first = true, first_round = true, async = false;
       int64_t done = 0;
@@ -1782,7 +1795,9 @@ struct Ctx {
         if (changed == 0) break;
         // every recursive rule took the fused direct join in this (non-seed) round: later
         // rounds need no host-side sizes, so they are issued without a sync (lagged stop test)
+        if (first_round) mark("seed round");
         if (!first_round && round_other == 0 && round_fused > 0 && strat.size() <= (size_t)AREL && async_ok(strat)) {
+          mark("sync rounds");
           async = true;
           async_nrel = (int)strat.size();
           for (int r : strat) rels[r]->async = true;
@@ -1790,6 +1805,7 @@ struct Ctx {
         }
         first_round = false;
       }
+      mark(async ? "async rounds" : "sync rounds");
       if (async) {
         sync();
         if (log_level >= 2 && trace.size() > trace_base + rounds) trace.resize(trace_base + rounds);
@@ -1802,6 +1818,7 @@ struct Ctx {
       HostTimer ht(host_ms[3]);
       for (int r : strat)
         if (rels[r]->dense) dense_to_sorted(*rels[r]);
+      mark("dense->sorted");
       stats.rounds_total += rounds;
       stats.strata++;
       if (round_cap_hit) break;
@@ -1830,6 +1847,17 @@ struct Ctx {
           break;
         default: stats.ms_grad += m; break;
       }
+    }
+    if (log_level >= 1 && marks.size() > 1) {  // GPU timeline sections (includes idle gaps)
+      std::string line = "[lobster] timeline ms:";
+      for (size_t q = 1; q < marks.size(); ++q) {
+        float m = 0;
+        cudaEventElapsedTime(&m, marks[q - 1].second, marks[q].second);
+        char b[96];
+        snprintf(b, sizeof b, " %s %.2f |", marks[q].first, m);
+        line += b;
+      }
+      fprintf(stderr, "%s\n", line.c_str());
     }
     if (log_level >= 2) {  // per-round trace: probe rows, |Δ'|, GPU ms of join / settle phases
       for (size_t t = 0; t < trace.size(); ++t) {
