@@ -13,6 +13,7 @@
 // Probe / output keys are u32 or u64 (template PK / OK): relations whose
 // packed key fits 31 bits move half the key bytes.
 #include <algorithm>
+#include <type_traits>
 
 #include "device_util.cuh"
 
@@ -310,8 +311,14 @@ __device__ __forceinline__ uint64_t moves_n(const Move* mv, int n, uint64_t a, u
   return o;
 }
 
+// resident CTAs per SM: 6 (40 registers) except max-mult, whose 64-bit words
+// need 48 registers to stay out of local memory (5)
+#ifndef FJ_MINB_MX
+#define FJ_MINB_MX 5
+#endif
 template <typename PK, int MAXDEG, int SEMI, int NM, bool REC>
-__global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_direct_k(const JoinPlan jp,
+__global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_MINB_MX : FJ_MINB) : 4)
+    join_rows_direct_k(const JoinPlan jp,
                                                           unsigned long long* __restrict__ ncand) {
   const PK* __restrict__ pkey = reinterpret_cast<const PK*>(jp.pkey);
   uint32_t mycount = 0;
@@ -347,7 +354,9 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
     }
     mycount += (uint32_t)n;
     const float pt = SEMI != S_UNIT ? jp.ptag[0][i] : 1.0f;
-    unsigned long long oldv[MAXDEG], newv[MAXDEG];
+    // word-sized values (u32 for unit / max-min): no wasted registers
+    using VW = typename std::conditional<SEMI == S_MAXMULT, unsigned long long, uint32_t>::type;
+    VW oldv[MAXDEG], newv[MAXDEG];
     uint32_t slotv[MAXDEG];
     bool live[MAXDEG];
     // phase A: candidate slot + packed value, and a plain (possibly stale) read
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
 #pragma unroll
     for (int d = 0; d < MAXDEG; ++d) {
       if (!live[d]) continue;
-      const unsigned long long v = newv[d];
+      const VW v = newv[d];
       if (SEMI == S_UNIT) {
         if (oldv[d] & v) continue;
         atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? FJ_MINB : 4) join_rows_di
         atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
       } else {
         if (v <= oldv[d]) continue;
-        atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], v);
+        atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], (unsigned long long)v);
       }
       atomicOr(jp.dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
     }
@@ -661,7 +670,8 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
   if (jp.np <= 0) return;
   // device-sized Δ: at most one wave of resident CTAs (grid-stride), at least 2 per SM
   int g = grid_for(np_hint, 256);
-  if (jp.np_dev) g = std::max(148 * 2, std::min(g, 148 * ((maxdeg <= 4) ? FJ_MINB : 4)));
+  if (jp.np_dev)
+    g = std::max(148 * 2, std::min(g, 148 * ((maxdeg <= 4) ? (jp.semi == S_MAXMULT ? FJ_MINB_MX : FJ_MINB) : 4)));
   note_launch();
   switch (jp.semi) {
     case S_UNIT: launch_rows_direct_s<S_UNIT>(jp, maxdeg, ncand, st, g); break;
