@@ -107,6 +107,8 @@ struct RelState {
   DBuf<unsigned long long> dctr;  // |Δ'| counter of the single-pass extraction
   DBuf<uint32_t> ndev;             // |Δ'| of the last extraction (device)
   bool async = false;              // rounds run without a host sync: Δ size lives in ndev
+  unsigned long long* ring_dst = nullptr;  // async: host-mapped word for (seq << 32 | |Δ'|)
+  uint32_t ring_seq = 0;
   // max-mult direct words (kernels.cuh MxEnc): witness field WB = wrb + wT bits,
   // round stamps in the SB = 34 - WB bits above it when they hold every round
   int wT = 0, wrb = 0, wWB = 0;
@@ -293,8 +295,6 @@ struct Ctx {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (hbuf) cudaFreeHost(hbuf);
     if (hring) cudaFreeHost(hring);
-    for (auto e : ring_ev)
-      if (e) cudaEventDestroy(e);
   }
 
   // --------------------------------------------------------------- create
@@ -1356,7 +1356,8 @@ struct Ctx {
       launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
                              semi != S_UNIT ? S.dp.ptr() : nullptr, nullptr,
                              arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(),
-                             semi == S_MAXMULT && !S.stamp_mode ? S.smax << S.wWB : 0ull, mx_wmask(S), st);
+                             semi == S_MAXMULT && !S.stamp_mode ? S.smax << S.wWB : 0ull, mx_wmask(S),
+                             S.async ? S.ring_dst : nullptr, S.ring_seq, st);
       kcheck("direct extract");
     }
     if (S.async) {  // |Δ'| stays on the device: the next join reads it, the host polls it later
@@ -1650,9 +1651,12 @@ struct Ctx {
 
   // one (micro-)batch: every stratum to fixpoint; returns 1 if max_iters was hit
   // Async rounds (direct strata): ring of pinned |Δ'| slots, one event per slot.
+  // The extraction kernel writes (seq << 32 | |Δ'|) straight into host-mapped pinned
+  // memory (zero-copy): no copy or event call per round, the host polls the words.
   static constexpr int ARING = 64, AREL = 8, ALAG = 6;
-  uint32_t* hring = nullptr;
-  cudaEvent_t ring_ev[ARING] = {};
+  unsigned long long* hring = nullptr;   // host view
+  unsigned long long* dring = nullptr;   // device view of the same words
+  uint32_t ring_seq = 0;                 // sequence of async rounds over the context's life
   int round_fused = 0, round_other = 0;
   int cur_round = 0;      // round of the stratum being issued (max-mult stamps)
   int64_t async_nd0 = 0;  // Δ rows probed by the first async round
@@ -1674,29 +1678,41 @@ struct Ctx {
       if ((double)need > 0.4 * (double)fr) return false;
     }
     if (!hring) {
-      cuda_check(cudaMallocHost(&hring, ARING * AREL * 4), "cudaMallocHost");
-      for (auto& e : ring_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      cuda_check(cudaHostAlloc(&hring, ARING * AREL * 8, cudaHostAllocMapped), "cudaHostAlloc");
+      std::memset(hring, 0, ARING * AREL * 8);
+      cuda_check(cudaHostGetDevicePointer((void**)&dring, hring, 0), "cudaHostGetDevicePointer");
     }
     return true;
   }
 
   // Consume finished rounds from the ring (all of them if `all`, else block only on
   // rounds more than ALAG behind).  Returns the first round whose Σ|Δ'| is 0, or 0.
-  int64_t drain_async(std::deque<int>& pending, size_t trace_base, bool all) {
-    const int newest = pending.empty() ? 0 : pending.back();
+  bool ring_ready(uint32_t seq) const {
+    const volatile unsigned long long* e = hring + (seq % ARING) * AREL;
+    for (int q = 0; q < async_nrel; ++q)
+      if ((uint32_t)(e[q] >> 32) != seq) return false;
+    return true;
+  }
+
+  int64_t drain_async(std::deque<std::pair<int, uint32_t>>& pending, size_t trace_base, bool all) {
+    const int newest = pending.empty() ? 0 : pending.back().first;
     while (!pending.empty()) {
-      const int pr = pending.front();
-      const int slot = pr % ARING;
+      const int pr = pending.front().first;
+      const uint32_t seq = pending.front().second;
       if (all || newest - pr >= ALAG) {
-        cuda_check(cudaEventSynchronize(ring_ev[slot]), "event sync");
-      } else {
-        const cudaError_t q = cudaEventQuery(ring_ev[slot]);
-        if (q == cudaErrorNotReady) break;
-        cuda_check(q, "event query");
+        for (uint64_t spin = 0; !ring_ready(seq); ++spin)
+          if ((spin & 1023) == 1023) {  // a failed kernel never writes its word
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaSuccess && !ring_ready(seq)) throw Failure(LOBSTER_E_CUDA, "async round count missing");
+            if (q != cudaSuccess && q != cudaErrorNotReady) cuda_check(q, "async round");
+          }
+      } else if (!ring_ready(seq)) {
+        break;
       }
       pending.pop_front();
       int64_t sum = 0;
-      for (int q = 0; q < async_nrel; ++q) sum += hring[slot * AREL + q];
+      const volatile unsigned long long* ent = hring + (seq % ARING) * AREL;
+      for (int q = 0; q < async_nrel; ++q) sum += (uint32_t)ent[q];
       const int64_t probe = async_nd0;
       async_nd0 = sum;  // Δ' of this round = probe rows of the next
       stats.fj_probe_rows += probe;
@@ -1728,7 +1744,7 @@ struct Ctx {
       int rounds = 0;
       bool first = true, first_round = true, async = false;
       int64_t done = 0;
-      std::deque<int> pending;
+      std::deque<std::pair<int, uint32_t>> pending;  // (round, ring sequence)
       const size_t trace_base = trace.size();
       async_nd0 = 0;
       for (;;) {
@@ -1779,15 +1795,17 @@ struct Ctx {
         int64_t changed = 0;
         {
           HostTimer ht(host_ms[2]);
+          if (async) {  // this round's |Δ'| words (zero-copy ring entry per relation)
+            ++ring_seq;
+            for (size_t q = 0; q < strat.size(); ++q) {
+              rels[strat[q]]->ring_dst = dring + (ring_seq % ARING) * AREL + q;
+              rels[strat[q]]->ring_seq = ring_seq;
+            }
+          }
           for (int r : strat) changed += settle(r);
         }
         if (async) {  // |Δ'| of this round -> pinned ring; poll earlier rounds without stalling the GPU
-          const int slot = rounds % ARING;
-          for (size_t q = 0; q < strat.size(); ++q)
-            cuda_check(cudaMemcpyAsync(hring + slot * AREL + q, rels[strat[q]]->ndev.ptr(), 4, cudaMemcpyDeviceToHost, st),
-                       "D2H");
-          cuda_check(cudaEventRecord(ring_ev[slot], st), "event");
-          pending.push_back(rounds);
+          pending.push_back({rounds, ring_seq});
           if ((done = drain_async(pending, trace_base, false)) > 0) { rounds = (int)done; break; }
           continue;
         }

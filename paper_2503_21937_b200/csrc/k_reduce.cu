@@ -507,7 +507,8 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
                                                          const uint32_t* __restrict__ tcnt,
                                                          const uint32_t* __restrict__ gsum,
                                                          uint32_t* __restrict__ total, unsigned long long restamp,
-                                                         unsigned long long wmask) {
+                                                         unsigned long long wmask, unsigned long long* ring,
+                                                         uint32_t seq) {
   __shared__ uint32_t wtot[8];
   __shared__ uint32_t wpre[8];
   __shared__ uint32_t s_base;
@@ -546,7 +547,13 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
     const uint32_t agg = __shfl_sync(0xffffffffu, inc, 7);
     if (lane == 0) {
       s_base = prefix;
-      if (tile == (int64_t)gridDim.x - 1) *total = prefix + agg;
+      if (tile == (int64_t)gridDim.x - 1) {
+        *total = prefix + agg;
+        if (ring) {  // zero-copy report to the host (async rounds)
+          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | (prefix + agg);
+          __threadfence_system();
+        }
+      }
     }
     __syncwarp();
     if (lane < 8) wtot[lane] = inc - own;
@@ -814,7 +821,7 @@ int64_t direct_extract2_scratch(int64_t nwords) {
 }
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
-                            unsigned long long wmask, cudaStream_t st) {
+                            unsigned long long wmask, unsigned long long* ring, uint32_t seq, cudaStream_t st) {
   if (nwords <= 0) return;
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   const int64_t ng = (nt + LB_GROUP - 1) / LB_GROUP;
@@ -824,9 +831,9 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
   note_launch();
   switch (semi) {
-    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
-    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
-    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask); break;
+    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
+    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
+    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
   }
 }
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
