@@ -106,6 +106,7 @@ struct RelState {
   DBuf<uint32_t> dirty;  // bitmap of the slots improved this round
   DBuf<unsigned long long> dctr;  // |Δ'| counter of the single-pass extraction
   DBuf<uint32_t> ndev;             // |Δ'| of the last extraction (device)
+  DBuf<uint32_t> ectr;             // one-launch extraction counters (rows, finished CTAs), kept zeroed
   bool async = false;              // rounds run without a host sync: Δ size lives in ndev
   unsigned long long* ring_dst = nullptr;  // async: host-mapped word for (seq << 32 | |Δ'|)
   uint32_t ring_seq = 0;
@@ -152,6 +153,7 @@ struct RelState {
     for (auto* b : {&o_soff, &goff, &gfid}) b->bind(st);
     dctr.bind(st);
     ndev.bind(st);
+    ectr.bind(st);
     for (auto& c : in.cols) c.bind(st);
     for (auto& c : acc_col) c.bind(st);
     acc_sid.bind(st);
@@ -245,6 +247,7 @@ struct Ctx {
   };
   bool force_sorted = getenv("LOBSTER_SORTED_STORE") != nullptr;      // A/B: merge-based store
   bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
+  bool sorted_delta = getenv("LOBSTER_SORTED_DELTA") != nullptr;      // A/B: fully slot-ordered Δ' (2 launches)
   int64_t num_facts_db = 0;
   // timing
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -1314,6 +1317,10 @@ struct Ctx {
       S.dirty.reserve((ns + 31) / 32);
       S.ndev.reserve(1);
       S.dctr.reserve(1);
+      if (S.ectr.bytes() < 8) {
+        S.ectr.reserve(2);
+        cuda_check(cudaMemsetAsync(S.ectr.ptr(), 0, 8, st), "memset");
+      }
       cuda_check(cudaMemsetAsync(S.dctr.ptr(), 0, 8, st), "memset");
       S.cand_bound = 0;
       cuda_check(cudaMemsetAsync(S.dirty.ptr(), 0, (size_t)((ns + 31) / 32) * 4, st), "memset");
@@ -1355,9 +1362,9 @@ struct Ctx {
       Phase ph(this, 3);
       launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
                              semi != S_UNIT ? S.dp.ptr() : nullptr, nullptr,
-                             arena.get<uint32_t>(direct_extract2_scratch(nw)), S.ndev.ptr(),
+                             sorted_delta ? arena.get<uint32_t>(direct_extract2_scratch(nw)) : nullptr, S.ndev.ptr(),
                              semi == S_MAXMULT && !S.stamp_mode ? S.smax << S.wWB : 0ull, mx_wmask(S),
-                             S.async ? S.ring_dst : nullptr, S.ring_seq, st);
+                             S.async ? S.ring_dst : nullptr, S.ring_seq, sorted_delta ? nullptr : S.ectr.ptr(), st);
       kcheck("direct extract");
     }
     if (S.async) {  // |Δ'| stays on the device: the next join reads it, the host polls it later

@@ -500,7 +500,11 @@ __global__ void __launch_bounds__(256) dirty_group_count_k(const uint32_t* __res
   }
 }
 
-template <int SEMI>
+// ATOMIC: one launch, no counting pass — each warp claims its output range with
+// one atomicAdd (Δ' = runs sorted within each warp's 8192 slots, runs in any
+// order; joins over idempotent ⊕ do not depend on Δ order) and the last CTA to
+// finish publishes |Δ'| (ctr[0] = rows, ctr[1] = finished CTAs; both reset).
+template <int SEMI, bool ATOMIC>
 __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
                                                          int64_t nw, uint32_t* __restrict__ dkey,
                                                          float* __restrict__ dp, uint32_t* __restrict__ dw,
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
                                                          const uint32_t* __restrict__ gsum,
                                                          uint32_t* __restrict__ total, unsigned long long restamp,
                                                          unsigned long long wmask, unsigned long long* ring,
-                                                         uint32_t seq) {
+                                                         uint32_t seq, uint32_t* __restrict__ ctr) {
   __shared__ uint32_t wtot[8];
   __shared__ uint32_t wpre[8];
   __shared__ uint32_t s_base;
@@ -523,13 +527,19 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
     m[j] = w < nw ? __ldcg(dirty + w) : 0u;
     c += __popc(m[j]);
   }
+  const uint32_t wsum = __reduce_add_sync(0xffffffffu, c);
+  uint32_t base;
+  if constexpr (ATOMIC) {
+    uint32_t wb = 0;
+    if (lane == 0 && wsum) wb = atomicAdd(ctr, wsum);
+    base = __shfl_sync(0xffffffffu, wb, 0);
+  } else {
   // tile base: groups before this tile's group + this group's earlier tiles
   const int64_t grp = tile / LB_GROUP;
   uint32_t pre = 0;
   for (int64_t i = threadIdx.x; i < grp; i += 256) pre += gsum[i];
   if (threadIdx.x < (unsigned)(tile - grp * LB_GROUP)) pre += tcnt[grp * LB_GROUP + threadIdx.x];
   pre = __reduce_add_sync(0xffffffffu, pre);
-  const uint32_t wsum = __reduce_add_sync(0xffffffffu, c);
   if (lane == 0) {
     wtot[warp] = wsum;
     wpre[warp] = pre;
@@ -559,7 +569,8 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
     if (lane < 8) wtot[lane] = inc - own;
   }
   __syncthreads();
-  uint32_t base = s_base + wtot[warp];
+  base = s_base + wtot[warp];
+  }
 #pragma unroll 1
   for (int j = 0; j < LB_WPT; ++j) {
     const uint32_t mm = m[j];
@@ -627,6 +638,23 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
       }
     }
     base += tot;
+  }
+  if constexpr (ATOMIC) {  // the last CTA to finish publishes |Δ'| and resets the counters
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctr);
+        *total = n;
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+        if (ring) {
+          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | n;
+          __threadfence_system();
+        }
+      }
+    }
   }
 }
 
@@ -821,20 +849,27 @@ int64_t direct_extract2_scratch(int64_t nwords) {
 }
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
-                            unsigned long long wmask, unsigned long long* ring, uint32_t seq, cudaStream_t st) {
+                            unsigned long long wmask, unsigned long long* ring, uint32_t seq, uint32_t* ctr,
+                            cudaStream_t st) {
   if (nwords <= 0) return;
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   const int64_t ng = (nt + LB_GROUP - 1) / LB_GROUP;
   uint32_t* tcnt = scratch;
-  uint32_t* gsum = scratch + nt;
-  note_launch();
-  dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
-  note_launch();
-  switch (semi) {
-    case S_UNIT: direct_extract2_k<S_UNIT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
-    case S_MAXMIN: direct_extract2_k<S_MAXMIN><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
-    default: direct_extract2_k<S_MAXMULT><<<(unsigned)nt, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, restamp, wmask, ring, seq); break;
+  uint32_t* gsum = scratch ? scratch + nt : nullptr;
+  const unsigned g = (unsigned)nt;
+  if (!ctr) {  // slot-ordered Δ': counting pass first
+    note_launch();
+    dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
   }
+  note_launch();
+#define LOB_EX(S, A) direct_extract2_k<S, A><<<g, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, \
+                                                                  restamp, wmask, ring, seq, ctr)
+  switch (semi) {
+    case S_UNIT: if (ctr) LOB_EX(S_UNIT, true); else LOB_EX(S_UNIT, false); break;
+    case S_MAXMIN: if (ctr) LOB_EX(S_MAXMIN, true); else LOB_EX(S_MAXMIN, false); break;
+    default: if (ctr) LOB_EX(S_MAXMULT, true); else LOB_EX(S_MAXMULT, false); break;
+  }
+#undef LOB_EX
 }
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
   if (nslots <= 0) return;

@@ -285,10 +285,13 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st);
 // dirty bits cleared, max-mult slots re-settled; |Δ'| -> *total (device).  scratch: direct_extract2_scratch u32
 int64_t direct_extract2_scratch(int64_t nwords);
 // restamp (max-mult): OR-ed into every Δ' slot word (0 = none).  ring (nullable,
-// host-mapped): also receives seq << 32 | |Δ'| (system-scope store)
+// host-mapped): also receives seq << 32 | |Δ'| (system-scope store).  ctr (nullable,
+// 2 zeroed u32 that the kernel leaves zeroed): one launch, Δ' in slot-sorted runs
+// claimed by atomics instead of fully slot-ordered (scratch unused)
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
-                            unsigned long long wmask, unsigned long long* ring, uint32_t seq, cudaStream_t st);
+                            unsigned long long wmask, unsigned long long* ring, uint32_t seq, uint32_t* ctr,
+                            cudaStream_t st);
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st);
 // wT / wrb: witness decompression (variable field width, rule-index bits)
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
