@@ -1922,6 +1922,12 @@ struct Ctx {
       w.p = S.p.ptr();
       w.w = S.w.ptr();
       w.fid = S.fid.ptr();
+      if (S.direct && semi == S_MAXMULT) {  // O(1) hops through the store's final words
+        w.dir = reinterpret_cast<const unsigned long long*>(S.dirf.get());
+        w.wmask = mx_wmask(S);
+        w.wT = S.wT;
+        w.wrb = S.wrb;
+      }
       w.n = S.n;
       w.input = prog.rels[r].input ? 1 : 0;
       w.has_sample = S.L.has_sample ? 1 : 0;

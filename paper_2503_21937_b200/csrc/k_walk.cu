@@ -38,14 +38,23 @@ __global__ void walk_k(const WalkTables T, int rel0, int64_t n, int pass, const 
     const int r = srel[sp];
     const uint64_t k = skey[sp];
     const WalkRel& R = T.rels[r];
-    const int64_t idx = find_key(R, k);
-    if (idx < 0) { atomicOr(err, 1); return; }
-    if (R.input) {
-      if (pass) leaves[out + count] = (int64_t)R.fid[idx];
-      ++count;
-      continue;
+    uint32_t w;
+    if (R.dir && !R.input) {  // direct store still holds the final words: slot = packed key
+      const unsigned long long word = R.dir[k];
+      if (!word) { atomicOr(err, 1); return; }
+      const unsigned long long wc = ~word & R.wmask;
+      const unsigned long long vars = wc & ((1ull << R.wT) - 1ull);
+      w = (uint32_t)(R.wrb ? (((wc >> R.wT) << (32 - R.wrb)) | vars) : vars);
+    } else {
+      const int64_t idx = find_key(R, k);
+      if (idx < 0) { atomicOr(err, 1); return; }
+      if (R.input) {
+        if (pass) leaves[out + count] = (int64_t)R.fid[idx];
+        ++count;
+        continue;
+      }
+      w = R.w[idx];
     }
-    const uint32_t w = R.w[idx];
     const int rb = T.rule_bits[r];
     const int lr = rb ? (int)(w >> (32 - rb)) : 0;
     const WalkRule& ru = T.rules[T.rule_base[r] + lr];

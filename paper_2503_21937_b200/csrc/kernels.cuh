@@ -315,6 +315,9 @@ struct WalkRel {
   const float* p;
   const uint32_t* w;       // IDB witness
   const int32_t* fid;      // EDB fact id
+  const unsigned long long* dir;  // nullable: the relation's direct max-mult store (O(1) hop, MxEnc words)
+  unsigned long long wmask;
+  int wT, wrb;
   int64_t n;
   int input;
   int has_sample;
