@@ -853,7 +853,7 @@ struct Ctx {
         direct_target(H, lp.direct, lp.fdir, lp.dirty, lp.aggregate, lp.mx);
       } else {
         reserve_candidates(H, H.nc + T.n);
-        lp.ok32 = H.dense;
+        lp.ok32 = c32(H);
         lp.okey = cand_key(H);
         lp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
         lp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
@@ -872,7 +872,7 @@ struct Ctx {
       ProjectPlan pp{};
       pp.key = T.key;
       pp.pk32 = T.k32;
-      pp.ok32 = H.dense;
+      pp.ok32 = c32(H);
       pp.tag = semi != S_UNIT ? T.tags[0] : nullptr;
       pp.n = T.n;
       for (auto& c : pending_start) pp.cmp[pp.ncmp++] = c;
@@ -1053,7 +1053,7 @@ struct Ctx {
           direct_target(H, jp.direct, jp.fdir, jp.dirty, jp.aggregate, jp.mx);
         } else {
           reserve_candidates(H, H.nc + total);
-          jp.ok32 = H.dense;
+          jp.ok32 = c32(H);
           jp.okey = cand_key(H);
           jp.oval32 = semi == S_MAXMIN || semi == S_ADDMULT ? H.cv32.ptr() + H.nc : nullptr;
           jp.oval64 = semi == S_MAXMULT ? H.cv64.ptr() + H.nc : nullptr;
@@ -1154,12 +1154,16 @@ struct Ctx {
     }
   }
 
+  // u32 candidate keys whenever the head's packed key fits 31 bits (dense stores
+  // always): the dead key ~0 still sorts last, and sorts move 4 B less per key
+  bool c32(const RelState& H) const { return H.dense || (H.L.total <= 31 && !getenv("LOBSTER_C64")); }
+
   void* cand_key(RelState& H) {
-    return H.dense ? (void*)(H.ckey32.ptr() + H.nc) : (void*)(H.ckey.ptr() + H.nc);
+    return c32(H) ? (void*)(H.ckey32.ptr() + H.nc) : (void*)(H.ckey.ptr() + H.nc);
   }
 
   void reserve_candidates(RelState& H, int64_t n) {
-    if (H.dense) H.ckey32.reserve(n, H.nc);
+    if (c32(H)) H.ckey32.reserve(n, H.nc);
     else H.ckey.reserve(n, H.nc);
     if (semi == S_MAXMIN || semi == S_ADDMULT) H.cv32.reserve(n, H.nc);
     if (semi == S_MAXMULT) H.cv64.reserve(n, H.nc);
@@ -1402,6 +1406,7 @@ struct Ctx {
     S.nc = 0;
     if (nc == 0) { S.nd = 0; return 0; }
     const int tb = S.L.total + 1;  // +1 bit: KEY_DEAD sorts after every key
+    if (c32(S)) return settle_sorted32(S, nc, tb);
     S.ckey2.reserve(nc);
     uint64_t* ks;
     const void* vs;
@@ -1442,6 +1447,61 @@ struct Ctx {
       launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey, up, uw, arena.get<uint32_t>(2 * nu + 2), st);
       kcheck("seg reduce");
     }
+    return merge_unique(S, ukey, up, uw, nu, nc);
+  }
+
+  // Sorted store with u32 candidates: u32 radix sort + segmented ⊕, then the
+  // unique keys widen to u64 for the diff / apply / merge against F.
+  int64_t settle_sorted32(RelState& S, int64_t nc, int tb) {
+    S.ckey32b.reserve(nc);
+    uint32_t* ks;
+    const void* vs;
+    {
+      Phase ph(this, 1);
+      void* stmp = arena.alloc(sort_tmp_bytes(nc));
+      int which;
+      if (semi == S_MAXMULT) {
+        S.cv64b.reserve(nc);
+        which = radix_sort(S.ckey32.ptr(), S.cv64.ptr(), S.ckey32b.ptr(), S.cv64b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv64b.ptr() : S.cv64.ptr();
+      } else if (semi == S_UNIT) {
+        which = radix_sort<uint32_t, void>(S.ckey32.ptr(), nullptr, S.ckey32b.ptr(), nullptr, nc, tb, stmp, st);
+        vs = nullptr;
+      } else {
+        S.cv32b.reserve(nc);
+        which = radix_sort(S.ckey32.ptr(), S.cv32.ptr(), S.ckey32b.ptr(), S.cv32b.ptr(), nc, tb, stmp, st);
+        vs = which ? S.cv32b.ptr() : S.cv32.ptr();
+      }
+      ks = which ? S.ckey32b.ptr() : S.ckey32.ptr();
+      kcheck("sort");
+    }
+    uint32_t* fl = arena.get<uint32_t>(nc);
+    uint32_t* pos = arena.get<uint32_t>(nc);
+    uint32_t* tot = arena.get<uint32_t>(1);
+    {
+      Phase ph(this, 2);
+      launch_heads(ks, nc, fl, st);
+      exclusive_scan<uint32_t>(fl, pos, nc, tot, arena.alloc(scan_tmp_bytes<uint32_t>(nc)), st);
+      kcheck("heads");
+    }
+    const int64_t nu = read_dev(tot);
+    uint32_t* ukey32 = arena.get<uint32_t>(nu);
+    uint64_t* ukey = arena.get<uint64_t>(nu);
+    float* up = semi != S_UNIT ? arena.get<float>(nu) : nullptr;
+    uint32_t* uw = semi == S_MAXMULT ? arena.get<uint32_t>(nu) : nullptr;
+    {
+      Phase ph(this, 2);
+      launch_seg_reduce(ks, vs, pos, nc, nu, semi, ukey32, up, uw, arena.get<uint32_t>(2 * nu + 2), st);
+      launch_widen_u32(ukey32, nu, ukey, st);
+      kcheck("seg reduce");
+    }
+    return merge_unique(S, ukey, up, uw, nu, nc);
+  }
+
+  // A8 for the sorted store: classify U against F, write Δ' and apply in place,
+  // merge the new tuples (U sorted, unique, u64 keys)
+  int64_t merge_unique(RelState& S, const uint64_t* ukey, const float* up, const uint32_t* uw, int64_t nu,
+                       int64_t nc) {
     uint64_t* flags = arena.get<uint64_t>(nu);
     uint64_t* offs = arena.get<uint64_t>(nu);
     int64_t* fpos = arena.get<int64_t>(nu);

@@ -430,6 +430,11 @@ __global__ void dense_compact_k(const float* __restrict__ fp, const uint32_t* __
   }
 }
 
+__global__ void widen_u32_k(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint64_t)in[i];
+}
+
 // ------------------------------------------------------ direct ⊕ store ----
 // wmask / wT / wrb: max-mult witness field and its decompression (kernels.cuh MxEnc):
 // wc = rule << wT | vars  ->  w = rule << (32 - wrb) | vars
@@ -843,6 +848,12 @@ void launch_direct_fill(void* f, int64_t nslots, int semi, cudaStream_t st) {
                                       : (size_t)nslots * (semi == S_MAXMULT ? 8 : 4);
   cudaMemsetAsync(f, 0, bytes, st);
 }
+void launch_widen_u32(const uint32_t* in, int64_t n, uint64_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch();
+  widen_u32_k<<<grid_for(n, 256), 256, 0, st>>>(in, n, out);
+}
+
 int64_t direct_extract2_scratch(int64_t nwords) {
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   return nt + (nt + LB_GROUP - 1) / LB_GROUP;

@@ -358,6 +358,9 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
                  int64_t ntup, const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
                  cudaStream_t st);
 
+// u32 keys -> u64 (sorted-store candidates narrowed for the sort)
+void launch_widen_u32(const uint32_t* in, int64_t n, uint64_t* out, cudaStream_t st);
+
 // ---- output extract (A12) ----
 void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,
                    const uint8_t* bits, const int32_t* mins, int32_t* sample, int32_t* cols, cudaStream_t st);
