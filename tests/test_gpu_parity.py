@@ -44,6 +44,28 @@ def test_random_digraphs(seed, sr):
     assert stats["rounds_total"] == int(res.rounds.sum())
 
 
+EVEN_ODD_PROGRAM = """
+type edge(x: i32, y: i32)
+rel odd(x, y) :- edge(x, y) or (even(x, z) and edge(z, y)).
+rel even(x, y) :- odd(x, z), edge(z, y).
+output odd
+output even
+"""
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("sr", [0, 1, 3])
+def test_mutual_recursion_async_rounds(seed, sr):
+    """Two relations in one recursive stratum (odd / even path lengths): the
+    asynchronous rounds count both relations' Δ' (one ring word each) and stop
+    on the same round as the oracle."""
+    w = W.random_digraph_workload(24, 0.12, 700 + seed, sr, batch=4, program=EVEN_ODD_PROGRAM)
+    eng, stats, res = run_both(w, outputs=["odd", "even"])
+    assert_parity(eng, res, "odd", sr)
+    assert_parity(eng, res, "even", sr)
+    assert stats["rounds_total"] == int(res.rounds.sum())
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_dag_addmult(seed):
     w = W.random_dag_workload(30, 0.2, 50 + seed, 2, batch=4)
