@@ -293,7 +293,9 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // Measured on C2 and rejected: two rows per thread (152 vs 101 us per launch:
 // fewer resident warps for the same requests in flight), a fixed-width ELL
 // copy of the build index replacing boff -> bkey (+3%: boff hits L1), a
-// software pipeline prefetching row i+stride's key and CSR range (+22%).
+// software pipeline prefetching row i+stride's key and CSR range (+22%),
+// warp-merged dirty-bit updates (__match_any_sync + __reduce_or_sync per
+// direction: +29%, the warp collectives cost more than the REDs they save).
 #ifndef FJ_MINB
 #define FJ_MINB 6
 #endif
