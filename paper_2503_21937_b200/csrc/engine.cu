@@ -108,6 +108,7 @@ struct RelState {
   DBuf<uint32_t> ndev;             // |Δ'| of the last extraction (device)
   DBuf<uint32_t> ectr;             // one-launch extraction counters (rows, finished CTAs), kept zeroed
   bool async = false;              // rounds run without a host sync: Δ size lives in ndev
+  bool lazy = false;               // finished direct store not yet compacted to the sorted form (n is exact)
   unsigned long long* ring_dst = nullptr;  // async: host-mapped word for (seq << 32 | |Δ'|)
   uint32_t ring_seq = 0;
   // max-mult direct words (kernels.cuh MxEnc): witness field WB = wrb + wT bits,
@@ -248,6 +249,7 @@ struct Ctx {
   bool force_sorted = getenv("LOBSTER_SORTED_STORE") != nullptr;      // A/B: merge-based store
   bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
   bool sorted_delta = getenv("LOBSTER_SORTED_DELTA") != nullptr;      // A/B: fully slot-ordered Δ' (2 launches)
+  bool eager_compact = getenv("LOBSTER_EAGER_COMPACT") != nullptr;    // A/B: compact direct stores at stratum end
   int64_t num_facts_db = 0;
   // timing
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -365,6 +367,7 @@ struct Ctx {
     for (auto& r : rels) {
       r->in.n = 0;
       r->n = r->nd = r->no = r->nc = 0;
+      r->lazy = false;
       r->out_dev_ready = r->out_host_ready = false;
       r->has_grad = false;
     }
@@ -680,6 +683,7 @@ struct Ctx {
     if (it != static_idx.end()) return it->second.get();
     std::unique_ptr<Index> ix(new Index());
     RelState& S = *rels[r];
+    ensure_sorted(S);
     build_index(*ix, S.L, order, nbound, S.key.ptr(), semi == S_UNIT ? nullptr : S.p.ptr(), S.n, true, true);
     Index* raw = ix.get();
     static_idx[key] = std::move(ix);
@@ -701,7 +705,9 @@ struct Ctx {
         if (S.dense) return {S.dkey32.ptr(), tag ? S.dp.ptr() : nullptr, S.nd, true};
         return {S.dkey.ptr(), tag ? S.dp.ptr() : nullptr, S.nd, false};
       case V_OLD: return {S.okey.ptr(), tag ? S.op.ptr() : nullptr, S.no, false};
-      default: return {S.key.ptr(), tag ? S.p.ptr() : nullptr, S.n, false};
+      default:
+        ensure_sorted(S);
+        return {S.key.ptr(), tag ? S.p.ptr() : nullptr, S.n, false};
     }
   }
 
@@ -754,7 +760,12 @@ struct Ctx {
     Table T;
     const BodyAtom& A0 = R.body[start];
     const Layout& L0 = rels[A0.rel]->L;
-    VerData d0 = version_data(A0.rel, ver[start]);
+    // a lazily compacted direct store probed by a lookup chain: probe its slot
+    // words directly (slot index = packed key; absent slots are skipped)
+    RelState& S0 = *rels[A0.rel];
+    const bool dense_probe = S0.lazy && ver[start] == V_EXT && na >= 2 && covers_rule(R, start) && !force_slot_join;
+    if (dense_probe && S0.n == 0) return;
+    VerData d0 = dense_probe ? VerData{nullptr, nullptr, S0.nslots, true} : version_data(A0.rel, ver[start]);
     if (d0.n == 0) return;
     T.key = d0.key;
     T.k32 = d0.k32;
@@ -790,6 +801,7 @@ struct Ctx {
       lp.pk32 = T.k32;
       lp.np = T.n;
       lp.ptag = semi != S_UNIT ? T.tags[0] : nullptr;
+      if (dense_probe) lp.pdir = S0.dirf.get();
       std::vector<int> tag_atoms{start};
       for (int a = 0; a < na; ++a) {
         if (a == start) continue;
@@ -1243,6 +1255,12 @@ struct Ctx {
     return nd;
   }
 
+  void ensure_sorted(RelState& S) {
+    if (!S.lazy) return;
+    S.lazy = false;
+    dense_to_sorted(S);
+  }
+
   // dense F -> sorted list (key, p, w) for later strata, outputs and the walk
   void dense_to_sorted(RelState& S) {
     const int64_t ns = S.nslots;
@@ -1303,6 +1321,7 @@ struct Ctx {
   void choose_store(RelState& S, int r) {
     S.dense = false;
     S.direct = false;
+    S.lazy = false;
     if (S.build_local || S.L.total > 30 || force_sorted) return;
     if (semi != S_ADDMULT && !force_sort_dedup) {  // idempotent ⊕: fused direct store
       const int64_t ns = (int64_t)1 << S.L.total;
@@ -1644,6 +1663,7 @@ struct Ctx {
       const Relation& R = prog.rels[r];
       if (R.input) continue;
       RelState& S = *rels[r];
+      if (R.output) ensure_sorted(S);
       if (!R.output) {
         S.retained = false;
         continue;
@@ -1901,8 +1921,23 @@ struct Ctx {
         pending.clear();
       }
       HostTimer ht(host_ms[3]);
-      for (int r : strat)
-        if (rels[r]->dense) dense_to_sorted(*rels[r]);
+      // Finished direct stores are compacted on first use (ensure_sorted): a lookup
+      // chain can probe the slot words directly, so e.g. C2's `path` (64M tuples)
+      // is never copied out unless an output or a sorted index asks for it.
+      for (int r : strat) {
+        RelState& S = *rels[r];
+        if (!S.dense) continue;
+        if (S.direct && !eager_compact) {
+          unsigned long long* c = arena.get<unsigned long long>(1);
+          cuda_check(cudaMemsetAsync(c, 0, 8, st), "memset");
+          launch_direct_count(S.dirf.get(), S.nslots, semi, c, st);
+          kcheck("direct count");
+          S.n = (int64_t)read_dev(c);
+          S.lazy = true;
+        } else {
+          dense_to_sorted(S);
+        }
+      }
       mark("dense->sorted");
       stats.rounds_total += rounds;
       stats.strata++;
@@ -1973,6 +2008,8 @@ struct Ctx {
   // --------------------------------------------------------- gradients (A11)
   void gradients() {
     const int nr = (int)prog.rels.size();
+    for (int r = 0; r < nr; ++r)  // walks start from the output relations' sorted rows
+      if (prog.rels[r].output) ensure_sorted(*rels[r]);
     std::vector<WalkRel> wr(nr);
     for (int r = 0; r < nr; ++r) {
       RelState& S = *rels[r];
@@ -2103,6 +2140,7 @@ struct Ctx {
     if (!S.retained)
       throw Failure(LOBSTER_E_INVALID_ARG, std::string("relation ") + relname +
                                                " was not retained by a micro-batched run (declare it `output`)");
+    ensure_sorted(S);
     const int ar = prog.rels[r].arity;
     const int64_t n = S.n;
     if (!S.out_dev_ready) {

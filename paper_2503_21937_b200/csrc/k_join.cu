@@ -442,8 +442,32 @@ constexpr int LC_CAND = 0, LC_DIRECT = 1;
 
 // One probe row of a lookup chain: filters, point lookups, ⊗ in body order,
 // witness and head key.  Returns whether the row yields a candidate.
+// probe row i: its key and tag, from the probe arrays or (pdir) a direct store's
+// slot word (slot i present <=> row exists; key = slot)
 template <typename PK>
-__device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pkr, int64_t i, float& t, uint32_t& w,
+__device__ __forceinline__ PK lookup_probe(const LookupPlan& lp, int semi, int64_t i, float& p0) {
+  p0 = 1.0f;
+  if (lp.pdir) {
+    if (semi == S_UNIT) {
+      const uint32_t wd = reinterpret_cast<const uint32_t*>(lp.pdir)[i >> 5];
+      return ((wd >> (i & 31)) & 1u) ? (PK)i : dead<PK>();
+    }
+    if (semi == S_MAXMIN) {
+      const uint32_t v = reinterpret_cast<const uint32_t*>(lp.pdir)[i];
+      p0 = mm_p(v);
+      return v ? (PK)i : dead<PK>();
+    }
+    const unsigned long long v = reinterpret_cast<const unsigned long long*>(lp.pdir)[i];
+    p0 = mx_p(v);
+    return v ? (PK)i : dead<PK>();
+  }
+  const PK k = reinterpret_cast<const PK*>(lp.pkey)[i];
+  if (semi != S_UNIT && lp.ptag && k != dead<PK>()) p0 = lp.ptag[i];
+  return k;
+}
+
+template <typename PK>
+__device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pkr, float p0, float& t, uint32_t& w,
                                            uint64_t& key) {
   bool ok = pkr != dead<PK>();
   const uint64_t pk = (uint64_t)pkr;
@@ -454,7 +478,7 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
     ok &= lp.cmp[c].neq ? (a != b) : (a == b);
   }
   float tags[MAXL + 1];
-  tags[0] = (semi != S_UNIT && lp.ptag && ok) ? lp.ptag[i] : 1.0f;
+  tags[0] = p0;
 #pragma unroll
   for (int l = 0; l < MAXL; ++l) {
     tags[l + 1] = 1.0f;
@@ -533,7 +557,6 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
   constexpr bool DIRECT = MODE >= LC_DIRECT;
   constexpr int SEMI_C = DIRECT ? MODE - LC_DIRECT : -1;
   const int semi = DIRECT ? SEMI_C : lp.semi;
-  const PK* __restrict__ pkey = reinterpret_cast<const PK*>(lp.pkey);
   OK* __restrict__ okey = reinterpret_cast<OK*>(lp.okey);
   uint32_t mycount = 0;
   if (DIRECT && lp.aggregate) {
@@ -550,11 +573,12 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
     unsigned long long run = 0;
     for (int64_t base = r0; base < r1; base += 32) {
       const int64_t i = base + (threadIdx.x & 31);
-      const PK pkr = i < r1 ? pkey[i] : dead<PK>();
+      float p0 = 1.0f;
+      const PK pkr = i < r1 ? lookup_probe<PK>(lp, SEMI_C, i, p0) : dead<PK>();
       float t;
       uint32_t w;
       uint64_t key;
-      const bool ok = lookup_row<PK>(lp, SEMI_C, pkr, i, t, w, key);
+      const bool ok = lookup_row<PK>(lp, SEMI_C, pkr, p0, t, w, key);
       if (ok) ++mycount;
       const uint32_t slot = (uint32_t)key;
       const unsigned act = __ballot_sync(0xffffffffu, ok);
@@ -580,10 +604,11 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
   } else {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lp.np;
          i += (int64_t)gridDim.x * blockDim.x) {
-      float t;
+      float t, p0;
       uint32_t w;
       uint64_t key;
-      const bool ok = lookup_row<PK>(lp, semi, pkey[i], i, t, w, key);
+      const PK pkr = lookup_probe<PK>(lp, semi, i, p0);
+      const bool ok = lookup_row<PK>(lp, semi, pkr, p0, t, w, key);
       if (ok) ++mycount;
       if constexpr (DIRECT) {
         if (ok) direct_oplus(SEMI_C, lp.fdir, (uint32_t)key, t, w, lp.dirty, 0, lp.mx);

@@ -674,6 +674,23 @@ __global__ void direct_present_k(const void* __restrict__ f, int64_t n, int semi
   }
 }
 
+__global__ void direct_count_k(const void* __restrict__ f, int64_t n, int semi, unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  if (semi == S_UNIT) {  // bitmap words (bits past n are never set)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n + 31) / 32; i += S)
+      c += __popc(reinterpret_cast<const uint32_t*>(f)[i]);
+  } else if (semi == S_MAXMIN) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += S)
+      c += reinterpret_cast<const uint32_t*>(f)[i] != 0u;
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += S)
+      c += reinterpret_cast<const unsigned long long*>(f)[i] != 0ull;
+  }
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void direct_compact_k(const void* __restrict__ f, const uint32_t* __restrict__ pos, int64_t n, int semi,
                                  uint64_t* __restrict__ key, float* __restrict__ p, uint32_t* __restrict__ w,
                                  unsigned long long wmask, int wT, int wrb) {
@@ -886,6 +903,11 @@ void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* fl
   if (nslots <= 0) return;
   note_launch();
   direct_present_k<<<grid_for(nslots, 256), 256, 0, st>>>(f, nslots, semi, flag);
+}
+void launch_direct_count(const void* f, int64_t nslots, int semi, unsigned long long* out, cudaStream_t st) {
+  if (nslots <= 0) return;
+  note_launch();
+  direct_count_k<<<148 * 8, 256, 0, st>>>(f, nslots, semi, out);
 }
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
                            uint32_t* w, unsigned long long wmask, int wT, int wrb, cudaStream_t st) {

@@ -165,6 +165,7 @@ struct LookupPlan {
   int8_t pk32, ok32;
   int64_t np;
   const float* ptag;
+  const void* pdir;   // nullable: probe = the present slots of a direct store (np = slots; key = slot)
   int nlk;
   Lookup lk[MAXL];
   int ncmp;
@@ -293,6 +294,8 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
                             unsigned long long wmask, unsigned long long* ring, uint32_t seq, uint32_t* ctr,
                             cudaStream_t st);
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st);
+// number of present slots -> atomicAdd into *out
+void launch_direct_count(const void* f, int64_t nslots, int semi, unsigned long long* out, cudaStream_t st);
 // wT / wrb: witness decompression (variable field width, rule-index bits)
 void launch_direct_compact(const void* f, const uint32_t* pos, int64_t nslots, int semi, uint64_t* key, float* p,
                            uint32_t* w, unsigned long long wmask, int wT, int wrb, cudaStream_t st);

@@ -349,14 +349,15 @@ def test_rerun_new_database():
 
 
 @pytest.mark.parametrize("env", ["LOBSTER_SORTED_STORE", "LOBSTER_SORT_DEDUP", "LOBSTER_SYNC_ROUNDS",
-                                 "LOBSTER_NO_STAMPS", "LOBSTER_SORTED_DELTA"])
+                                 "LOBSTER_NO_STAMPS", "LOBSTER_SORTED_DELTA", "LOBSTER_EAGER_COMPACT"])
 @pytest.mark.parametrize("sr", [0, 1, 3])
 def test_store_paths_match(sr, env, monkeypatch):
     """Every relation-store path (merge-based sorted store; dense store with
     radix sort + segmented ⊕; default dense direct ⊕, with host-synchronised
     rounds as well as the default asynchronous ones, max-mult words with a
-    re-stamped settled field instead of round stamps, and a fully slot-ordered
-    Δ' instead of atomically claimed sorted runs) matches the oracle."""
+    re-stamped settled field instead of round stamps, a fully slot-ordered Δ'
+    instead of atomically claimed sorted runs, and stores compacted at stratum
+    end instead of on first use) matches the oracle."""
     monkeypatch.setenv(env, "1")
     w = W.c2_workload(semiring=sr, n=8, batch=5)
     eng, stats, res = run_both(w, outputs=["path", "endpoints_connected"])
