@@ -2019,6 +2019,16 @@ struct Ctx {
       w.p = S.p.ptr();
       w.w = S.w.ptr();
       w.fid = S.fid.ptr();
+      if (prog.rels[r].input) {  // an index aliasing the rows, with CSR offsets: O(1) + a short scan
+        for (auto& kv : static_idx) {
+          const Index& ix = *kv.second;
+          if (kv.first.first != r || ix.key != S.key.ptr() || !ix.offp || ix.maxdeg < 0 || ix.maxdeg > 64) continue;
+          w.off = ix.offp;
+          w.nprefix = ix.nprefix;
+          w.pshift = ix.free_bits;
+          break;
+        }
+      }
       if (S.direct && semi == S_MAXMULT) {  // O(1) hops through the store's final words
         w.dir = reinterpret_cast<const unsigned long long*>(S.dirf.get());
         w.wmask = mx_wmask(S);

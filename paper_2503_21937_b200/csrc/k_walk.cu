@@ -16,6 +16,13 @@ namespace {
 constexpr int STACK = 64;
 
 __device__ int64_t find_key(const WalkRel& R, uint64_t k) {
+  if (R.off) {
+    const uint64_t pre = k >> R.pshift;
+    if (pre >= (uint64_t)R.nprefix) return -1;
+    for (int64_t i = R.off[pre], e = R.off[pre + 1]; i < e; ++i)
+      if (R.key[i] == k) return i;
+    return -1;
+  }
   const int64_t i = lower_bound_u64(R.key, R.n, k);
   return (i < R.n && R.key[i] == k) ? i : -1;
 }

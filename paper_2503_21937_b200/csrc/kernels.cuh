@@ -321,6 +321,9 @@ struct WalkRel {
   const unsigned long long* dir;  // nullable: the relation's direct max-mult store (O(1) hop, MxEnc words)
   unsigned long long wmask;
   int wT, wrb;
+  const int64_t* off;  // nullable: CSR over key >> pshift (an aliasing static index): O(1) + short scan
+  int64_t nprefix;
+  int pshift;
   int64_t n;
   int input;
   int has_sample;
