@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) dirty_group_count_k(const uint32_t* __res
 // one atomicAdd (Δ' = runs sorted within each warp's 8192 slots, runs in any
 // order; joins over idempotent ⊕ do not depend on Δ order) and the last CTA to
 // finish publishes |Δ'| (ctr[0] = rows, ctr[1] = finished CTAs; both reset).
-template <int SEMI, bool ATOMIC>
+template <int SEMI, bool ATOMIC, int WPT>
 __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
                                                          int64_t nw, uint32_t* __restrict__ dkey,
                                                          float* __restrict__ dp, uint32_t* __restrict__ dw,
@@ -523,11 +523,11 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   __shared__ uint32_t s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tile = blockIdx.x;
-  const int64_t w0 = tile * LB_TILE + (int64_t)warp * (32 * LB_WPT);
-  uint32_t m[LB_WPT];
+  const int64_t w0 = tile * (256 * WPT) + (int64_t)warp * (32 * WPT);
+  uint32_t m[WPT];
   uint32_t c = 0;
 #pragma unroll
-  for (int j = 0; j < LB_WPT; ++j) {
+  for (int j = 0; j < WPT; ++j) {
     const int64_t w = w0 + j * 32 + lane;
     m[j] = w < nw ? __ldcg(dirty + w) : 0u;
     c += __popc(m[j]);
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   base = s_base + wtot[warp];
   }
 #pragma unroll 1
-  for (int j = 0; j < LB_WPT; ++j) {
+  for (int j = 0; j < WPT; ++j) {
     const uint32_t mm = m[j];
     const uint32_t cnt = __popc(mm);
     uint32_t inc = cnt;
@@ -884,19 +884,25 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   const int64_t ng = (nt + LB_GROUP - 1) / LB_GROUP;
   uint32_t* tcnt = scratch;
   uint32_t* gsum = scratch ? scratch + nt : nullptr;
-  const unsigned g = (unsigned)nt;
   if (!ctr) {  // slot-ordered Δ': counting pass first
     note_launch();
     dirty_group_count_k<<<(unsigned)ng, 256, 0, st>>>(dirty, nwords, nt, tcnt, gsum);
   }
   note_launch();
-#define LOB_EX(S, A) direct_extract2_k<S, A><<<g, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, total, \
-                                                                  restamp, wmask, ring, seq, ctr)
+  // atomic runs: 4 words per lane (twice the CTAs, shorter per-warp chains) up to
+  // C2-sized bitmaps; 8 beyond, where the per-CTA claim / completion atomics on
+  // one counter would otherwise serialise (C5: 32M words per micro-batch)
+  const bool small = ctr && nwords <= (int64_t(1) << 22);
+  const unsigned g = (unsigned)(small ? (nwords + 1023) / 1024 : nt);
+#define LOB_EX(S, A, W) direct_extract2_k<S, A, W><<<g, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, \
+                                                                  total, restamp, wmask, ring, seq, ctr)
+#define LOB_EXS(S) if (!ctr) LOB_EX(S, false, LB_WPT); else if (small) LOB_EX(S, true, 4); else LOB_EX(S, true, LB_WPT)
   switch (semi) {
-    case S_UNIT: if (ctr) LOB_EX(S_UNIT, true); else LOB_EX(S_UNIT, false); break;
-    case S_MAXMIN: if (ctr) LOB_EX(S_MAXMIN, true); else LOB_EX(S_MAXMIN, false); break;
-    default: if (ctr) LOB_EX(S_MAXMULT, true); else LOB_EX(S_MAXMULT, false); break;
+    case S_UNIT: LOB_EXS(S_UNIT); break;
+    case S_MAXMIN: LOB_EXS(S_MAXMIN); break;
+    default: LOB_EXS(S_MAXMULT); break;
   }
+#undef LOB_EXS
 #undef LOB_EX
 }
 void launch_direct_present(const void* f, int64_t nslots, int semi, uint32_t* flag, cudaStream_t st) {
