@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // copy of the build index replacing boff -> bkey (+3%: boff hits L1), a
 // software pipeline prefetching row i+stride's key and CSR range (+22%),
 // warp-merged dirty-bit updates (__match_any_sync + __reduce_or_sync per
-// direction: +29%, the warp collectives cost more than the REDs they save).
+// direction: +29%, the warp collectives cost more than the REDs they save),
+// and (for join_write_k too) u32 copies of the build keys' free bits (no
+// change on C4, +1% on C2/C3: build rows are L2-resident already).
 #ifndef FJ_MINB
 #define FJ_MINB 6
 #endif
