@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(256) dirty_group_count_k(const uint32_t* __res
 // ATOMIC: one launch, no counting pass — each warp claims its output range with
 // one atomicAdd (Δ' = runs sorted within each warp's 8192 slots, runs in any
 // order; joins over idempotent ⊕ do not depend on Δ order) and the last CTA to
-// finish publishes |Δ'| (ctr[0] = rows, ctr[1] = finished CTAs; both reset).
+// claim publishes |Δ'| (ctr[0] = rows, ctr[1] = CTAs that claimed; both reset).
 template <int SEMI, bool ATOMIC, int WPT>
 __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, uint32_t* __restrict__ dirty,
                                                          int64_t nw, uint32_t* __restrict__ dkey,
@@ -538,6 +538,24 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
     uint32_t wb = 0;
     if (lane == 0 && wsum) wb = atomicAdd(ctr, wsum);
     base = __shfl_sync(0xffffffffu, wb, 0);
+    // |Δ'| is final once every CTA has claimed (writes may still be in flight:
+    // the next kernel is stream-ordered after them), so the last CTA to claim
+    // publishes it and resets the counters — no barrier at the end of the work
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctr);
+        *total = n;
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+        if (ring) {  // zero-copy report to the host (async rounds)
+          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | n;
+          __threadfence_system();
+        }
+      }
+    }
   } else {
   // tile base: groups before this tile's group + this group's earlier tiles
   const int64_t grp = tile / LB_GROUP;
@@ -643,23 +661,6 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
       }
     }
     base += tot;
-  }
-  if constexpr (ATOMIC) {  // the last CTA to finish publishes |Δ'| and resets the counters
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
-        __threadfence();
-        const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctr);
-        *total = n;
-        ctr[0] = 0u;
-        ctr[1] = 0u;
-        if (ring) {
-          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | n;
-          __threadfence_system();
-        }
-      }
-    }
   }
 }
 
