@@ -468,7 +468,7 @@ __device__ __forceinline__ PK lookup_probe(const LookupPlan& lp, int semi, int64
   return k;
 }
 
-template <typename PK>
+template <typename PK, int NM>
 __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pkr, float p0, float& t, uint32_t& w,
                                            uint64_t& key) {
   bool ok = pkr != dead<PK>();
@@ -486,7 +486,7 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
     tags[l + 1] = 1.0f;
     if (l >= lp.nlk || !ok) continue;
     const Lookup& L = lp.lk[l];
-    const uint64_t pre = L.cprefix | apply_moves(L.prem, L.nprem, pk, 0);
+    const uint64_t pre = L.cprefix | (NM ? moves_n<NM>(L.prem, L.nprem, pk, 0) : apply_moves(L.prem, L.nprem, pk, 0));
     int64_t j = -1;
     if (L.boff) {
       if (pre < (uint64_t)L.nprefix) {
@@ -513,9 +513,10 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
     t = pick(lp.tag_order[0]);
 #pragma unroll 1
     for (int k = 1; k < lp.ntag; ++k) t = otimes(semi, t, pick(lp.tag_order[k]));
-    if (semi == S_MAXMULT) w = lp.wconst | (uint32_t)apply_moves(lp.wm, lp.nwm, pk, 0);
+    if (semi == S_MAXMULT)
+      w = lp.wconst | (uint32_t)(NM ? moves_n<NM>(lp.wm, lp.nwm, pk, 0) : apply_moves(lp.wm, lp.nwm, pk, 0));
   }
-  key = lp.cout | apply_moves(lp.om, lp.nom, pk, 0);
+  key = lp.cout | (NM ? moves_n<NM>(lp.om, lp.nom, pk, 0) : apply_moves(lp.om, lp.nom, pk, 0));
   return ok;
 }
 
@@ -554,7 +555,8 @@ __device__ __forceinline__ void agg_flush(void* f, uint32_t* dirty, uint32_t slo
   }
 }
 
-template <typename PK, typename OK, int MODE>
+// NM: 2 when every move list (prefixes, head, witness) has <= 2 moves, else 0 (generic)
+template <typename PK, typename OK, int MODE, int NM>
 __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsigned long long* __restrict__ ncand) {
   constexpr bool DIRECT = MODE >= LC_DIRECT;
   constexpr int SEMI_C = DIRECT ? MODE - LC_DIRECT : -1;
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       float t;
       uint32_t w;
       uint64_t key;
-      const bool ok = lookup_row<PK>(lp, SEMI_C, pkr, p0, t, w, key);
+      const bool ok = lookup_row<PK, NM>(lp, SEMI_C, pkr, p0, t, w, key);
       if (ok) ++mycount;
       const uint32_t slot = (uint32_t)key;
       const unsigned act = __ballot_sync(0xffffffffu, ok);
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       uint32_t w;
       uint64_t key;
       const PK pkr = lookup_probe<PK>(lp, semi, i, p0);
-      const bool ok = lookup_row<PK>(lp, semi, pkr, p0, t, w, key);
+      const bool ok = lookup_row<PK, NM>(lp, semi, pkr, p0, t, w, key);
       if (ok) ++mycount;
       if constexpr (DIRECT) {
         if (ok) direct_oplus(SEMI_C, lp.fdir, (uint32_t)key, t, w, lp.dirty, 0, lp.mx);
@@ -715,12 +717,19 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
   }
 }
 
+template <typename PK, typename OK, int NM>
+static void launch_lookup_chain_m(const LookupPlan& lp, unsigned long long* ncand, int g, cudaStream_t st) {
+  if (!lp.direct) lookup_chain_k<PK, OK, LC_CAND, NM><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.semi == S_UNIT) lookup_chain_k<PK, OK, LC_DIRECT + S_UNIT, NM><<<g, 256, 0, st>>>(lp, ncand);
+  else if (lp.semi == S_MAXMIN) lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMIN, NM><<<g, 256, 0, st>>>(lp, ncand);
+  else lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMULT, NM><<<g, 256, 0, st>>>(lp, ncand);
+}
 template <typename PK, typename OK>
 static void launch_lookup_chain_t(const LookupPlan& lp, unsigned long long* ncand, int g, cudaStream_t st) {
-  if (!lp.direct) lookup_chain_k<PK, OK, LC_CAND><<<g, 256, 0, st>>>(lp, ncand);
-  else if (lp.semi == S_UNIT) lookup_chain_k<PK, OK, LC_DIRECT + S_UNIT><<<g, 256, 0, st>>>(lp, ncand);
-  else if (lp.semi == S_MAXMIN) lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMIN><<<g, 256, 0, st>>>(lp, ncand);
-  else lookup_chain_k<PK, OK, LC_DIRECT + S_MAXMULT><<<g, 256, 0, st>>>(lp, ncand);
+  int nm = std::max(lp.nom, lp.nwm);
+  for (int l = 0; l < lp.nlk; ++l) nm = std::max(nm, lp.lk[l].nprem);
+  if (nm <= 2) launch_lookup_chain_m<PK, OK, 2>(lp, ncand, g, st);
+  else launch_lookup_chain_m<PK, OK, 0>(lp, ncand, g, st);
 }
 
 void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaStream_t st) {
