@@ -278,17 +278,28 @@ struct Ctx {
   struct Phase {
     Ctx* c;
     int id;
-    cudaEvent_t a;
-    Phase(Ctx* cc, int i) : c(cc), id(i) {
+    cudaEvent_t a = nullptr;
+    Phase(Ctx* cc, int i, bool on = true) : c(cc), id(i) {
+      if (!on) return;
       a = c->get_event();
       cudaEventRecord(a, c->st);
     }
     ~Phase() {
+      if (!a) return;
       cudaEvent_t b = c->get_event();
       cudaEventRecord(b, c->st);
       c->ev.push_back({id, {a, b}});
     }
   };
+  // async sections: one event pair around all their rounds; their settle time is
+  // the section's span minus its (individually timed) fused joins — per-launch
+  // event pairs for the extraction would cost ~1 µs of host time each at
+  // finish_run (hundreds per run)
+  struct Section {
+    cudaEvent_t a, b;
+    size_t ev0, ev1;
+  };
+  std::vector<Section> sections;
 
   ~Ctx() {
     for (auto& r : rels) r.reset();
@@ -1382,7 +1393,7 @@ struct Ctx {
     if (semi != S_UNIT) S.dp.reserve(cap);
     {  // Δ' in slot order (two launches); dirty bits cleared, slots re-settled.  Joins read
        // Δ keys and p only (a candidate's witness comes from its own body), so no Δ' witness.
-      Phase ph(this, 3);
+      Phase ph(this, 3, !S.async || log_level >= 2);  // per-round trace keeps them
       launch_direct_extract2(S.dirf.get(), S.dirty.ptr(), nw, semi, S.dkey32.ptr(),
                              semi != S_UNIT ? S.dp.ptr() : nullptr, nullptr,
                              sorted_delta ? arena.get<uint32_t>(direct_extract2_scratch(nw)) : nullptr, S.ndev.ptr(),
@@ -1580,6 +1591,7 @@ struct Ctx {
     ev.clear();
     ev_used = 0;
     marks.clear();
+    sections.clear();
     cudaEvent_t t0 = get_event();
     cudaEventRecord(t0, st);
     mark("start");
@@ -1904,6 +1916,8 @@ struct Ctx {
         if (!first_round && round_other == 0 && round_fused > 0 && strat.size() <= (size_t)AREL && async_ok(strat)) {
           mark("sync rounds");
           async = true;
+          sections.push_back({get_event(), nullptr, ev.size(), 0});
+          cudaEventRecord(sections.back().a, st);
           async_nrel = (int)strat.size();
           for (int r : strat) rels[r]->async = true;
           for (int r : strat) async_nd0 += rels[r]->nd;
@@ -1912,6 +1926,9 @@ struct Ctx {
       }
       mark(async ? "async rounds" : "sync rounds");
       if (async) {
+        sections.back().b = get_event();
+        cudaEventRecord(sections.back().b, st);
+        sections.back().ev1 = ev.size();
         sync();
         if (log_level >= 2 && trace.size() > trace_base + rounds) trace.resize(trace_base + rounds);
         for (int r : strat) {
@@ -1953,9 +1970,12 @@ struct Ctx {
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
     stats.ms_total = ms;
-    for (auto& e : ev) {
+    std::vector<float> evms(ev.size(), 0.0f);
+    for (size_t q = 0; q < ev.size(); ++q) {
+      auto& e = ev[q];
       float m = 0;
       cudaEventElapsedTime(&m, e.second.first, e.second.second);
+      evms[q] = m;
       switch (e.first) {
         case 0: stats.ms_join += m; break;
         case 1: stats.ms_sort += m; break;
@@ -1968,6 +1988,16 @@ struct Ctx {
         default: stats.ms_grad += m; break;
       }
     }
+    for (const Section& sc : sections) {  // async rounds: settle = span - fused joins
+      if (!sc.b || log_level >= 2) continue;  // (LOBSTER_LOG=2 times every settle itself)
+      float span = 0;
+      cudaEventElapsedTime(&span, sc.a, sc.b);
+      double joins = 0;
+      for (size_t q = sc.ev0; q < sc.ev1 && q < ev.size(); ++q)
+        if (ev[q].first == 5) joins += evms[q];
+      stats.ms_merge += std::max(0.0, (double)span - joins);
+    }
+    sections.clear();
     if (log_level >= 1 && marks.size() > 1) {  // GPU timeline sections (includes idle gaps)
       std::string line = "[lobster] timeline ms:";
       for (size_t q = 1; q < marks.size(); ++q) {
