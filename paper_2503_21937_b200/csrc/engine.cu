@@ -826,7 +826,7 @@ struct Ctx {
           ix = static_index(A.rel, order, (int)order.size());
         } else {
           VerData vd = version_data(A.rel, ver[a]);
-          build_index(local_ix, L, order, (int)order.size(), (const uint64_t*)vd.key, vd.p, vd.n, false, false);
+          build_index(local_ix, L, order, (int)order.size(), (const uint64_t*)vd.key, vd.p, vd.n, false, true);
           ix = &local_ix;
         }
         if (ix->n == 0) return;
@@ -949,7 +949,7 @@ struct Ctx {
         ix = static_index(A.rel, iorder, nbound);
       } else {
         VerData vd = version_data(A.rel, ver[ai]);
-        build_index(local_ix, L, iorder, nbound, (const uint64_t*)vd.key, vd.p, vd.n, false, false);
+        build_index(local_ix, L, iorder, nbound, (const uint64_t*)vd.key, vd.p, vd.n, false, true);
         ix = &local_ix;
       }
       if (ix->n == 0) return;
