@@ -71,6 +71,11 @@ __device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int semi, int
     const float a = jp.ptag[0][row], b = jp.btag[j];
     return jp.tag_order[0] == 0 ? otimes(semi, a, b) : otimes(semi, b, a);
   }
+  if (jp.npt == 2 && jp.ntag == 3) {  // three-atom rules (e.g. C3's composition): 3 loads, no scan
+    const float v0 = jp.ptag[0][row], v1 = jp.ptag[1][row], v2 = jp.btag ? jp.btag[j] : 1.0f;
+    auto pick = [&](int idx) { return idx == 0 ? v0 : (idx == 1 ? v1 : v2); };
+    return otimes(semi, otimes(semi, pick(jp.tag_order[0]), pick(jp.tag_order[1])), pick(jp.tag_order[2]));
+  }
   float t = tag_at(jp, jp.tag_order[0], row, j);
 #pragma unroll 1
   for (int k = 1; k < jp.ntag; ++k) t = otimes(semi, t, tag_at(jp, jp.tag_order[k], row, j));
