@@ -126,8 +126,12 @@ typedef struct {
      bounded-fan-out programs): launches, CUDA-event time, probe rows and
      candidates it processed, and its row bytes (key + tag) for §8(d) bytes   */
   int64_t fj_launches, fj_probe_rows, fj_candidates;
-  double ms_fused_join;
+  double ms_fused_join;           /* CUDA-event time of the TIMED fused launches only      */
   int32_t fj_row_bytes, pad0;
+  /* the fused launches timed with CUDA events (every k-th, LOBSTER_JOIN_TIMING_EVERY,
+     default 4) and the probe rows / candidates of exactly those launches: their
+     bytes over ms_fused_join is the kernel's measured throughput                   */
+  int64_t fj_timed_launches, fj_timed_probe_rows, fj_timed_candidates;
 } lobster_run_stats;
 
 /* Evaluate every stratum to fixpoint (termination: no new tuple and no tag whose

@@ -32,7 +32,9 @@ class RunStats(ctypes.Structure):
                 ("ms_grad", ctypes.c_double), ("ms_comm", ctypes.c_double), ("bytes_algorithmic", ctypes.c_int64),
                 ("fj_launches", ctypes.c_int64), ("fj_probe_rows", ctypes.c_int64),
                 ("fj_candidates", ctypes.c_int64), ("ms_fused_join", ctypes.c_double),
-                ("fj_row_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32)]
+                ("fj_row_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("fj_timed_launches", ctypes.c_int64), ("fj_timed_probe_rows", ctypes.c_int64),
+                ("fj_timed_candidates", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -250,6 +250,10 @@ struct Ctx {
   bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
   bool sorted_delta = getenv("LOBSTER_SORTED_DELTA") != nullptr;      // A/B: fully slot-ordered Δ' (2 launches)
   bool eager_compact = getenv("LOBSTER_EAGER_COMPACT") != nullptr;    // A/B: compact direct stores at stratum end
+  // time every k-th fused join launch (LOBSTER_JOIN_TIMING_EVERY, default 4; 1 = all)
+  int join_timing_every = getenv("LOBSTER_JOIN_TIMING_EVERY") ? std::max(1, atoi(getenv("LOBSTER_JOIN_TIMING_EVERY"))) : 4;
+  uint64_t fj_seq = 0;
+  std::set<int> timed_rounds;  // async rounds of the current stratum whose fused join is timed
   int64_t num_facts_db = 0;
   // timing
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -1028,17 +1032,28 @@ struct Ctx {
         merge_moves(jp.prem, jp.nprem);
         merge_moves(jp.om, jp.nom);
         merge_moves(jp.wm, jp.nwm);
+        // every join_timing_every-th launch is timed with a CUDA event pair (its candidates
+        // count into d_ncand[2]): each event pair costs ~4 µs of issue / GPU bubble, ~2.5 ms
+        // per C2 step if every launch were timed
+        const bool timed = (fj_seq++ % join_timing_every) == 0;
         {
-          Phase ph(this, 5);
+          Phase ph(this, 5, timed);
           // async: Δ size unknown here; grid from the last size the host saw (any grid is
           // correct: the kernel strides over the device-side count)
-          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand + 1, st, jp.np_dev ? 8 * async_nd0 + 1 : jp.np);
+          launch_join_rows_direct(jp, (int)ix->maxdeg, d_ncand + (timed ? 2 : 1), st,
+                                  jp.np_dev ? 8 * async_nd0 + 1 : jp.np);
           kcheck("join rows direct");
         }
         stats.fj_launches++;
+        if (timed) stats.fj_timed_launches++;
         round_other--;
         round_fused++;
-        if (!H.async) stats.fj_probe_rows += T.n;
+        if (!H.async) {
+          stats.fj_probe_rows += T.n;
+          if (timed) stats.fj_timed_probe_rows += T.n;
+        } else if (timed) {
+          timed_rounds.insert(cur_round);  // its probe rows are learnt when the previous round drains
+        }
         H.nc += T.n;  // candidates counted on the device (d_ncand[1])
         H.cand_bound += T.n * ix->maxdeg;
         return;
@@ -1586,8 +1601,9 @@ struct Ctx {
     if (!loaded) throw Failure(LOBSTER_E_STATE, "run before program_load");
     if (sticky) throw Failure(LOBSTER_E_CUDA, "context is in a failed state");
     stats = lobster_run_stats{};
-    if (!d_ncand) cuda_check(cudaMalloc(&d_ncand, 16), "cudaMalloc");
-    cuda_check(cudaMemsetAsync(d_ncand, 0, 16, st), "memset");
+    if (!d_ncand) cuda_check(cudaMalloc(&d_ncand, 24), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(d_ncand, 0, 24, st), "memset");
+    fj_seq = 0;
     ev.clear();
     ev_used = 0;
     marks.clear();
@@ -1641,7 +1657,8 @@ struct Ctx {
     }
     batch_cur = B;
     if (micro) finalize_collected();
-    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1);
+    stats.fj_timed_candidates = (int64_t)read_dev(d_ncand + 2);
+    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1) + stats.fj_timed_candidates;
     stats.candidates += (int64_t)read_dev(d_ncand) + stats.fj_candidates;
     stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
     finish_run(t0, round_cap_hit, out);
@@ -1815,6 +1832,7 @@ struct Ctx {
       const int64_t probe = async_nd0;
       async_nd0 = sum;  // Δ' of this round = probe rows of the next
       stats.fj_probe_rows += probe;
+      if (timed_rounds.count(pr)) stats.fj_timed_probe_rows += probe;
       stats.bytes_algorithmic += bytes_round_direct(probe, sum);
       if (log_level >= 2 && trace_base + pr - 1 < trace.size()) {
         trace[trace_base + pr - 1][1] = probe;
@@ -1844,6 +1862,7 @@ struct Ctx {
       bool first = true, first_round = true, async = false;
       int64_t done = 0;
       std::deque<std::pair<int, uint32_t>> pending;  // (round, ring sequence)
+      timed_rounds.clear();
       const size_t trace_base = trace.size();
       async_nd0 = 0;
       for (;;) {
@@ -1981,13 +2000,15 @@ struct Ctx {
         case 1: stats.ms_sort += m; break;
         case 2: stats.ms_reduce += m; break;
         case 3: stats.ms_merge += m; break;
-        case 5:
+        case 5:  // timed fused joins (every join_timing_every-th launch)
           stats.ms_fused_join += m;
-          stats.ms_join += m;
           break;
         default: stats.ms_grad += m; break;
       }
     }
+    // phase total of the fused joins: the timed launches scaled to all launches
+    if (stats.fj_timed_launches)
+      stats.ms_join += stats.ms_fused_join * (double)stats.fj_launches / (double)stats.fj_timed_launches;
     for (const Section& sc : sections) {  // async rounds: settle = span - fused joins
       if (!sc.b || log_level >= 2) continue;  // (LOBSTER_LOG=2 times every settle itself)
       float span = 0;
@@ -1995,7 +2016,8 @@ struct Ctx {
       double joins = 0;
       for (size_t q = sc.ev0; q < sc.ev1 && q < ev.size(); ++q)
         if (ev[q].first == 5) joins += evms[q];
-      stats.ms_merge += std::max(0.0, (double)span - joins);
+      // only every k-th join carries events: the section's join time is estimated as k x
+      stats.ms_merge += std::max(0.0, (double)span - joins * join_timing_every);
     }
     sections.clear();
     if (log_level >= 1 && marks.size() > 1) {  // GPU timeline sections (includes idle gaps)
