@@ -250,7 +250,11 @@ struct Ctx {
   bool force_sort_dedup = getenv("LOBSTER_SORT_DEDUP") != nullptr;    // A/B: radix sort + seg ⊕ on dense
   bool sorted_delta = getenv("LOBSTER_SORTED_DELTA") != nullptr;      // A/B: fully slot-ordered Δ' (2 launches)
   bool eager_compact = getenv("LOBSTER_EAGER_COMPACT") != nullptr;    // A/B: compact direct stores at stratum end
-  // time every k-th fused join launch (LOBSTER_JOIN_TIMING_EVERY, default 4; 1 = all)
+  // time every k-th fused join launch (LOBSTER_JOIN_TIMING_EVERY, default 4; 1 = all).
+  // Other phases keep an event pair per launch: sampling them by round was tried and
+  // rejected — rounds are too uneven (C4: 9 rounds, two of them hold most of the
+  // work), and their sums feed the fixpoint-phase roofline of the non-fused configs.
+  // That timing costs ~2 ms of a 32 ms C3 step and 0.25 ms of C1's 0.95 ms.
   int join_timing_every = getenv("LOBSTER_JOIN_TIMING_EVERY") ? std::max(1, atoi(getenv("LOBSTER_JOIN_TIMING_EVERY"))) : 4;
   uint64_t fj_seq = 0;
   std::set<int> timed_rounds;  // async rounds of the current stratum whose fused join is timed
