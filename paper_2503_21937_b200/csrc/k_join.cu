@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // bit moves for prefix / slot / witness) — the generic kernel was 3.7k SASS
 // instructions and stalled on instruction fetch (ncu: 21% no_instruction).
 // Measured on C2 and rejected: two rows per thread (152 vs 101 us per launch:
-// fewer resident warps for the same requests in flight), a fixed-width ELL
+// fewer resident warps for the same requests in flight; re-measured with the
+// specialised kernel, 8-B paired key/tag loads and all 8 peeks in flight:
+// +30%, 48 registers with spills), a fixed-width ELL
 // copy of the build index replacing boff -> bkey (+3%: boff hits L1), a
 // software pipeline prefetching row i+stride's key and CSR range (+22%),
 // warp-merged dirty-bit updates (__match_any_sync + __reduce_or_sync per
