@@ -66,6 +66,25 @@ def test_mutual_recursion_async_rounds(seed, sr):
     assert stats["rounds_total"] == int(res.rounds.sum())
 
 
+TWO_STRATA_PROGRAM = """
+type edge(x: i32, y: i32)
+rel path(x, y) :- edge(x, y) or (path(x, z) and edge(z, y)).
+rel hop2(x, w) :- path(x, y), edge(y, z), edge(z, w), x != w.
+output hop2
+"""
+
+
+@pytest.mark.parametrize("sr", [0, 1, 3])
+def test_later_stratum_reads_lazily_compacted_store(sr):
+    """A later stratum joins the recursive relation through a general join (a
+    static index over it), so its direct store is compacted on first use."""
+    w = W.random_digraph_workload(20, 0.15, 900 + sr, sr, batch=3, program=TWO_STRATA_PROGRAM)
+    eng, stats, res = run_both(w, outputs=["hop2", "path"])
+    assert_parity(eng, res, "hop2", sr)
+    assert_parity(eng, res, "path", sr, check_grads=False)
+    assert stats["rounds_total"] == int(res.rounds.sum())
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_dag_addmult(seed):
     w = W.random_dag_workload(30, 0.2, 50 + seed, 2, batch=4)
