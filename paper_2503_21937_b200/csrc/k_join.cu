@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
 constexpr int LC_CAND = 0, LC_DIRECT = 1;
 
 // One probe row of a lookup chain: filters, point lookups, ⊗ in body order,
-// witness and head key.  Returns whether the row yields a candidate.
+// witness and head key.  Returns whether the row yields a candidate.  (A
+// per-prefix tag table replacing the offsets -> tag loads of a point lookup
+// was measured on C2's endpoints_connected: no change — not load-bound.)
 // probe row i: its key and tag, from the probe arrays or (pdir) a direct store's
 // slot word (slot i present <=> row exists; key = slot)
 template <typename PK>
