@@ -304,7 +304,11 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // warp-merged dirty-bit updates (__match_any_sync + __reduce_or_sync per
 // direction: +29%, the warp collectives cost more than the REDs they save),
 // and (for join_write_k too) u32 copies of the build keys' free bits (no
-// change on C4, +1% on C2/C3: build rows are L2-resident already).
+// change on C4, +1% on C2/C3: build rows are L2-resident already), and a
+// window variant for TC-shaped heads (the CTA's 256 rows max-reduce their
+// candidates over two 1024-slot shared-memory windows, one global update per
+// touched slot: +49% — the zero / flush passes and two barriers per 256 rows
+// cost more than the global operations saved).
 #ifndef FJ_MINB
 #define FJ_MINB 6
 #endif
