@@ -143,9 +143,11 @@ __device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slo
 }
 
 __device__ __forceinline__ unsigned long long direct_peek(int semi, const void* f, uint32_t slot) {
-  if (semi == S_UNIT) return __ldcg(reinterpret_cast<const uint32_t*>(f) + (slot >> 5));
-  if (semi == S_MAXMIN) return __ldcg(reinterpret_cast<const uint32_t*>(f) + slot);
-  return __ldcg(reinterpret_cast<const unsigned long long*>(f) + slot);
+  // through L1 (ld.ca): L1 holds no line from before this launch, so a hit is
+  // still a lower bound of the slot's round-start value
+  if (semi == S_UNIT) return __ldca(reinterpret_cast<const uint32_t*>(f) + (slot >> 5));
+  if (semi == S_MAXMIN) return __ldca(reinterpret_cast<const uint32_t*>(f) + slot);
+  return __ldca(reinterpret_cast<const unsigned long long*>(f) + slot);
 }
 
 template <int N>
