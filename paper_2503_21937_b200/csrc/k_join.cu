@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
 // +30%, 48 registers with spills), a fixed-width ELL
 // copy of the build index replacing boff -> bkey (+3%: boff hits L1), a
 // software pipeline prefetching row i+stride's key and CSR range (+22%),
+// grids other than one wave of resident CTAs in async rounds (2 or 4 waves:
+// +7% / +15%; 4 or 3 CTAs per SM: +8% / +24%),
 // warp-merged dirty-bit updates (__match_any_sync + __reduce_or_sync per
 // direction: +29%, the warp collectives cost more than the REDs they save),
 // and (for join_write_k too) u32 copies of the build keys' free bits (no
