@@ -2161,15 +2161,43 @@ struct Ctx {
       }
       int64_t* cnt = arena.get<int64_t>(n);
       int64_t* loff = arena.get<int64_t>(n + 1);
-      launch_walk(T, r, n, 0, nullptr, cnt, nullptr, d_err, st);
-      exclusive_scan<int64_t>(cnt, loff, n, loff + n, arena.alloc(scan_tmp_bytes<int64_t>(n)), st);
-      kcheck("walk");
-      const int64_t nleaf = read_dev(loff + n);
-      const int e = read_dev(d_err);
-      if (e) throw Failure(LOBSTER_E_CUDA, "witness walk failed (code " + std::to_string(e) + ")");
+      // Proofs whose pending IDB atoms outgrow the in-register stack (deep
+      // non-linear trees; linear recursion never does) are re-walked with a
+      // global spill region per thread, doubling it until every stack fits.
+      uint64_t* gkey = nullptr;
+      int* grel = nullptr;
+      int64_t gcap = 0, gthreads = 0;
+      auto free_spill = [&]() {
+        if (gkey) cudaFreeAsync(gkey, st);
+        if (grel) cudaFreeAsync(grel, st);
+        gkey = nullptr;
+        grel = nullptr;
+      };
+      int64_t nleaf = 0;
+      for (;;) {
+        launch_walk(T, r, n, 0, nullptr, cnt, nullptr, d_err, gkey, grel, gcap, gthreads, st);
+        exclusive_scan<int64_t>(cnt, loff, n, loff + n, arena.alloc(scan_tmp_bytes<int64_t>(n)), st);
+        kcheck("walk");
+        nleaf = read_dev(loff + n);
+        const int e = read_dev(d_err);
+        if (e == 0) break;
+        if (e & ~2) { free_spill(); throw Failure(LOBSTER_E_CUDA, "witness walk failed (code " + std::to_string(e) + ")"); }
+        free_spill();
+        gcap = gcap ? 2 * gcap : 1024;
+        gthreads = std::min<int64_t>(n, 148 * 64);
+        while (gthreads > 148 && gthreads * gcap * 12 > ((int64_t)1 << 30)) gthreads /= 2;
+        if (gthreads * gcap * 12 > ((int64_t)4 << 30)) {
+          throw Failure(LOBSTER_E_RANGE, "witness walk: a proof needs more than " + std::to_string(gcap / 2) +
+                                             " pending IDB atoms");
+        }
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&gkey), gthreads * gcap * 8, st), "walk spill");
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&grel), gthreads * gcap * 4, st), "walk spill");
+        cuda_check(cudaMemsetAsync(d_err, 0, sizeof(int), st), "memset");
+      }
       uint64_t* k0 = arena.get<uint64_t>(nleaf);
       uint64_t* k1 = arena.get<uint64_t>(nleaf);
-      launch_walk(T, r, n, 1, loff, nullptr, reinterpret_cast<int64_t*>(k0), d_err, st);
+      launch_walk(T, r, n, 1, loff, nullptr, reinterpret_cast<int64_t*>(k0), d_err, gkey, grel, gcap, gthreads, st);
+      free_spill();
       // leaf keys: tuple << 32 | fact, sorted -> unique (tuple, fact) runs
       tag_leaves(k0, loff, n, nleaf);
       const int tbits = 32 + bits_for((uint64_t)n);

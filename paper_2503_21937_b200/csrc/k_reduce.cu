@@ -897,7 +897,11 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
   // one counter would otherwise serialise (C5: 32M words per micro-batch)
   const bool small = ctr && nwords <= (int64_t(1) << 22);
   // words per lane on C2-sized bitmaps: 2 (measured 1% faster than 4 on C2, equal on C4)
-  const int swpt = getenv("LOBSTER_EX_WPT") ? atoi(getenv("LOBSTER_EX_WPT")) : 2;
+  // (LOBSTER_EX_WPT=4 selects the other instantiated width; read once, anything else = 2)
+  static const int swpt = [] {
+    const char* e = getenv("LOBSTER_EX_WPT");
+    return (e && atoi(e) == 4) ? 4 : 2;
+  }();
   const unsigned g = (unsigned)(small ? (nwords + 256 * swpt - 1) / (256 * swpt) : nt);
 #define LOB_EX(S, A, W) direct_extract2_k<S, A, W><<<g, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, \
                                                                   total, restamp, wmask, ring, seq, ctr)

@@ -13,7 +13,14 @@
 namespace lob {
 namespace {
 
-constexpr int STACK = 64;
+// Pending IDB atoms of the walk.  Input atoms are leaves and are emitted the
+// moment their key is known, so only IDB atoms are pushed: linear recursion
+// (path :- path, edge) keeps one entry whatever the proof length, and a tree of
+// height h with b IDB atoms per rule needs at most h·(b−1)+1.  The bottom STACK
+// entries live in registers / local memory; deeper entries spill to a global
+// per-thread region (gstack, gcap entries per thread) when the host provides
+// one — the retry after a pass reports err bit 2.
+constexpr int STACK = 32;
 
 __device__ int64_t find_key(const WalkRel& R, uint64_t k) {
   if (R.off) {
@@ -27,70 +34,89 @@ __device__ int64_t find_key(const WalkRel& R, uint64_t k) {
   return (i < R.n && R.key[i] == k) ? i : -1;
 }
 
+__device__ __forceinline__ int64_t emit_leaf(const WalkRel& A, uint64_t key, int pass, int64_t* leaves,
+                                             int64_t out, int64_t count, int* err) {
+  const int64_t idx = find_key(A, key);
+  if (idx < 0) { atomicOr(err, 1); return -1; }
+  if (pass) leaves[out + count] = (int64_t)A.fid[idx];
+  return count + 1;
+}
+
 __global__ void walk_k(const WalkTables T, int rel0, int64_t n, int pass, const int64_t* __restrict__ offs,
-                       int64_t* __restrict__ cnt, int64_t* __restrict__ leaves, int* __restrict__ err) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  int srel[STACK];
-  uint64_t skey[STACK];
-  int sp = 0;
-  srel[sp] = rel0;
-  skey[sp] = T.rels[rel0].key[t];
-  ++sp;
-  int64_t count = 0;
-  const int64_t out = pass ? offs[t] : 0;
-  int32_t val[16];
-  while (sp > 0) {
-    --sp;
-    const int r = srel[sp];
-    const uint64_t k = skey[sp];
-    const WalkRel& R = T.rels[r];
-    uint32_t w;
-    if (R.dir && !R.input) {  // direct store still holds the final words: slot = packed key
-      const unsigned long long word = R.dir[k];
-      if (!word) { atomicOr(err, 1); return; }
-      const unsigned long long wc = ~word & R.wmask;
-      const unsigned long long vars = wc & ((1ull << R.wT) - 1ull);
-      w = (uint32_t)(R.wrb ? (((wc >> R.wT) << (32 - R.wrb)) | vars) : vars);
-    } else {
-      const int64_t idx = find_key(R, k);
-      if (idx < 0) { atomicOr(err, 1); return; }
-      if (R.input) {
-        if (pass) leaves[out + count] = (int64_t)R.fid[idx];
-        ++count;
-        continue;
-      }
-      w = R.w[idx];
-    }
-    const int rb = T.rule_bits[r];
-    const int lr = rb ? (int)(w >> (32 - rb)) : 0;
-    const WalkRule& ru = T.rules[T.rule_base[r] + lr];
-    const uint64_t sample = R.has_sample ? (k >> R.sshift) : 0ull;
-    for (int v = 0; v < ru.nvars && v < 16; ++v) {
-      const int hc = ru.head_col[v];
-      if (hc >= 0) {
-        val[v] = (int32_t)((k >> R.shift[hc]) & bmask(R.bits[hc])) + R.min[hc];
-      } else {
-        val[v] = (int32_t)((w >> ru.wshift[v]) & bmask(ru.wbits[v])) + ru.wmin[v];
-      }
-    }
-    for (int a = ru.natoms - 1; a >= 0; --a) {
-      const WalkAtom& at = ru.atom[a];
-      const WalkRel& A = T.rels[at.rel];
-      uint64_t key = A.has_sample ? (sample << A.sshift) : 0ull;
-      for (int c = 0; c < at.ncols; ++c) {
-        const int32_t x = at.var[c] >= 0 ? val[at.var[c]] : at.cst[c];
-        const int64_t f = (int64_t)x - (int64_t)A.min[c];
-        if (f < 0 || f > (int64_t)bmask(A.bits[c])) { atomicOr(err, 4); return; }
-        key |= (uint64_t)f << A.shift[c];
-      }
-      if (sp >= STACK) { atomicOr(err, 2); return; }
-      srel[sp] = at.rel;
-      skey[sp] = key;
+                       int64_t* __restrict__ cnt, int64_t* __restrict__ leaves, int* __restrict__ err,
+                       uint64_t* __restrict__ gkey, int* __restrict__ grel, int64_t gcap) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // without a spill region: one thread per tuple; with one: grid-stride, the
+  // region indexed by the thread
+  const int64_t step = gkey ? (int64_t)gridDim.x * blockDim.x : n;
+  for (int64_t t = tid; t < n; t += step) {
+    int srel[STACK];
+    uint64_t skey[STACK];
+    int64_t sp = 0;
+    auto push = [&](int r, uint64_t k) -> bool {
+      if (sp < STACK) { srel[sp] = r; skey[sp] = k; }
+      else if (gkey && sp - STACK < gcap) { gkey[tid * gcap + sp - STACK] = k; grel[tid * gcap + sp - STACK] = r; }
+      else return false;
       ++sp;
+      return true;
+    };
+    int64_t count = 0;
+    const int64_t out = pass ? offs[t] : 0;
+    bool ok = push(rel0, T.rels[rel0].key[t]);
+    int32_t val[16];
+    while (ok && sp > 0) {
+      --sp;
+      int r;
+      uint64_t k;
+      if (sp < STACK) { r = srel[sp]; k = skey[sp]; }
+      else { r = grel[tid * gcap + sp - STACK]; k = gkey[tid * gcap + sp - STACK]; }
+      const WalkRel& R = T.rels[r];
+      uint32_t w;
+      if (R.dir && !R.input) {  // direct store still holds the final words: slot = packed key
+        const unsigned long long word = R.dir[k];
+        if (!word) { atomicOr(err, 1); return; }
+        const unsigned long long wc = ~word & R.wmask;
+        const unsigned long long vars = wc & ((1ull << R.wT) - 1ull);
+        w = (uint32_t)(R.wrb ? (((wc >> R.wT) << (32 - R.wrb)) | vars) : vars);
+      } else {
+        const int64_t idx = find_key(R, k);
+        if (idx < 0) { atomicOr(err, 1); return; }
+        w = R.w[idx];
+      }
+      const int rb = T.rule_bits[r];
+      const int lr = rb ? (int)(w >> (32 - rb)) : 0;
+      const WalkRule& ru = T.rules[T.rule_base[r] + lr];
+      const uint64_t sample = R.has_sample ? (k >> R.sshift) : 0ull;
+      for (int v = 0; v < ru.nvars && v < 16; ++v) {
+        const int hc = ru.head_col[v];
+        if (hc >= 0) {
+          val[v] = (int32_t)((k >> R.shift[hc]) & bmask(R.bits[hc])) + R.min[hc];
+        } else {
+          val[v] = (int32_t)((w >> ru.wshift[v]) & bmask(ru.wbits[v])) + ru.wmin[v];
+        }
+      }
+      for (int a = ru.natoms - 1; a >= 0; --a) {
+        const WalkAtom& at = ru.atom[a];
+        const WalkRel& A = T.rels[at.rel];
+        uint64_t key = A.has_sample ? (sample << A.sshift) : 0ull;
+        for (int c = 0; c < at.ncols; ++c) {
+          const int32_t x = at.var[c] >= 0 ? val[at.var[c]] : at.cst[c];
+          const int64_t f = (int64_t)x - (int64_t)A.min[c];
+          if (f < 0 || f > (int64_t)bmask(A.bits[c])) { atomicOr(err, 4); return; }
+          key |= (uint64_t)f << A.shift[c];
+        }
+        if (A.input) {
+          count = emit_leaf(A, key, pass, leaves, out, count, err);
+          if (count < 0) return;
+        } else if (!push(at.rel, key)) {
+          ok = false;
+          break;
+        }
+      }
     }
+    if (!ok) { atomicOr(err, 2); if (!pass) cnt[t] = 0; continue; }
+    if (!pass) cnt[t] = count;
   }
-  if (!pass) cnt[t] = count;
 }
 
 // One thread per output tuple: leaves sorted by (tuple << 32 | fact); unique
@@ -214,10 +240,12 @@ void launch_sample_offsets_i32(const int32_t* sid, int64_t n, int32_t batch, int
 }
 
 void launch_walk(const WalkTables& T, int rel, int64_t n, int pass, const int64_t* offs, int64_t* cnt,
-                 int64_t* leaves, int* err, cudaStream_t st) {
+                 int64_t* leaves, int* err, uint64_t* gkey, int* grel, int64_t gcap, int64_t gthreads,
+                 cudaStream_t st) {
   if (n <= 0) return;
   note_launch();
-  walk_k<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(T, rel, n, pass, offs, cnt, leaves, err);
+  const int64_t thr = gkey ? std::min<int64_t>(n, gthreads) : n;
+  walk_k<<<(unsigned)((thr + 127) / 128), 128, 0, st>>>(T, rel, n, pass, offs, cnt, leaves, err, gkey, grel, gcap);
 }
 
 void launch_leaf_heads(const uint64_t* k, int64_t n, uint32_t* flag, cudaStream_t st) { launch_heads(k, n, flag, st); }
@@ -232,9 +260,9 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
 
 void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,
                    const uint8_t* bits, const int32_t* mins, int32_t* sample, int32_t* cols, cudaStream_t st) {
-  if (n > 0)
-    note_launch();
-    unpack_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, has_sample, sshift, ncols, shift, bits, mins, sample, cols);
+  if (n <= 0) return;
+  note_launch();
+  unpack_k<<<grid_for(n, 256), 256, 0, st>>>(key, n, has_sample, sshift, ncols, shift, bits, mins, sample, cols);
 }
 
 void launch_sample_offsets(const uint64_t* key, int64_t n, int32_t batch, uint8_t sshift, int has_sample,

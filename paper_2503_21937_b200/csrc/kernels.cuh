@@ -355,9 +355,13 @@ struct WalkTables {
   int* rule_bits;       // per relation: witness bits taken by the rule index
   int nrels;
 };
-// pass 0: count leaves per tuple; pass 1: write leaf fact ids at offs
+// pass 0: count leaves per tuple; pass 1: write leaf fact ids at offs.
+// gkey/grel (nullable): spill region of gcap entries per thread for stacks
+// deeper than the in-register part; with it the launch is gthreads threads,
+// grid-stride.  err bit 2 = a stack overflowed (cnt of that tuple is 0).
 void launch_walk(const WalkTables& T, int rel, int64_t n, int pass, const int64_t* offs, int64_t* cnt,
-                 int64_t* leaves, int* err, cudaStream_t st);
+                 int64_t* leaves, int* err, uint64_t* gkey, int* grel, int64_t gcap, int64_t gthreads,
+                 cudaStream_t st);
 // grads from sorted (tuple, fact) leaves: unique facts with multiplicity
 void launch_leaf_heads(const uint64_t* k, int64_t n, uint32_t* flag, cudaStream_t st);
 void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, int64_t nuniq, const float* fact_p,

@@ -103,6 +103,7 @@ class Engine:
         o.micro_batch = micro_batch
         self.batch_size = batch_size
         self.semiring = semiring
+        self.device = device
         h = ctypes.c_void_p()
         rc = self._L.lobster_create(ctypes.byref(o), ctypes.byref(h))
         if rc != 0:
@@ -195,7 +196,7 @@ class Engine:
                 out.grad_values = _np_view(o.grad_values, ng, np.float32, copy)
             return out
         import torch
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = torch.device("cuda", self.device)
 
         def t(ptr, shape, ts):
             if not ptr or 0 in shape:

@@ -1,0 +1,133 @@
+"""GPU parity on long proofs and at full size.
+
+* Linear recursion with proofs far longer than any fixed stack: a 200-node
+  chain and a 32x32 lattice with `output path` under diff-max-mult (proof
+  lengths up to 199 / >= 62 hops, P:126-128 gradients through the witnesses).
+* Non-linear recursion whose witness walk keeps one pending IDB atom per
+  level (depth ~ chain length): exercises the global spill of walk_k.
+* Full-size C2 under max-min (half of the headline) on sampled samples.
+* Full-size C5 (4096 samples, auto micro-batched, 8-words-per-lane Δ'
+  extraction) against the oracle on two samples, bit-exact with proofs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.gpu_util import assert_parity, engine_run, run_both
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_21937_b200 import build
+    build()
+    oracle.build()
+
+
+def _chain(n, probs, batch=1):
+    src = np.arange(n - 1, dtype=np.int32)
+    dst = src + 1
+    return W.Facts([np.tile(src, batch), np.tile(dst, batch)],
+                   np.repeat(np.arange(batch, dtype=np.int32), n - 1), np.tile(probs, batch).astype(np.float32))
+
+
+def test_chain_200_output_path_maxmult():
+    """Every path(0, k) proof is the k-edge chain prefix: proofs of 1..199 hops."""
+    rng = np.random.default_rng(5)
+    n = 200
+    f = _chain(n, rng.uniform(0.9, 1.0, n - 1), batch=2)
+    w = W.Workload("chain", W.PATH_PROGRAM, 3, 2, {"edge": f})
+    eng, stats, res = run_both(w, outputs=["path"])
+    assert assert_parity(eng, res, "path", 3) == 2 * n * (n - 1) // 2
+    o = eng.output("path")
+    assert int(np.max(np.diff(o.grad_offsets))) == n - 1
+
+
+STEP_FIRST = """
+type edge(x: i32, y: i32)
+rel step(x, y) :- edge(x, y).
+rel path(x, y) :- step(x, y) or (path(z, y) and step(x, z)).
+output path
+"""
+
+
+@pytest.mark.parametrize("n", [40, 120])
+def test_idb_leaves_deep_walk_spills(n):
+    """`step` is IDB (an earlier stratum), so the walk pushes it; the body
+    order visits path(z, y) first and leaves step(x, z) pending at every level:
+    a stack of ~n entries, past the in-register part (32)."""
+    rng = np.random.default_rng(n)
+    f = _chain(n, rng.uniform(0.9, 1.0, n - 1))
+    w = W.Workload("chain_step", STEP_FIRST, 3, 1, {"edge": f})
+    eng, stats, res = run_both(w, outputs=["path"])
+    assert assert_parity(eng, res, "path", 3) == n * (n - 1) // 2
+
+
+def test_lattice_32_output_path_maxmult():
+    """One C2 sample with every `path` tuple's gradient (proofs >= 62 hops for
+    far corners of the grid)."""
+    w = W.grid_workload(32, 1, 2, 3, program=W.PATH_PROGRAM)
+    eng, stats, res = run_both(w, outputs=["path"])
+    assert assert_parity(eng, res, "path", 3) == 32 ** 4
+    o = eng.output("path")
+    assert int(np.max(np.diff(o.grad_offsets))) >= 62
+
+
+def test_c2_full_size_maxmin_sampled():
+    """Full C2 batch (64 x 32x32) under max-min-prob; the oracle recomputes
+    samples 5 and 63."""
+    w = W.c2_workload(semiring=1)
+    samples = [5, 63]
+    eng, stats, _ = engine_run(w)
+    res = oracle.run(w.program, 1, w.batch_size, w.facts, outputs=["path", "endpoints_connected"],
+                     samples=samples)
+    assert_parity(eng, res, "path", 1, samples=samples)
+    assert_parity(eng, res, "endpoints_connected", 1, samples=samples)
+    assert stats["tuples_derived"] == 64 * 32 ** 4 + 64
+
+
+def test_c5_full_size_two_samples_bit_exact():
+    """The whole C5 batch (4096 x 64x64, micro-batched automatically) on one
+    GPU; samples 0 and 4095 recomputed by the oracle: tags bit-exact, proofs
+    exact, gradients within 1e-6."""
+    w = W.c5_workload()
+    eng, stats, _ = engine_run(w)
+    samples = [0, 4095]
+    sub = W.c5_workload(samples=samples)
+    res = oracle.run(sub.program, 3, sub.batch_size, sub.facts, outputs=["endpoints_connected"],
+                     samples=samples, threads=2)
+    # the oracle's fact ids are those of the two-sample push; map the GPU's
+    # global ids (full push order: all edges, then all endpoints) onto them
+    o = eng.output("endpoints_connected")
+    assert o.n == 4096
+    full_e, full_p = w.facts["edge"], w.facts["is_endpoint"]
+    sub_e = sub.facts["edge"]
+    ne_full = full_e.n
+    ne_per = sub_e.n // 2
+    np_per = sub.facts["is_endpoint"].n // 2
+
+    def to_sub(fid, s, j):
+        if fid < ne_full:  # edge of sample s: global offset s * ne_per
+            return j * ne_per + (fid - s * ne_per)
+        return sub_e.n + j * np_per + (fid - ne_full - s * np_per)
+
+    r = res.relations["endpoints_connected"]
+    for j, s in enumerate(samples):
+        i = int(np.nonzero(o.sample_ids == s)[0][0])
+        assert o.probs[i].view(np.uint32) == r.tags[j].view(np.uint32)
+        a, b = o.grad_offsets[i], o.grad_offsets[i + 1]
+        c, d = r.grad_offsets[j], r.grad_offsets[j + 1]
+        mapped = np.array([to_sub(int(f), s, j) for f in o.grad_fact_ids[a:b]])
+        order = np.argsort(mapped, kind="stable")
+        assert np.array_equal(mapped[order], r.grad_fact_ids[c:d])
+        gv = o.grad_values[a:b][order].astype(np.float64)
+        ov = r.grad_values[c:d].astype(np.float64)
+        assert np.max(np.abs(gv - ov) / np.maximum(np.abs(ov), 1e-30)) <= 1e-6
+    assert full_p.n == 4096 * 4096
