@@ -48,7 +48,14 @@
 
 namespace orc {
 
-enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3 };
+enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3, DMAX_MIN = 4 };
+
+// Semirings whose tag carries a witness (rule + non-head variables of the
+// winning derivation) and whose ⊕ is max with strict improvement:
+// diff-max-mult-prob (SURVEY §8(c) point 7) and diff-max-min-prob (§3.5
+// "the differentiable versions of the probabilistic semirings"; DESIGN.md
+// reading "diff-max-min").
+static bool witnessed(int sr) { return sr == MAX_MULT || sr == DMAX_MIN; }
 
 static const int MAXA = 8;  // max arity / max non-head variables in the oracle
 
@@ -91,6 +98,7 @@ struct Tag {
 static float otimes(int sr, float a, float b) {
   switch (sr) {
     case MAX_MIN: return a < b ? a : b;       // min
+    case DMAX_MIN: return a < b ? a : b;      // min (diff-max-min-prob)
     case ADD_MULT: return a * b;              // ×  (compiled with -ffp-contract=off)
     case MAX_MULT: return a * b;              // ×
     default: return 1.0f;                     // unit: ∧ of true facts
@@ -107,6 +115,7 @@ static Tag oplus_state(int sr, const Tag& s, const Tag& b) {
     case MAX_MIN: { Tag r = s; if (b.p > s.p) r.p = b.p; return r; }
     case ADD_MULT: { Tag r = s; r.p = (float)((double)s.p + (double)b.p); return r; }
     case MAX_MULT: return (b.p > s.p) ? b : s;
+    case DMAX_MIN: return (b.p > s.p) ? b : s;
     default: return s;
   }
 }
@@ -388,7 +397,7 @@ struct Engine {
   std::map<std::pair<const Rel*, std::vector<int>>, std::map<Tuple, std::vector<const Entry*>>> shared_idx;
 
   Engine(const std::string& text, int semiring, int b) : prog(parse_program(text)), sr(semiring), batch(b < 1 ? 1 : b) {
-    if (semiring < 0 || semiring > 3) throw Err(E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 4) throw Err(E_INVALID_ARG, "bad semiring");
   }
 
   void push(const std::string& rel, int64_t n, const int32_t* cols, const int32_t* sids, const float* probs, int64_t* first) {
@@ -428,7 +437,7 @@ struct Engine {
     Tag& g = it->second;
     if (sr == ADD_MULT) g.p = (float)((double)g.p + (double)p);
     else if (sr == MAX_MIN) { if (p > g.p) g.p = p; }
-    else if (sr == MAX_MULT) { if (p > g.p || (p == g.p && fid < g.fact)) { g.p = p; g.fact = fid; } }
+    else if (witnessed(sr)) { if (p > g.p || (p == g.p && fid < g.fact)) { g.p = p; g.fact = fid; } }
   }
 
   void run(const std::vector<int>& samples, int threads) {
@@ -645,7 +654,7 @@ struct Engine {
             for (j = i; j < c.size() && c[j].head == c[i].head; ++j) {
               if (sr == ADD_MULT) acc += (double)c[j].p;
               else if (sr == MAX_MIN) { if (c[j].p > u.p) u.p = c[j].p; }
-              else if (sr == MAX_MULT) { if (c[j].p > u.p) { u.p = c[j].p; u.rule = c[j].rule; u.wv = c[j].wv; } }
+              else if (witnessed(sr)) { if (c[j].p > u.p) { u.p = c[j].p; u.rule = c[j].rule; u.wv = c[j].wv; } }
             }
             if (sr == ADD_MULT) u.p = (float)acc;
             if (sr == UNIT) u.p = 1.0f;
@@ -667,7 +676,7 @@ struct Engine {
       d.rounds.push_back(rounds);
       d.cands.push_back(cands);
     }
-    if (sr == MAX_MULT) gradients(d);
+    if (witnessed(sr)) gradients(d);
   }
 
   // Witness walk (SURVEY §8(c) point 7): multiset {f: m_f} of the winning
@@ -699,6 +708,15 @@ struct Engine {
         std::map<int64_t, int> mult;
         walk(d, kv.first, e.first, mult, 0);
         std::vector<std::pair<int64_t, float>> g;
+        if (sr == DMAX_MIN) {
+          // p = min over the derivation's leaves: ∂p/∂p_f = 1 for the leaf
+          // holding the minimum (ties: the smallest fact id), 0 elsewhere
+          int64_t arg = -1;
+          for (auto& f : mult) if (arg < 0 || fact_p[f.first] < fact_p[arg]) arg = f.first;
+          if (arg >= 0) g.push_back({arg, 1.0f});
+          gl.push_back(g);
+          continue;
+        }
         for (auto& f : mult) {
           double v = (double)f.second * std::pow((double)fact_p[f.first], f.second - 1);
           for (auto& h : mult) if (h.first != f.first) v *= std::pow((double)fact_p[h.first], h.second);

@@ -261,3 +261,60 @@ def test_constants_eq_repeated_vars(oracle_lib, sr, seed):
                 assert abs(got[k] - v) <= 2.0 ** -23 * abs(v), (rel, k)
             else:
                 assert got[k] == v, (rel, k, got[k], v)
+
+
+# ---------------------------------------------------------------------------
+# diff-max-min-prob (NEXT-4; §3.5): tags = max-min, one-hot gradient
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", range(6))
+def test_diff_maxmin_tags_equal_floyd_warshall(oracle_lib, seed):
+    """The tag is the bottleneck value (Floyd–Warshall max-min, exact); the
+    gradient is one-hot on an input fact whose p equals the tag."""
+    n = 14
+    w = W.random_digraph_workload(n, 0.2, 1200 + seed, 4, self_loops=bool(seed % 2))
+    src, dst, p, _ = refs.edge_lists(w)
+    A = refs.floyd_warshall(n, src, dst, p, "maxmin")
+    reach = refs.floyd_warshall(n, src, dst, p, "bool")
+    rel = oracle.run_workload(w).relations["path"]
+    got = _dict(rel)
+    assert set(got) == {(0, int(a), int(b)) for a, b in zip(*np.nonzero(reach))}
+    for i, (s, a, b) in enumerate(zip(rel.sample_ids, rel.cols[:, 0], rel.cols[:, 1])):
+        assert float(rel.tags[i]) == A[a, b]
+        g = _grad(rel, i)
+        assert list(g.values()) == [1.0]
+        (f,) = g
+        assert float(p[f]) == float(rel.tags[i])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_diff_maxmin_forward_differences(oracle_lib, seed):
+    """Distinct probabilities: raising the gradient's fact by h raises the tag
+    by h; raising any other fact leaves it unchanged (forward differences)."""
+    rng = np.random.default_rng(1300 + seed)
+    w = W.random_dag_workload(8, 0.45, 1300 + seed, 4)
+    f = w.facts["edge"]
+    f.probs = rng.permutation(np.linspace(0.2, 0.9, f.n)).astype(np.float32)
+    base = oracle.run_workload(w).relations["path"]
+    keys = [tuple(int(v) for v in c) for c in base.cols]
+    h = np.float32(2.0 ** -12)
+    for fid in range(f.n):
+        plus = f.probs.copy()
+        plus[fid] += h
+        tp = _dict(oracle.run(w.program, 4, 1, {"edge": W.Facts(f.cols, f.sample_ids, plus)}).relations["path"])
+        for i, k in enumerate(keys):
+            d = tp[(0,) + k] - float(base.tags[i])
+            exp = float(h) if _grad(base, i).get(fid) == 1.0 else 0.0
+            assert d == pytest.approx(exp, abs=1e-7), (k, fid, d)
+
+
+def test_diff_maxmin_c1_golden(oracle_lib):
+    """C1 worked example: diff-max-min tags are the max-min column of the
+    golden table; the gradient names the bottleneck edge of the witnessed path."""
+    from tests.test_oracle_pins import _load_golden
+    E, R, T, G = _load_golden()
+    rel = oracle.run_workload(W.c1_workload(4)).relations["path"]
+    for i, c in enumerate(rel.cols):
+        k = (int(c[0]), int(c[1]))
+        assert float(rel.tags[i]) == T[k][1]
+        (fid,) = _grad(rel, i)
+        assert E[fid][2] == T[k][1]
