@@ -41,13 +41,14 @@ UNIT = "tuples/s"
 
 
 def _rank_batch(make, per_gpu, rank):
-    """This rank's samples (global ids per_gpu*rank ...), pushed with local ids."""
+    """This rank's samples with their GLOBAL ids [per_gpu*rank, per_gpu*(rank+1))
+    (the shard the library assigns to `rank` of a per_gpu*world batch)."""
     samples = list(range(per_gpu * rank, per_gpu * (rank + 1)))
     w = make(per_gpu * (rank + 1), samples)
-    for f in w.facts.values():
-        if f.sample_ids is not None and "samples" in (w.meta or {}):
-            f.sample_ids = (np.asarray(f.sample_ids) - per_gpu * rank).astype(np.int32)
-    w.batch_size = per_gpu
+    lo = per_gpu * rank
+    for f in w.facts.values():  # generators without a sample selector (C1) start at 0
+        if f.sample_ids is not None and f.n and int(np.min(f.sample_ids)) < lo:
+            f.sample_ids = (np.asarray(f.sample_ids) + lo).astype(np.int32)
     return w
 
 
@@ -82,7 +83,22 @@ def parse():
     ap.add_argument("--impl", default="lobster", choices=["lobster", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--serial", action="store_true",
+                    help="run the config's semiring fixpoints one after another instead of on two streams")
     return ap.parse_args()
+
+
+def spawn_ranks(n):
+    """`--gpus N` without a torchrun environment: launch N ranks of this script
+    (one per GPU) through torch.distributed.run on 127.0.0.1 and wait."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -185,12 +201,25 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------ cpu baseline
-def cpu_baseline(cfg_name: str, threads: int, sr_index: int = -1, nsamples: int = 0):
-    """The oracle, as it stands, on a bounded sample of the config's workload;
-    one sample per thread.  Returns (tuples, seconds, description)."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg_name: str, threads: int, sr_indices=None, nsamples: int = 0):
+    """The oracle, as it stands, on a bounded sample of the config's workload:
+    `nsamples` samples (default one per thread, at most the per-GPU batch)
+    under each listed semiring of the config, samples in parallel on
+    `threads` host threads.  Returns (tuples, seconds, description)."""
     import oracle
     cfg = CONFIGS[cfg_name]
-    sr = cfg["semirings"][sr_index]
+    srs = [cfg["semirings"][i] for i in (sr_indices if sr_indices is not None else range(len(cfg["semirings"])))]
     n = nsamples or max(1, min(threads, cfg["per_gpu"]))
     if cfg_name == "C4":
         n = min(n, 8)
@@ -199,12 +228,15 @@ def cpu_baseline(cfg_name: str, threads: int, sr_index: int = -1, nsamples: int 
         n = 1
     reps = 200 if cfg_name == "C1" else 1  # C1 is one 14-tuple problem: repeat it
     t = time.perf_counter()
-    for _ in range(reps):
-        res = oracle.run(w.program, sr, w.batch_size, w.facts, samples=list(range(n)), threads=threads)
+    tuples = 0
+    for sr in srs:
+        for _ in range(reps):
+            res = oracle.run(w.program, sr, w.batch_size, w.facts, samples=list(range(n)), threads=threads)
+            tuples += sum(len(r) for r in res.relations.values())
     dt = time.perf_counter() - t
-    tuples = reps * sum(len(r) for r in res.relations.values())
-    return tuples, dt, (f"{n} of the {cfg['per_gpu']} {cfg_name} samples under semiring {sr} (one per thread)"
-                        + (f", repeated {reps}x" if reps > 1 else ""))
+    names = {0: "unit", 1: "max-min-prob", 2: "add-mult-prob", 3: "diff-max-mult-prob"}
+    return tuples, dt, (f"{n} of the {cfg['per_gpu']} {cfg_name} samples under {' + '.join(names[x] for x in srs)}"
+                        f" on {threads} thread(s)" + (f", repeated {reps}x" if reps > 1 else ""))
 
 
 def run_reference(args):
@@ -218,10 +250,10 @@ def run_reference(args):
     threads = max(1, min(cores, cfg["per_gpu"]))
     nsr = len(cfg["semirings"])
     for i in range(args.warmup):  # warm-up: load and exercise the oracle library (C1-sized, ms)
-        cpu_baseline("C1", 1, -1, 1)
+        cpu_baseline("C1", 1, [-1], 1)
     tot_t, tot_tuples, desc = 0.0, 0, ""
     for i in range(args.steps):
-        tuples, dt, desc = cpu_baseline(args.config, threads, i % nsr)
+        tuples, dt, desc = cpu_baseline(args.config, threads, [i % nsr])
         tot_t += dt
         tot_tuples += tuples
     v = tot_tuples / tot_t
@@ -230,7 +262,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": cfg["desc"], "global_batch": cfg["per_gpu"]},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": desc + "; semirings alternate by step"},
+                             "cpu_model": cpu_model(), "sample": desc + "; semirings alternate by step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -238,6 +270,8 @@ def run_reference(args):
 # ------------------------------------------------------------------- lobster
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -248,11 +282,13 @@ def main():
     cfg = CONFIGS[args.config]
     per_gpu = cfg["per_gpu"]
     ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
     L = _lib.load()
+    gbatch = per_gpu * ws
+    lo = per_gpu * rank  # == dist.shard(gbatch, rank, ws)[0]
 
     w = _rank_batch(cfg["make"], per_gpu, rank)
     # device-resident inputs (value) and pinned host inputs (e2e)
@@ -269,46 +305,92 @@ def main():
         h2d += sum(c.numel() * 4 for c in cols_h) + (0 if s_h is None else s_h.numel() * 4) + p_h.numel() * 4
     h2d *= len(cfg["semirings"])  # pushed once per semiring
 
-    engines = {sr: Engine(w.program, sr, batch_size=per_gpu, device=local) for sr in cfg["semirings"]}
+    # independent fixpoints (one per semiring) overlap on their own streams,
+    # each driven by its own host thread (the ctypes calls release the GIL)
+    overlap = len(cfg["semirings"]) > 1 and not args.serial
+    streams = {sr: (torch.cuda.Stream(device=dev) if overlap else torch.cuda.current_stream(dev))
+               for sr in cfg["semirings"]}
+    engines = {sr: Engine(w.program, sr, batch_size=gbatch, device=local, rank=rank, world_size=ws,
+                          stream=streams[sr].cuda_stream if overlap else None)
+               for sr in cfg["semirings"]}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     nfacts = w.n_facts()
-    grad_dense = torch.zeros(nfacts * ws, dtype=torch.float32, device=dev)
     rel = cfg["out"]
     arity0 = rel in ("endpoints_connected",)
+    grad_local = torch.zeros(nfacts, dtype=torch.float32, device=dev)
+    layout = D.fact_layout(w.facts, device=dev) if ws > 1 else None
+    grad_global = torch.zeros(layout.total if layout else nfacts, dtype=torch.float32, device=dev)
 
-    def step(facts, host_out=False):
-        stats, d2h = [], 0
-        for sr, eng in engines.items():
+    def run_one(sr, facts, host_out, box):
+        try:
+            _run_one(sr, facts, host_out, box)
+        except BaseException as e:  # surfaced by step() on the main thread
+            box[("error", sr)] = e
+
+    def _run_one(sr, facts, host_out, box):
+        eng = engines[sr]
+        with torch.cuda.stream(streams[sr]):
             eng.push_facts(facts)
-            stats.append(eng.run())
-        if DIFF_MAX_MULT_PROB in engines:
-            em = engines[DIFF_MAX_MULT_PROB]
-            out_dev = em.output(rel, device=True)
-            grad_dense.zero_()
-            em.backward(rel, torch.ones(out_dev.n, dtype=torch.float32, device=dev),
-                        grad_dense[rank * nfacts:(rank + 1) * nfacts])
-            if ws > 1:
-                rec = D.arity0_records(out_dev.sample_ids, out_dev.probs, per_gpu, device=dev) if arity0 else \
-                    torch.zeros(2 * per_gpu, device=dev)
-                D.all_gather_records(rec)
-                D.all_reduce_grad(grad_dense)
-        if host_out:  # e2e: results back to the host through the C ABI
-            for sr, eng in engines.items():
+            st = eng.run()
+            d2h = 0
+            if sr == DIFF_MAX_MULT_PROB:
+                out_dev = eng.output(rel, device=True)
+                grad_local.zero_()
+                eng.backward(rel, torch.ones(out_dev.n, dtype=torch.float32, device=dev), grad_local)
+                if ws > 1:
+                    box["rec"] = D.arity0_records(out_dev.sample_ids, out_dev.probs, lo, per_gpu, device=dev)
+            if host_out:  # e2e: results back to the host through the C ABI
                 o = eng.output(rel, device=False, copy=False)  # pinned host views (valid until next run)
                 d2h += o.n * 4 * (1 + o.arity) + o.sample_offsets.nbytes
                 if o.probs is not None:
                     d2h += o.probs.nbytes
                 if o.grad_values is not None:
                     d2h += o.grad_offsets.nbytes + o.grad_fact_ids.nbytes + o.grad_values.nbytes
-        return stats, d2h
+            box[sr] = (st, d2h)
+
+    def step(facts, host_out=False):
+        box = {}
+        main = torch.cuda.current_stream(dev)
+        if overlap:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            for s_ in streams.values():
+                s_.wait_event(ev)
+            ths = [threading.Thread(target=run_one, args=(sr, facts, host_out, box)) for sr in engines]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            for sr in engines:
+                if ("error", sr) in box:
+                    raise box[("error", sr)]
+                main.wait_stream(streams[sr])
+        else:
+            for sr in engines:
+                _run_one(sr, facts, host_out, box)
+        if ws > 1:  # the exchange after the fixpoint
+            if DIFF_MAX_MULT_PROB in engines:
+                grad_global.zero_()
+                D.scatter_grad(grad_local, layout, grad_global)
+                D.all_reduce_grad(grad_global)
+            rec = box.get("rec")
+            if rec is None or not arity0:  # variable-size outputs: per-sample row counts
+                o = engines[list(engines)[-1]].output(rel, device=True)
+                rec = torch.diff(o.sample_offsets).float()
+            D.records_global(D.all_gather_records(rec), gbatch, ws) if arity0 else D.all_gather_records(rec)
+        return [box[sr][0] for sr in engines], sum(box[sr][1] for sr in engines)
 
     def barrier():
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    # warm-up: the device path and (outside the timed region) the e2e path's
+    # pinned output buffers, allocated on first use
     for _ in range(max(args.warmup, 0)):
         step(dfacts)
+    if not args.no_e2e:
+        step(hfacts, True)
     barrier()
 
     def timed(facts, host_out):
@@ -326,51 +408,66 @@ def main():
             stats_all.append(st)
         launches = L.lobster_kernel_launches() - l0
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        per_rank = [total_ms]
         if ws > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()), stats_all, d2h, launches
+            allt = [torch.zeros_like(t) for _ in range(ws)]
+            dist.all_gather(allt, t)
+            per_rank = [float(x.item()) for x in allt]
+        return max(per_rank), stats_all, d2h, launches, per_rank
 
     with ClockSampler(local) as clk:
-        total_ms, stats_all, _, launches = timed(dfacts, False)
+        total_ms, stats_all, _, launches, per_rank = timed(dfacts, False)
     e2e_ms, e2e_d2h = None, 0
     if not args.no_e2e:
-        step(hfacts, True)  # warm the e2e path too (pinned output buffers are allocated on first use)
+        e2e_ms, _, e2e_d2h, _, _ = timed(hfacts, True)
+    # Roofline pass: the dominant kernel's live CUDA-event time is taken with the
+    # fixpoints serialised (overlapping streams would charge one fixpoint's
+    # kernels to the other's events); same steps, same inputs, after the timed region.
+    rf_stats = stats_all
+    if overlap:
+        was = overlap
+        overlap = False
+        rf_stats = []
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            rf_stats.append(step(dfacts)[0])
         barrier()
-        e2e_ms, _, e2e_d2h, _ = timed(hfacts, True)
+        overlap = was
 
     tuples_step = sum(s["tuples_derived"] for s in stats_all[-1])
     cands_step = sum(s["candidates"] for s in stats_all[-1])
     ms_step = total_ms / args.steps
     value = tuples_step * ws / (ms_step / 1000.0)
-    ph = {k: sum(s[k] for s in stats_all[-1]) for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge", "ms_grad")}
+    ph = {k: sum(s[k] for s in rf_stats[-1]) for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge", "ms_grad")}
     peak, peak_src = peaks()
     # Dominant kernel: the fused row-centric join + direct ⊕ (join_rows_direct_k).
     # SURVEY §8(d) algorithmic bytes per launch = |Δ|·r_Δ (probe read) + 2·|C|·r_C
     # (candidate write + re-read for dedup), r = packed key (4 B) + tag bytes;
-    # duration = the engine's CUDA events around each launch, on its stream,
-    # summed over the timed steps (averaged per launch).
-    # the engine times every 4th fused launch with CUDA events (an event pair per launch
-    # costs ~8% of the step); bytes and time below are those of exactly the timed launches
-    fj_l = sum(s["fj_timed_launches"] for st in stats_all for s in st)
-    fj_all = sum(s["fj_launches"] for st in stats_all for s in st)
-    fj_ms = sum(s["ms_fused_join"] for st in stats_all for s in st)
+    # the engine times every 4th fused launch with CUDA events on its stream
+    # (an event pair per launch costs ~8% of the step); bytes and time below
+    # are those of exactly the timed launches.
+    fj_l = sum(s["fj_timed_launches"] for st in rf_stats for s in st)
+    fj_all = sum(s["fj_launches"] for st in rf_stats for s in st)
+    fj_ms = sum(s["ms_fused_join"] for st in rf_stats for s in st)
     fj_b = sum(s["fj_timed_probe_rows"] * s["fj_row_bytes"] + 2 * s["fj_timed_candidates"] * s["fj_row_bytes"]
-               for st in stats_all for s in st)
+               for st in rf_stats for s in st)
     tr = ncu_traffic() if args.config == "C2" else {}
     if fj_l and fj_ms > 0:
         achieved = fj_b / fj_l / (fj_ms / fj_l / 1000.0) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr.get("dram_bytes_per_launch"),
                     "kernel": "join_rows_direct_k (fused count-free join + ⊗ + direct ⊕ into the dense store)",
-                    "launches_per_step": fj_all / len(stats_all), "timed_launches_per_step": fj_l / len(stats_all),
+                    "launches_per_step": fj_all / len(rf_stats), "timed_launches_per_step": fj_l / len(rf_stats),
                     "timing": "CUDA events on the engine stream around every 4th launch (systematic sample); "
-                              "bytes and time are those of the timed launches",
+                              "bytes and time are those of the timed launches" +
+                              ("; taken over K serialised steps after the overlapped timed region" if overlap else ""),
                     "avg_launch_us": 1000.0 * fj_ms / fj_l,
                     "alg_bytes_per_launch": fj_b / fj_l,
                     "alg_bytes_def": "SURVEY §8(d): |Δ|·r + 2·|C|·r per launch, r = 4 B key + tag (8 B max-mult)",
                     "traffic_source": tr.get("source"), "peak_source": peak_src}
     else:
-        bytes_alg = sum(s["bytes_algorithmic"] for s in stats_all[-1])
+        bytes_alg = sum(s["bytes_algorithmic"] for s in rf_stats[-1])
         t_alg = max(1e-9, sum(ph[k] for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge")) / 1000.0)
         achieved = bytes_alg / t_alg / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -379,12 +476,14 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "name": args.config, "global_batch": per_gpu * ws,
-                       "parallelism": f"dp{ws} (batch sharded, no collective inside the fixpoint)",
+            "config": {"workload": cfg["desc"], "name": args.config, "global_batch": gbatch,
+                       "parallelism": f"dp{ws} (batch sharded, global sample ids; no collective inside the fixpoint)",
+                       "semiring_fixpoints": "overlapped on two streams" if overlap else "serial",
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "samples_per_s": per_gpu * ws / (ms_step / 1000.0),
+            "samples_per_s": gbatch / (ms_step / 1000.0),
             "candidates_per_s": cands_step * ws / (ms_step / 1000.0),
             "tuples_per_step": tuples_step * ws, "rounds_per_step": sum(s["rounds_total"] for s in stats_all[-1]),
+            "per_rank_ms_per_step": [t_ / args.steps for t_ in per_rank],
             "phases_ms": ph, "gpu_launches": launches, "roofline": roofline}
     if e2e_ms is not None:
         line["e2e"] = {"value": tuples_step * ws / (e2e_ms / args.steps / 1000.0), "unit": UNIT,
@@ -393,9 +492,11 @@ def main():
     line["clocks"] = clk.summary()
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config != "C5":
         cores = os.cpu_count() or 1
-        tuples, dt, desc = cpu_baseline(args.config, max(1, min(cores, 16)))
-        line["cpu_baseline"] = {"value": tuples / dt, "unit": UNIT, "cores": max(1, min(cores, 16)),
-                                "kind": "oracle", "sample": f"{desc}, {dt:.1f} s wall"}
+        tuples, dt, desc = cpu_baseline(args.config, cores)
+        t1, d1, desc1 = cpu_baseline(args.config, 1, [0], 1)
+        line["cpu_baseline"] = {"value": tuples / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "cpu_model": cpu_model(), "sample": f"{desc}, {dt:.1f} s wall",
+                                "single_thread": {"value": t1 / d1, "unit": UNIT, "sample": f"{desc1}, {d1:.1f} s"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     for e in engines.values():

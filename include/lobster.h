@@ -58,24 +58,39 @@ typedef enum {
  *   DIFF_MAX_MULT_PROB : [0,1] × witness, 0, 1, max (strict improvement; ties keep
  *                        the existing tag, same-round ties pick the smallest
  *                        (rule, non-head variables)), fp32 ×.  Gradients flow to
- *                        the input facts of the winning derivation      (reading 7, 8) */
+ *                        the input facts of the winning derivation      (reading 7, 8)
+ *   DIFF_MAX_MIN_PROB  : [0,1] × witness, 0, 1, max (tie rules as DIFF_MAX_MULT_PROB),
+ *                        min.  Tags equal MAX_MIN_PROB's; the gradient is one-hot on
+ *                        the winning derivation's minimum leaf (smallest fact id on
+ *                        ties): "the differentiable versions of the probabilistic
+ *                        semirings", PAPER.md:617 (§3.5)                  */
 typedef enum {
   LOBSTER_UNIT = 0,
   LOBSTER_MAX_MIN_PROB = 1,
   LOBSTER_ADD_MULT_PROB = 2,
-  LOBSTER_DIFF_MAX_MULT_PROB = 3
+  LOBSTER_DIFF_MAX_MULT_PROB = 3,
+  LOBSTER_DIFF_MAX_MIN_PROB = 4
 } lobster_semiring;
 
 typedef struct {
   int32_t device;       /* CUDA device ordinal                                              */
   void* cuda_stream;    /* cudaStream_t all work is ordered on (NULL = default stream)     */
-  int32_t batch_size;   /* samples per database (>= 1; 0 is treated as 1)                   */
+  int32_t batch_size;   /* samples per database (>= 1; 0 is treated as 1).  With
+                           world_size > 1 this is the GLOBAL batch (see rank)               */
   int32_t max_iters;    /* per-stratum round cap; 0 = default 100000                        */
   int64_t arena_bytes;  /* initial per-round scratch arena; 0 = auto (grows on demand)      */
-  int32_t micro_batch;  /* reserved (0 = whole batch in one fixpoint)                       */
-  int32_t rank;         /* this process's rank (informational; collectives live above)      */
-  int32_t world_size;   /* number of ranks (informational)                                   */
-  void* nccl_comm;      /* reserved                                                          */
+  int32_t micro_batch;  /* samples per fixpoint pass; 0 = auto: the largest power of two
+                           whose packed keys fit the direct-mapped store (samples are
+                           independent databases), else the whole batch  */
+  int32_t rank;         /* world_size > 1: this context owns the contiguous sample shard
+                           [lo, hi) of rank `rank` (lo = rank*(B/W) + min(rank, B%W), sizes
+                           differing by at most one).  Sample ids crossing
+                           the ABI (facts_push, output_get) are GLOBAL ids; pushing a
+                           sample outside the shard is a RANGE error.  Fact ids stay
+                           local to the context (the distributed layer, dist.py, maps
+                           them to global ids).  The fixpoint has no collective.       */
+  int32_t world_size;   /* number of ranks sharing the batch (0 or 1 = unsharded)          */
+  void* nccl_comm;      /* reserved (collectives run above the ABI, on torch.distributed) */
 } lobster_options;
 
 /* Create a context on options->device.  options may be NULL (device 0, default
@@ -105,7 +120,8 @@ lobster_status lobster_program_load(lobster_ctx* ctx, const char* program_text, 
 /* Append n facts to input relation `relation`.
  *   columns    : `arity` pointers, each to n int32 values (host or device memory,
  *                detected per pointer); may be NULL when arity == 0
- *   sample_ids : n int32 in [0, batch_size) (host or device); NULL for a shared relation
+ *   sample_ids : n int32 in [0, batch_size) (host or device), or in the context's
+ *                shard [lo, hi) when world_size > 1; NULL for a shared relation
  *   probs      : n float in [0,1] (host or device); NULL = 1.0; ignored under UNIT
  * Fact ids are dense in push order: [*first_fact_id, *first_fact_id + n).
  * The data is copied before return; the caller keeps ownership of its buffers.
@@ -146,11 +162,12 @@ typedef struct {
   int64_t n;                      /* rows                                                  */
   int32_t arity;
   int32_t on_device;              /* 1: pointers are device pointers                        */
-  const int32_t* sample_ids;      /* n (sample of each row)                                 */
+  const int32_t* sample_ids;      /* n (global sample id of each row)                       */
   const int32_t* const* columns;  /* arity pointers to n int32; rows sorted by (sample, cols) */
   const float* probs;             /* n; NULL under UNIT; add-mult is unclamped      */
-  const int64_t* sample_offsets;  /* batch_size+1: rows of sample s are [off[s], off[s+1])  */
-  const int64_t* grad_offsets;    /* n+1, DIFF_MAX_MULT_PROB output relations only, else NULL */
+  const int64_t* sample_offsets;  /* B+1 (B = this context's samples: batch_size, or hi-lo
+                                     when sharded): rows of sample lo+s are [off[s], off[s+1]) */
+  const int64_t* grad_offsets;    /* n+1, DIFF_* output relations only, else NULL            */
   const int64_t* grad_fact_ids;   /* grad_offsets[n] ids, ascending within each row         */
   const float* grad_values;       /* ∂probs[row] / ∂p(fact), fp64-accumulated, rounded to fp32 */
 } lobster_output;

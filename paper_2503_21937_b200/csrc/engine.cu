@@ -204,11 +204,13 @@ enum Version { V_EXT = 0, V_NEW = 1, V_OLD = 2, V_DELTA = 3 };
 
 struct Ctx {
   lobster_options opt{};
+  int32_t sample_base = 0;  // first global sample id of this context's shard (world_size > 1)
   cudaStream_t st = nullptr;
   std::string err;
   bool sticky = false;
   bool loaded = false, ran = false, dirty = false;
   int semi = 0;
+  bool omin = false;  // diff-max-min-prob (semi == S_MAXMULT internally)
   Program prog;
   std::vector<std::unique_ptr<RelState>> rels;
   int64_t next_fact = 0;
@@ -325,6 +327,18 @@ struct Ctx {
   void create(const lobster_options* o) {
     if (o) opt = *o;
     if (opt.batch_size < 1) opt.batch_size = 1;
+    // Sharded batch: batch_size is the GLOBAL batch and this
+    // context owns the contiguous shard [lo, hi) of `rank`; sample ids cross the
+    // ABI as global ids and are rebased to the shard inside.
+    if (opt.world_size > 1) {
+      if (opt.rank < 0 || opt.rank >= opt.world_size) throw Failure(LOBSTER_E_INVALID_ARG, "rank outside [0, world_size)");
+      const int64_t B = opt.batch_size, W = opt.world_size, base = B / W, extra = B % W;
+      const int64_t lo = opt.rank * base + std::min<int64_t>(opt.rank, extra);
+      const int64_t hi = lo + base + (opt.rank < extra ? 1 : 0);
+      if (hi <= lo) throw Failure(LOBSTER_E_INVALID_ARG, "world_size larger than the batch");
+      sample_base = (int32_t)lo;
+      opt.batch_size = (int32_t)(hi - lo);
+    }
     max_iters = opt.max_iters > 0 ? opt.max_iters : 100000;
     int ndev = 0;
     cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -345,10 +359,14 @@ struct Ctx {
   // ---------------------------------------------------------- program load
   void load(const char* text, int semiring) {
     if (loaded) throw Failure(LOBSTER_E_STATE, "program already loaded");
-    if (semiring < 0 || semiring > 3) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 4) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
     if (!text) throw Failure(LOBSTER_E_INVALID_ARG, "program text is NULL");
     prog = parse_program(text);
-    semi = semiring;
+    // diff-max-min-prob runs on the max-mult machinery (packed (p, stamp,
+    // witness) words, strict improvement, tie rules 8a/8b) with ⊗ = min and a
+    // one-hot gradient (reading "diff-max-min")
+    omin = semiring == LOBSTER_DIFF_MAX_MIN_PROB;
+    semi = omin ? S_MAXMULT : semiring;
     for (auto& r : prog.rels)
       if (r.arity > MAXARITY) throw Failure(LOBSTER_E_PARSE, "relation " + r.name + ": arity above 8 is unsupported");
     for (auto& R : prog.rules) {
@@ -434,6 +452,7 @@ struct Ctx {
       uint32_t* flags = reinterpret_cast<uint32_t*>(hbuf);
       uint32_t* dflag = arena.get<uint32_t>(1);
       cuda_check(cudaMemsetAsync(dflag, 0, 4, st), "memset");
+      if (sample_base && !R.shared) launch_add_i32(S.in.sid.ptr() + base, n, -sample_base, st);
       launch_validate((probs && semi != S_UNIT) ? S.in.p.ptr() + base : nullptr,
                       R.shared ? nullptr : S.in.sid.ptr() + base, n, opt.batch_size, dflag, st);
       kcheck("validate");
@@ -874,6 +893,7 @@ struct Ctx {
       merge_moves(lp.om, lp.nom);
       merge_moves(lp.wm, lp.nwm);
       lp.semi = semi;
+      lp.omin = omin ? 1 : 0;
       if (semi != S_UNIT) {
         lp.ntag = na;
         for (int k = 0; k < na; ++k)
@@ -1018,6 +1038,7 @@ struct Ctx {
         cmp_done[i] = 1;
       }
       jp.semi = semi;
+      jp.omin = omin ? 1 : 0;
       const bool last = s == na - 1;
       jp.final_step = last ? 1 : 0;
       // fused row-centric join + direct ⊕: bounded fan-out, one probe tag
@@ -1757,6 +1778,7 @@ struct Ctx {
                                           cudaMemcpyDeviceToDevice, st), "finalize");
       S.o_soff.reserve(opt.batch_size + 1);
       launch_sample_offsets_i32(S.o_sid.ptr(), n, opt.batch_size, S.o_soff.ptr(), st);
+      if (sample_base && S.L.has_sample) launch_add_i32(S.o_sid.ptr(), n, sample_base, st);
       if (semi != S_UNIT) S.p.swap(S.acc_p);
       if (S.has_grad) {
         S.goff.swap(S.acc_goff);
@@ -2203,6 +2225,15 @@ struct Ctx {
       const int tbits = 32 + bits_for((uint64_t)n);
       int which = radix_sort<uint64_t, void>(k0, nullptr, k1, nullptr, nleaf, tbits, arena.alloc(sort_tmp_bytes(nleaf)), st);
       uint64_t* ks = which ? k1 : k0;
+      if (omin) {
+        S.gfid.reserve(n);
+        S.gval.reserve(n);
+        launch_grad_onehot(ks, nleaf, fact_p.ptr(), n, loff, S.goff.ptr(), S.gfid.ptr(), S.gval.ptr(), st);
+        kcheck("grad one-hot");
+        S.ng = n;
+        S.has_grad = true;
+        continue;
+      }
       uint32_t* fl = arena.get<uint32_t>(nleaf);
       uint32_t* pos = arena.get<uint32_t>(nleaf);
       uint32_t* tot = arena.get<uint32_t>(1);
@@ -2249,6 +2280,7 @@ struct Ctx {
       launch_unpack(S.key.ptr(), n, S.L.has_sample, (uint8_t)S.L.sshift, ar, dsh, dsh + 8,
                     reinterpret_cast<int32_t*>(dsh + 16), S.o_sid.ptr(), S.o_cols.ptr(), st);
       launch_sample_offsets(S.key.ptr(), n, opt.batch_size, (uint8_t)S.L.sshift, S.L.has_sample, S.o_soff.ptr(), st);
+      if (sample_base && S.L.has_sample) launch_add_i32(S.o_sid.ptr(), n, sample_base, st);
       kcheck("unpack");
       sync();
       arena.reset();

@@ -67,6 +67,7 @@ constexpr int SPT = WT / 256;
 // ⊗ in body order over T = [ptag[0..npt-1], btag] (reading 9).  Fast path:
 // one probe tag followed by the build tag (every linear TC-shaped rule).
 __device__ __forceinline__ float candidate_tag(const JoinPlan& jp, int semi, int64_t row, int64_t j) {
+  if (jp.omin) semi = S_MAXMIN;  // diff-max-min: ⊗ = min
   if (jp.npt == 1 && jp.ntag == 2) {
     const float a = jp.ptag[0][row], b = jp.btag[j];
     return jp.tag_order[0] == 0 ? otimes(semi, a, b) : otimes(semi, b, a);
@@ -414,7 +415,8 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
         oldv[d] = PEEK(reinterpret_cast<const uint32_t*>(jp.fdir) + (slot >> 5));
         continue;
       }
-      const float t = jp.tag_order[0] == 0 ? otimes(SEMI, pt, bt) : otimes(SEMI, bt, pt);
+      const int osemi = (SEMI == S_MAXMULT && jp.omin) ? S_MAXMIN : SEMI;  // diff-max-min: ⊗ = min
+      const float t = jp.tag_order[0] == 0 ? otimes(osemi, pt, bt) : otimes(osemi, bt, pt);
       if (SEMI == S_MAXMIN) {
         newv[d] = mm_word(t);
         oldv[d] = PEEK(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
@@ -527,7 +529,7 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
     };
     t = pick(lp.tag_order[0]);
 #pragma unroll 1
-    for (int k = 1; k < lp.ntag; ++k) t = otimes(semi, t, pick(lp.tag_order[k]));
+    for (int k = 1; k < lp.ntag; ++k) t = otimes(lp.omin ? S_MAXMIN : semi, t, pick(lp.tag_order[k]));
     if (semi == S_MAXMULT)
       w = lp.wconst | (uint32_t)(NM ? moves_n<NM>(lp.wm, lp.nwm, pk, 0) : apply_moves(lp.wm, lp.nwm, pk, 0));
   }

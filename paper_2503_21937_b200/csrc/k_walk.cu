@@ -161,6 +161,27 @@ __global__ void grad_k(const uint64_t* __restrict__ tf, const uint32_t* __restri
   }
 }
 
+// diff-max-min-prob: p = min over the derivation's leaves, so ∂p/∂p_f is one-hot
+// on the leaf holding the minimum; leaves are sorted by (tuple, fact), so a
+// strict < keeps the smallest fact id among equal minima.
+__global__ void grad_onehot_k(const uint64_t* __restrict__ tf, int64_t nleaf, const float* __restrict__ fact_p,
+                              int64_t ntup, const int64_t* __restrict__ loff, int64_t* __restrict__ goff,
+                              int64_t* __restrict__ gfid, float* __restrict__ gval) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntup) return;
+  goff[t] = t;
+  if (t == ntup) return;
+  uint32_t best = 0;
+  float bp = 0.0f;
+  for (int64_t i = loff[t], e = loff[t + 1]; i < e && i < nleaf; ++i) {
+    const uint32_t f = (uint32_t)(tf[i] & 0xffffffffu);
+    const float p = fact_p[f];
+    if (i == loff[t] || p < bp) { best = f; bp = p; }
+  }
+  gfid[t] = (int64_t)best;
+  gval[t] = 1.0f;
+}
+
 __global__ void unpack_k(const uint64_t* __restrict__ key, int64_t n, int has_sample, int sshift, int ncols,
                          const uint8_t* __restrict__ shift, const uint8_t* __restrict__ bits,
                          const int32_t* __restrict__ mins, int32_t* __restrict__ sample, int32_t* __restrict__ cols) {
@@ -256,6 +277,13 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
   note_launch();
   grad_k<<<(unsigned)((ntup + 1 + 127) / 128), 128, 0, st>>>(sorted_tf, pos, nleaf, nuniq, fact_p, ntup, loff, goff,
                                                             gfid, gval, scratch);
+}
+
+void launch_grad_onehot(const uint64_t* sorted_tf, int64_t nleaf, const float* fact_p, int64_t ntup,
+                        const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, cudaStream_t st) {
+  note_launch();
+  grad_onehot_k<<<(unsigned)((ntup + 1 + 127) / 128), 128, 0, st>>>(sorted_tf, nleaf, fact_p, ntup, loff, goff, gfid,
+                                                                   gval);
 }
 
 void launch_unpack(const uint64_t* key, int64_t n, int has_sample, uint8_t sshift, int ncols, const uint8_t* shift,

@@ -86,6 +86,7 @@ struct JoinPlan {
   uint64_t cout;            // constant bits of the output key
   int final_step;           // 1: candidates (head key, ⊗, witness); 0: intermediate
   int semi;
+  int omin;                 // diff-max-min-prob: max-mult storage and witnesses, ⊗ = min
   // ⊗ in body order over T = [ptag[0..npt-1], btag]: T[tag_order[k]] for k = 0..ntag-1
   int ntag;
   int8_t tag_order[MAXT];
@@ -174,6 +175,7 @@ struct LookupPlan {
   Move om[MAXM];
   uint64_t cout;
   int semi;
+  int omin;           // diff-max-min-prob: ⊗ = min (storage as max-mult)
   // ⊗ in body order over T = [probe tag, lookup tags...]
   int ntag;
   int8_t tag_order[MAXT];
@@ -367,6 +369,10 @@ void launch_leaf_heads(const uint64_t* k, int64_t n, uint32_t* flag, cudaStream_
 void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, int64_t nuniq, const float* fact_p,
                  int64_t ntup, const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
                  cudaStream_t st);
+
+// diff-max-min: one-hot gradient on each tuple's minimum leaf (goff[t] = t)
+void launch_grad_onehot(const uint64_t* sorted_tf, int64_t nleaf, const float* fact_p, int64_t ntup,
+                        const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, cudaStream_t st);
 
 // u32 keys -> u64 (sorted-store candidates narrowed for the sort)
 void launch_widen_u32(const uint32_t* in, int64_t n, uint64_t* out, cudaStream_t st);

@@ -92,7 +92,8 @@ class Engine:
     """One lobster context: program_load -> facts_push* -> run -> output_get*."""
 
     def __init__(self, program: str, semiring: int, batch_size: int = 1, device: int = 0,
-                 stream: Optional[int] = None, max_iters: int = 0, arena_bytes: int = 0, micro_batch: int = 0):
+                 stream: Optional[int] = None, max_iters: int = 0, arena_bytes: int = 0, micro_batch: int = 0,
+                 rank: int = 0, world_size: int = 1):
         self._L = _lib.load()
         o = _lib.Options()
         o.device = device
@@ -101,6 +102,13 @@ class Engine:
         o.max_iters = max_iters
         o.arena_bytes = arena_bytes
         o.micro_batch = micro_batch
+        o.rank = rank
+        o.world_size = world_size
+        # samples this context owns: the whole batch, or its shard of the
+        # global batch (include/lobster.h `rank`); sample ids stay global
+        base, extra = divmod(batch_size, max(world_size, 1))
+        self.sample_lo = rank * base + min(rank, extra) if world_size > 1 else 0
+        self.local_batch = (base + (1 if rank < extra else 0)) if world_size > 1 else batch_size
         self.batch_size = batch_size
         self.semiring = semiring
         self.device = device
@@ -187,8 +195,8 @@ class Engine:
                 cols = np.zeros((0, n), np.int32)
             out = RelationOutput(n, ar, _np_view(o.sample_ids, n, np.int32, copy), cols,
                                  _np_view(o.probs, n, np.float32, copy) if self.semiring != _lib.UNIT else None,
-                                 _np_view(o.sample_offsets, self.batch_size + 1, np.int64, copy))
-            if o.grad_offsets or (self.semiring == _lib.DIFF_MAX_MULT_PROB and n == 0 and o.grad_offsets is not None):
+                                 _np_view(o.sample_offsets, self.local_batch + 1, np.int64, copy))
+            if o.grad_offsets or (self.semiring in (_lib.DIFF_MAX_MULT_PROB, _lib.DIFF_MAX_MIN_PROB) and n == 0 and o.grad_offsets is not None):
                 goff = _np_view(o.grad_offsets, n + 1, np.int64, copy) if n else np.zeros(1, np.int64)
                 ng = int(goff[-1]) if n else 0
                 out.grad_offsets = goff
@@ -205,7 +213,7 @@ class Engine:
             return torch.as_tensor(_CudaArray(ptr, shape, ts, self), device=dev)
         out = RelationOutput(n, ar, t(o.sample_ids, (n,), "<i4"), [t(o.columns[c], (n,), "<i4") for c in range(ar)],
                              t(o.probs, (n,), "<f4") if self.semiring != _lib.UNIT else None,
-                             t(o.sample_offsets, (self.batch_size + 1,), "<i8"))
+                             t(o.sample_offsets, (self.local_batch + 1,), "<i8"))
         if o.grad_offsets:
             goff = t(o.grad_offsets, (n + 1,), "<i8")
             ng = int(goff[-1].item()) if n else 0
