@@ -223,6 +223,13 @@ struct Ctx {
   DBuf<float> fact_p;
   lobster_run_stats stats{};
   unsigned long long* d_ncand = nullptr;  // device counter of fused-join candidates
+  // bit-sliced frontier (k_slice.cu): relation / round bits, Δ triples, per-rule CSR
+  struct SliceBufs {
+    DBuf<uint32_t> Rb, Nb, dt, dwi, dbits, deg, pos, cnt, scan;
+    std::vector<std::unique_ptr<DBuf<uint32_t>>> off, nbr;
+    DBuf<unsigned long long> tup;
+  } sl;
+  bool no_slice = getenv("LOBSTER_NO_SLICE") != nullptr;  // A/B: per-sample bitmap rounds
   bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
   int32_t batch_cur = 1;  // samples of the (micro-)batch being evaluated
@@ -353,6 +360,8 @@ struct Ctx {
     cuda_check(cudaMallocHost(&hbuf, 64), "cudaMallocHost");
     arena.bind(st);
     fact_p.bind(st);
+    for (auto* b : {&sl.Rb, &sl.Nb, &sl.dt, &sl.dwi, &sl.dbits, &sl.deg, &sl.pos, &sl.cnt, &sl.scan}) b->bind(st);
+    sl.tup.bind(st);
     if (opt.arena_bytes > 0) arena.reserve_initial((size_t)opt.arena_bytes);
   }
 
@@ -1869,6 +1878,141 @@ struct Ctx {
     return 0;
   }
 
+  // ------------------------------------------------ bit-sliced frontier
+  // A stratum qualifies when: unit semiring; one batched unary relation R in a
+  // direct (bitmap) store; every rule of R is either all-external (the seed
+  // round, evaluated as usual) or R(u) :- R(v), E(.., ..) / E(.., ..), R(v)
+  // with E a SHARED binary input whose columns are v and u (distinct
+  // variables of R's domain class), no constants, no comparisons.
+  struct SliceRule {
+    int erel;      // the shared binary relation
+    int ccol;      // its column joined with R's variable
+    int hcol;      // its column projected to R's head
+  };
+  bool slice_ok(const std::vector<int>& strat, std::vector<SliceRule>& out) {
+    out.clear();
+    if (no_slice || semi != S_UNIT || strat.size() != 1) return false;
+    const int r = strat[0];
+    const Relation& RR = prog.rels[r];
+    RelState& S = *rels[r];
+    if (RR.arity != 1 || RR.shared || !S.direct || !S.L.has_sample || S.L.bits[0] > 24) return false;
+    for (const Rule& R : prog.rules) {
+      if (R.head_rel != r) continue;
+      int nloc = 0;
+      for (auto& a : R.body) nloc += a.rel == r;
+      if (nloc == 0) continue;  // seed rule: already evaluated
+      if (R.body.size() != 2 || nloc != 1 || !R.cmps.empty() || !R.head[0].is_var()) return false;
+      const BodyAtom& ra = R.body[0].rel == r ? R.body[0] : R.body[1];
+      const BodyAtom& ea = R.body[0].rel == r ? R.body[1] : R.body[0];
+      const Relation& E = prog.rels[ea.rel];
+      if (!E.input || !E.shared || E.arity != 2 || !ra.args[0].is_var()) return false;
+      if (!ea.args[0].is_var() || !ea.args[1].is_var()) return false;
+      const int v = ra.args[0].var, u = R.head[0].var;
+      if (u == v) return false;
+      SliceRule sr;
+      if (ea.args[0].var == v && ea.args[1].var == u) { sr.ccol = 0; sr.hcol = 1; }
+      else if (ea.args[1].var == v && ea.args[0].var == u) { sr.ccol = 1; sr.hcol = 0; }
+      else return false;
+      sr.erel = ea.rel;
+      const Layout& EL = rels[ea.rel]->L;
+      if (EL.mins[0] != S.L.mins[0] || EL.mins[1] != S.L.mins[0] || EL.bits[0] != S.L.bits[0] ||
+          EL.bits[1] != S.L.bits[0] || rels[ea.rel]->n >= ((int64_t)1 << 32))
+        return false;
+      out.push_back(sr);
+    }
+    return !out.empty() && out.size() <= 4;
+  }
+
+  // Rounds 2.. of a qualifying stratum on bit-sliced words; R's bitmap holds
+  // the seed round's tuples on entry and every tuple on exit.  Returns the
+  // rounds run (the last one empty, as in the per-sample loop).
+  int run_sliced(RelState& S, const std::vector<SliceRule>& srules) {
+    const int tbits = S.L.bits[0];
+    const int64_t T = (int64_t)1 << tbits;
+    const int B = batch_cur;
+    const int W = (B + 31) / 32;
+    const int64_t nw = T * W;         // sliced words
+    const int64_t ndw = (nw + 31) / 32;  // dirty-bitmap words
+    while (sl.off.size() < srules.size()) {
+      sl.off.emplace_back(new DBuf<uint32_t>());
+      sl.nbr.emplace_back(new DBuf<uint32_t>());
+      sl.off.back()->bind(st);
+      sl.nbr.back()->bind(st);
+    }
+    sl.cnt.reserve(T + 4);
+    sl.scan.reserve((int64_t)(scan_tmp_bytes<uint32_t>(std::max<int64_t>(T + 1, nw)) / 4 + 1));
+    for (size_t q = 0; q < srules.size(); ++q) {  // per-rule CSR of E by its joined column
+      const RelState& E = *rels[srules[q].erel];
+      sl.off[q]->reserve(T + 1);
+      sl.nbr[q]->reserve(std::max<int64_t>(E.n, 1));
+      launch_slice_csr(E.key.ptr(), E.n, E.L.shift[srules[q].ccol], E.L.shift[srules[q].hcol], tbits, T,
+                       sl.off[q]->ptr(), sl.cnt.ptr(), sl.nbr[q]->ptr(), sl.scan.ptr(), st);
+    }
+    sl.Rb.reserve(nw);
+    sl.Nb.reserve(nw);
+    sl.dt.reserve(nw);
+    sl.dwi.reserve(nw);
+    sl.dbits.reserve(nw);
+    sl.deg.reserve(nw + 1);
+    sl.pos.reserve(nw + 1);
+    sl.tup.reserve(1);
+    uint32_t* dirty = S.dirty.ptr();  // sized for B·T bits >= T·W bits; zero between rounds
+    cuda_check(cudaMemsetAsync(sl.Rb.ptr(), 0, nw * 4, st), "memset");
+    cuda_check(cudaMemsetAsync(sl.tup.ptr(), 0, 8, st), "memset");
+    uint32_t* bm = reinterpret_cast<uint32_t*>(S.dirf.get());
+    launch_slice_from_bitmap(bm, tbits, B, T, W, sl.Nb.ptr(), dirty, st);
+    kcheck("slice from bitmap");
+    // Δ of round 2 = the seed round's tuples
+    uint32_t* count = sl.cnt.ptr() + ((T + 2) & ~(int64_t)1);  // two scratch words (8-B aligned) after the CSR counts
+    // count[0] = |Δ'| (entries), count[1] = (edge, word) items of the round's joins
+    int64_t items = 0;
+    auto extract = [&]() -> int64_t {
+      Phase ph(this, 3);
+      cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset");
+      launch_slice_extract(dirty, ndw, sl.Nb.ptr(), sl.Rb.ptr(), W, sl.dt.ptr(), sl.dwi.ptr(), sl.dbits.ptr(), count,
+                           sl.tup.ptr(), st);
+      kcheck("slice extract");
+      const uint64_t both = read_dev(reinterpret_cast<const uint64_t*>(count));
+      items = (int64_t)(both >> 32);
+      return (int64_t)(both & 0xffffffffu);
+    };
+    int64_t nd = extract();
+    int rounds = 0;
+    round_cap_hit_slice = false;
+    while (nd > 0) {
+      if (rounds + 1 >= max_iters) {  // the stratum's round 1 was the seed round
+        round_cap_hit_slice = true;
+        break;
+      }
+      ++rounds;
+      {
+        Phase ph(this, 0);
+        for (size_t q = 0; q < srules.size(); ++q) {
+          launch_slice_deg(sl.dt.ptr(), nd, sl.off[q]->ptr(), sl.deg.ptr(), st);
+          exclusive_scan<uint32_t>(sl.deg.ptr(), sl.pos.ptr(), nd, sl.pos.ptr() + nd, sl.scan.ptr(), st);
+          launch_slice_expand(sl.dt.ptr(), sl.dwi.ptr(), sl.dbits.ptr(), sl.pos.ptr(), nd, sl.pos.ptr() + nd,
+                              sl.off[q]->ptr(), sl.nbr[q]->ptr(), sl.Rb.ptr(), sl.Nb.ptr(), W, dirty, d_ncand, st);
+          // this rule's item total joins count[1] (read with |Δ'| after the extraction)
+          launch_add_u32_dev(count + 1, sl.pos.ptr() + nd, q == 0, st);
+        }
+        kcheck("slice join");
+      }
+      // §8(d) bytes of the sliced round: Δ triples read (12 B), per (edge, word)
+      // item the neighbour id and the target word (8 B), Δ' word update + triple (16 B)
+      const int64_t nd_prev = nd;
+      nd = extract();
+      stats.bytes_algorithmic += nd_prev * 12 + items * 8 + nd * 16;
+      sl_items += items;
+    }
+    // all tuples back into R's (s, t) bitmap (downstream strata, outputs, counting)
+    cuda_check(cudaMemsetAsync(bm, 0, (size_t)((S.nslots + 31) / 32) * 4, st), "memset");
+    launch_slice_to_bitmap(sl.Rb.ptr(), tbits, B, T, W, bm, st);
+    kcheck("slice to bitmap");
+    return rounds;
+  }
+  bool round_cap_hit_slice = false;
+  int64_t sl_items = 0;  // (edge, word) items of the sliced joins in this run (diagnostics)
+
   int64_t run_strata() {
     int64_t round_cap_hit = 0;
     for (size_t si = 0; si < prog.strata.size(); ++si) {
@@ -1955,6 +2099,16 @@ struct Ctx {
         }
         if (log_level >= 2) { trace.back()[1] = stats.fj_probe_rows - probe0; trace.back()[2] = changed; }
         if (changed == 0) break;
+        if (first_round) {  // C4-shaped strata continue as a bit-sliced frontier (k_slice.cu)
+          std::vector<SliceRule> srules;
+          if (slice_ok(strat, srules)) {
+            mark("seed round");
+            rounds += run_sliced(*rels[strat[0]], srules);
+            if (round_cap_hit_slice) round_cap_hit = 1;
+            async = false;
+            break;
+          }
+        }
         // every recursive rule took the fused direct join in this (non-seed) round: later
         // rounds need no host-side sizes, so they are issued without a sync (lagged stop test)
         if (first_round) mark("seed round");

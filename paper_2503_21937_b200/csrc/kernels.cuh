@@ -374,6 +374,22 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
 void launch_grad_onehot(const uint64_t* sorted_tf, int64_t nleaf, const float* fact_p, int64_t ntup,
                         const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, cudaStream_t st);
 
+// ---- bit-sliced multi-source frontier (k_slice.cu; unit, C4-shaped strata) ----
+// CSR of a shared binary relation by column ssrc (counting sort): off[T+1], nbr[n]
+void launch_slice_csr(const uint64_t* key, int64_t n, int ssrc, int sdst, int bits, int64_t T, uint32_t* off,
+                      uint32_t* cursor, uint32_t* nbr, void* scan_tmp, cudaStream_t st);
+void launch_slice_from_bitmap(const uint32_t* bm, int tbits, int B, int64_t T, int W, uint32_t* Nb, uint32_t* dirty,
+                              cudaStream_t st);
+void launch_slice_to_bitmap(const uint32_t* Rb, int tbits, int B, int64_t T, int W, uint32_t* bm, cudaStream_t st);
+void launch_slice_extract(uint32_t* dirty, int64_t ndw, uint32_t* Nb, uint32_t* Rb, int W, uint32_t* dt, uint32_t* dwi,
+                          uint32_t* dbits, uint32_t* count, unsigned long long* tuples, cudaStream_t st);
+void launch_add_u32_dev(uint32_t* dst, const uint32_t* src, bool assign, cudaStream_t st);  // *dst (+)= *src
+void launch_slice_deg(const uint32_t* dt, int64_t nd, const uint32_t* off, uint32_t* deg, cudaStream_t st);
+void launch_slice_expand(const uint32_t* dt, const uint32_t* dwi, const uint32_t* dbits, const uint32_t* pos,
+                         int64_t nd, const uint32_t* total_dev, const uint32_t* off, const uint32_t* nbr,
+                         const uint32_t* Rb, uint32_t* Nb, int W, uint32_t* dirty, unsigned long long* cands,
+                         cudaStream_t st);
+
 // u32 keys -> u64 (sorted-store candidates narrowed for the sort)
 void launch_widen_u32(const uint32_t* in, int64_t n, uint64_t* out, cudaStream_t st);
 
