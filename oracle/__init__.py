@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "oracle.cpp")
 LIB = os.path.join(HERE, "liboracle.so")
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB = 0, 1, 2, 3, 4
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
 
 
 def build(force: bool = False) -> str:
@@ -52,6 +52,7 @@ def lib():
         L.orc_num_strata.argtypes = [vp]
         L.orc_push.argtypes = [vp, cp, ctypes.c_int64, i32p, i32p, f32p, i64p]
         L.orc_run.argtypes = [vp, ctypes.c_int, i32p, ctypes.c_int]
+        L.orc_set_groups.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, i32p]
         L.orc_result_size.restype = ctypes.c_int64
         L.orc_result_size.argtypes = [vp, cp]
         L.orc_result.argtypes = [vp, cp, i32p, i32p, f32p]
@@ -110,11 +111,13 @@ def oplus(sr: int, a: float, b: float) -> float:
 
 def run(program: str, semiring: int, batch: int, facts: dict, outputs: Sequence[str] = (),
         samples: Optional[Sequence[int]] = None, threads: int = 0,
-        max_iters: Optional[int] = None, want_grads: bool = True) -> Result:
+        max_iters: Optional[int] = None, want_grads: bool = True,
+        groups: Optional[Dict[str, np.ndarray]] = None) -> Result:
     """Evaluate `program` on `facts` (dict rel -> workloads.Facts-like object with
     .cols list, .sample_ids, .probs). Facts are pushed in dict order, so fact ids
     are dense in that order. `outputs`: IDB relations to read back
-    (default: every IDB relation)."""
+    (default: every IDB relation).  `groups`: rel -> int32 exclusion group per
+    fact (top-1-proof conflicts; -1 = none)."""
     L = lib()
     err = ctypes.create_string_buffer(512)
     h = L.orc_create(program.encode(), semiring, batch, err, 512)
@@ -140,6 +143,11 @@ def run(program: str, semiring: int, batch: int, facts: dict, outputs: Sequence[
             if rc:
                 raise OracleError(rc, L.orc_last_error(h).decode())
             first_ids[rel] = first.value
+            if groups and rel in groups and n:
+                g = np.ascontiguousarray(groups[rel], dtype=np.int32)
+                rc = L.orc_set_groups(h, first.value, n, _ptr(g, ctypes.c_int32))
+                if rc:
+                    raise OracleError(rc, L.orc_last_error(h).decode())
         s = np.asarray([] if samples is None else list(samples), dtype=np.int32)
         rc = L.orc_run(h, int(s.shape[0]), _ptr(s, ctypes.c_int32) if s.shape[0] else None, threads)
         if rc:
@@ -167,7 +175,7 @@ def run(program: str, semiring: int, batch: int, facts: dict, outputs: Sequence[
             if rc:
                 raise OracleError(rc, L.orc_last_error(h).decode())
             r = Relation(sid, cols, tags)
-            if semiring in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB) and want_grads:
+            if semiring in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS) and want_grads:
                 g = L.orc_grad_size(h, rel.encode())
                 off = np.zeros(n + 1, dtype=np.int64)
                 fid = np.zeros(max(g, 1), dtype=np.int64)

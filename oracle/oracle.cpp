@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <iterator>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -48,14 +49,23 @@
 
 namespace orc {
 
-enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3, DMAX_MIN = 4 };
+enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3, DMAX_MIN = 4, TOP1 = 5 };
 
 // Semirings whose tag carries a witness (rule + non-head variables of the
 // winning derivation) and whose ⊕ is max with strict improvement:
 // diff-max-mult-prob (SURVEY §8(c) point 7) and diff-max-min-prob (§3.5
 // "the differentiable versions of the probabilistic semirings"; DESIGN.md
 // reading "diff-max-min").
-static bool witnessed(int sr) { return sr == MAX_MULT || sr == DMAX_MIN; }
+static bool witnessed(int sr) { return sr == MAX_MULT || sr == DMAX_MIN || sr == TOP1; }
+
+// diff-top-1-proofs (§2, §3.5 "Limitations"; DESIGN.md reading
+// "top-1-proof"): a tag is ONE proof, a set of input facts of at most
+// PROOF_CAP (300) facts; p(proof) = Π_{f in proof} p_f, the product
+// taken in fp64 in ascending fact-id order and rounded once to fp32 (a
+// function of the set).  ⊗ = union, dropped on a conflict (two facts of one
+// exclusion group); ⊕ = the more likely proof, with the
+// tie rules of diff-max-mult (reading 8).  ∂p/∂p_f = Π_{g in proof, g != f} p_g.
+static const size_t PROOF_CAP = 300;
 
 static const int MAXA = 8;  // max arity / max non-head variables in the oracle
 
@@ -91,6 +101,7 @@ struct Tag {
   int rule = -1;      // diff-max-mult witness: global rule index (IDB tuples)
   Tuple wv;           // witness: non-head variable values in order of first appearance
   int64_t fact = -1;  // EDB tuples: id of the (surviving) input fact
+  std::vector<int64_t> proof;  // top-1-proof: sorted fact ids
 };
 
 // ⊗ (Fig. 7b for max-min; SURVEY §8(c) point 6/7 for add-mult and max-mult):
@@ -99,6 +110,7 @@ static float otimes(int sr, float a, float b) {
   switch (sr) {
     case MAX_MIN: return a < b ? a : b;       // min
     case DMAX_MIN: return a < b ? a : b;      // min (diff-max-min-prob)
+    case TOP1: return 1.0f;                   // (p comes from the proof set, see eval_rule)
     case ADD_MULT: return a * b;              // ×  (compiled with -ffp-contract=off)
     case MAX_MULT: return a * b;              // ×
     default: return 1.0f;                     // unit: ∧ of true facts
@@ -116,6 +128,7 @@ static Tag oplus_state(int sr, const Tag& s, const Tag& b) {
     case ADD_MULT: { Tag r = s; r.p = (float)((double)s.p + (double)b.p); return r; }
     case MAX_MULT: return (b.p > s.p) ? b : s;
     case DMAX_MIN: return (b.p > s.p) ? b : s;
+    case TOP1: return (b.p > s.p) ? b : s;
     default: return s;
   }
 }
@@ -358,6 +371,7 @@ using Entry = std::pair<const Tuple, Tag>;
 
 struct Candidate {
   Tuple head; float p; int rule; Tuple wv; int variant;
+  std::vector<int64_t> proof;  // top-1-proof
   bool operator<(const Candidate& o) const {  // canonical order (SURVEY §8(c) point 8b)
     if (!(head == o.head)) return head < o.head;
     if (rule != o.rule) return rule < o.rule;
@@ -389,6 +403,7 @@ struct Engine {
   std::map<std::string, InputFacts> in;
   int64_t next_fact = 0;
   std::vector<float> fact_p;
+  std::vector<int64_t> fact_group;  // top-1-proof exclusion group per fact (-1: none)
   std::map<std::string, Rel> shared;     // shared EDB relations
   std::vector<std::unique_ptr<SampleDB>> db;
   std::vector<int> run_samples;
@@ -397,7 +412,7 @@ struct Engine {
   std::map<std::pair<const Rel*, std::vector<int>>, std::map<Tuple, std::vector<const Entry*>>> shared_idx;
 
   Engine(const std::string& text, int semiring, int b) : prog(parse_program(text)), sr(semiring), batch(b < 1 ? 1 : b) {
-    if (semiring < 0 || semiring > 4) throw Err(E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 5) throw Err(E_INVALID_ARG, "bad semiring");
   }
 
   void push(const std::string& rel, int64_t n, const int32_t* cols, const int32_t* sids, const float* probs, int64_t* first) {
@@ -423,8 +438,9 @@ struct Engine {
       f.sample.push_back(d.shared ? 0 : sids[i]);
       f.p.push_back(sr == UNIT ? 1.0f : (probs ? probs[i] : 1.0f));
       f.fid.push_back(next_fact);
-      if ((int64_t)fact_p.size() <= next_fact) fact_p.resize(next_fact + 1);
+      if ((int64_t)fact_p.size() <= next_fact) { fact_p.resize(next_fact + 1); fact_group.resize(next_fact + 1, -1); }
       fact_p[next_fact] = f.p.back();
+      fact_group[next_fact] = -1;
       next_fact++;
     }
   }
@@ -433,11 +449,18 @@ struct Engine {
   // diff-max-mult the surviving fact is the larger p, then the smaller id.
   void ingest(Rel& r, const Tuple& t, float p, int64_t fid) {
     auto it = r.find(t);
-    if (it == r.end()) { Tag g; g.p = p; g.fact = fid; r[t] = g; return; }
+    if (it == r.end()) {
+      Tag g; g.p = p; g.fact = fid;
+      if (sr == TOP1) g.proof = {fid};
+      r[t] = g;
+      return;
+    }
     Tag& g = it->second;
     if (sr == ADD_MULT) g.p = (float)((double)g.p + (double)p);
     else if (sr == MAX_MIN) { if (p > g.p) g.p = p; }
-    else if (witnessed(sr)) { if (p > g.p || (p == g.p && fid < g.fact)) { g.p = p; g.fact = fid; } }
+    else if (witnessed(sr)) {
+      if (p > g.p || (p == g.p && fid < g.fact)) { g.p = p; g.fact = fid; if (sr == TOP1) g.proof = {fid}; }
+    }
   }
 
   void run(const std::vector<int>& samples, int threads) {
@@ -500,6 +523,7 @@ struct Engine {
     std::vector<int32_t> val(nv, 0);
     std::vector<char> isb(nv, 0);
     std::vector<float> tags(r.body.size(), 1.0f);
+    std::vector<const Tag*> etag(r.body.size(), nullptr);  // top-1-proof: the body tuples' proofs
     auto vid = [&](const std::string& n) { return (int)(std::find(r.vars.begin(), r.vars.end(), n) - r.vars.begin()); };
     // statically: for atom k, bound columns = constants + vars bound by atoms < k
     std::vector<std::vector<int>> bcols(r.body.size());
@@ -545,6 +569,22 @@ struct Engine {
         float t = tags[0];                                   // ⊗ left-deep in body order
         for (size_t i = 1; i < r.body.size(); ++i) t = otimes(sr, t, tags[i]);
         cd.p = (sr == UNIT) ? 1.0f : t;
+        if (sr == TOP1) {  // ⊗ = union of the body proofs; conflict -> no candidate
+          std::vector<int64_t> u;
+          for (size_t i = 0; i < r.body.size(); ++i) {
+            std::vector<int64_t> m;
+            std::set_union(u.begin(), u.end(), etag[i]->proof.begin(), etag[i]->proof.end(), std::back_inserter(m));
+            u.swap(m);
+          }
+          for (size_t i = 0; i + 1 < u.size(); ++i)
+            for (size_t j = i + 1; j < u.size(); ++j)
+              if (fact_group[u[i]] >= 0 && fact_group[u[i]] == fact_group[u[j]]) return;  // exclusive facts
+          if (u.size() > PROOF_CAP) throw Err(E_RANGE, "a proof exceeds 300 facts (P:628)");
+          double q = 1.0;
+          for (int64_t f : u) q *= (double)fact_p[f];
+          cd.p = (float)q;
+          cd.proof.swap(u);
+        }
         cd.rule = r.index;
         cd.wv.n = (int)r.nonhead.size();
         for (size_t i = 0; i < r.nonhead.size(); ++i) cd.wv.v[i] = val[r.nonhead[i]];
@@ -564,7 +604,7 @@ struct Engine {
           if (isb[v]) { if (val[v] != e.first.v[c]) ok = false; }
           else { isb[v] = 1; val[v] = e.first.v[c]; newly.push_back(v); }
         }
-        if (ok) { tags[k] = e.second.p; rec(k + 1); }
+        if (ok) { tags[k] = e.second.p; etag[k] = &e.second; rec(k + 1); }
         for (int v : newly) isb[v] = 0;
       };
       if (!idx[k]) { for (auto& e : *versions[k]) visit(e); return; }
@@ -649,12 +689,14 @@ struct Engine {
           size_t i = 0;
           while (i < c.size()) {
             size_t j = i;
-            Tag u; u.p = c[i].p; u.rule = c[i].rule; u.wv = c[i].wv;
+            Tag u; u.p = c[i].p; u.rule = c[i].rule; u.wv = c[i].wv; u.proof = c[i].proof;
             double acc = 0.0;
             for (j = i; j < c.size() && c[j].head == c[i].head; ++j) {
               if (sr == ADD_MULT) acc += (double)c[j].p;
               else if (sr == MAX_MIN) { if (c[j].p > u.p) u.p = c[j].p; }
-              else if (witnessed(sr)) { if (c[j].p > u.p) { u.p = c[j].p; u.rule = c[j].rule; u.wv = c[j].wv; } }
+              else if (witnessed(sr)) {
+                if (c[j].p > u.p) { u.p = c[j].p; u.rule = c[j].rule; u.wv = c[j].wv; u.proof = c[j].proof; }
+              }
             }
             if (sr == ADD_MULT) u.p = (float)acc;
             if (sr == UNIT) u.p = 1.0f;
@@ -705,6 +747,16 @@ struct Engine {
       if (!kv.second.output || kv.second.input) continue;
       auto& gl = d.grads[kv.first];
       for (auto& e : d.rel[kv.first]) {
+        if (sr == TOP1) {  // ∂p/∂p_f = Π_{g in proof, g != f} p_g (fp64, ascending ids)
+          std::vector<std::pair<int64_t, float>> g;
+          for (int64_t f : e.second.proof) {
+            double v = 1.0;
+            for (int64_t h : e.second.proof) if (h != f) v *= (double)fact_p[h];
+            g.push_back({f, (float)v});
+          }
+          gl.push_back(g);
+          continue;
+        }
         std::map<int64_t, int> mult;
         walk(d, kv.first, e.first, mult, 0);
         std::vector<std::pair<int64_t, float>> g;
@@ -772,6 +824,15 @@ int orc_num_strata(void* hv) { return (int)((OrcHandle*)hv)->e->prog.strata.size
 int orc_push(void* hv, const char* rel, int64_t n, const int32_t* cols, const int32_t* sids, const float* probs, int64_t* first) {
   OrcHandle* h = (OrcHandle*)hv;
   return guard(h, [&]() { h->e->push(rel, n, cols, sids, probs, first); });
+}
+
+// top-1-proof exclusion groups of facts [first, first + n) (-1 = none)
+int orc_set_groups(void* hv, int64_t first, int64_t n, const int32_t* groups) {
+  OrcHandle* h = (OrcHandle*)hv;
+  return guard(h, [&]() {
+    if (first < 0 || first + n > (int64_t)h->e->fact_group.size()) throw Err(E_INVALID_ARG, "fact range");
+    for (int64_t i = 0; i < n; ++i) h->e->fact_group[first + i] = groups[i];
+  });
 }
 
 int orc_run(void* hv, int nsamples, const int32_t* samples, int threads) {
