@@ -63,13 +63,22 @@ typedef enum {
  *                        min.  Tags equal MAX_MIN_PROB's; the gradient is one-hot on
  *                        the winning derivation's minimum leaf (smallest fact id on
  *                        ties): "the differentiable versions of the probabilistic
- *                        semirings", PAPER.md:617 (§3.5)                  */
+ *                        semirings", PAPER.md:617 (§3.5)
+ *   DIFF_TOP1_PROOFS   : one proof per tuple — a set of at most 300 input facts
+ *                         — with p = Π over the set (fp64, ascending fact
+ *                        ids, rounded once); ⊗ = union, dropped when two facts of
+ *                        one exclusion group meet (lobster_facts_groups); ⊕ = the
+ *                        more likely proof, tie rules as DIFF_MAX_MULT_PROB;
+ *                        gradient ∂p/∂p_f = Π of the proof's other facts
+ *                        (§2, 617-628 §3.5).  GPU: rules may read
+ *                        their own stratum at most once (linear recursion)  */
 typedef enum {
   LOBSTER_UNIT = 0,
   LOBSTER_MAX_MIN_PROB = 1,
   LOBSTER_ADD_MULT_PROB = 2,
   LOBSTER_DIFF_MAX_MULT_PROB = 3,
-  LOBSTER_DIFF_MAX_MIN_PROB = 4
+  LOBSTER_DIFF_MAX_MIN_PROB = 4,
+  LOBSTER_DIFF_TOP1_PROOFS = 5
 } lobster_semiring;
 
 typedef struct {
@@ -167,7 +176,8 @@ typedef struct {
   const float* probs;             /* n; NULL under UNIT; add-mult is unclamped      */
   const int64_t* sample_offsets;  /* B+1 (B = this context's samples: batch_size, or hi-lo
                                      when sharded): rows of sample lo+s are [off[s], off[s+1]) */
-  const int64_t* grad_offsets;    /* n+1, DIFF_* output relations only, else NULL            */
+  const int64_t* grad_offsets;    /* n+1, DIFF_* output relations only, else NULL (for
+                                     DIFF_TOP1_PROOFS the ids are the tuple's proof)         */
   const int64_t* grad_fact_ids;   /* grad_offsets[n] ids, ascending within each row         */
   const float* grad_values;       /* ∂probs[row] / ∂p(fact), fp64-accumulated, rounded to fp32 */
 } lobster_output;
@@ -185,6 +195,15 @@ lobster_status lobster_output_get(lobster_ctx* ctx, const char* relation, int32_
  * INVALID_ARG (not an output relation / not DIFF_MAX_MULT_PROB). */
 lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation,
                                        const float* upstream, float* grad_facts);
+
+/* diff-top-1-proofs exclusion groups ("ensures that no conflict is
+ * present"): facts [first_fact_id, first_fact_id + n) of the current database
+ * get group_ids (n int32, host or device; -1 = none).  Two facts with the same
+ * group id >= 0 are mutually exclusive: a conjunction holding both is a
+ * conflict and yields no proof.  Call after lobster_facts_push, before
+ * lobster_run.  Ignored by the other semirings.  Errors: STATE (no program, or
+ * after run), INVALID_ARG (range outside the pushed facts). */
+lobster_status lobster_facts_groups(lobster_ctx* ctx, int64_t first_fact_id, int64_t n, const int32_t* group_ids);
 
 /* Number of facts pushed into the current database (size of grad_facts). */
 int64_t lobster_num_facts(const lobster_ctx* ctx);

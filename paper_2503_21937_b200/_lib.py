@@ -14,9 +14,10 @@ LIB_PATH = os.path.join(HERE, "liblobster.so")
 OK, E_INVALID_ARG, E_PARSE, E_SCHEMA, E_RANGE, E_STATE, E_OOM, E_ITER_CAP, E_CUDA, E_NCCL = range(10)
 STATUS_NAMES = ["OK", "INVALID_ARG", "PARSE", "SCHEMA", "RANGE", "STATE", "OOM", "ITER_CAP", "CUDA", "NCCL"]
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB = 0, 1, 2, 3, 4
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
 SEMIRINGS = {"unit": UNIT, "max-min-prob": MAX_MIN_PROB, "add-mult-prob": ADD_MULT_PROB,
-             "diff-max-mult-prob": DIFF_MAX_MULT_PROB, "diff-max-min-prob": DIFF_MAX_MIN_PROB}
+             "diff-max-mult-prob": DIFF_MAX_MULT_PROB, "diff-max-min-prob": DIFF_MAX_MIN_PROB,
+             "diff-top-1-proofs": DIFF_TOP1_PROOFS}
 
 
 class Options(ctypes.Structure):
@@ -50,7 +51,7 @@ class Output(ctypes.Structure):
 
 EXPORTS = ["lobster_create", "lobster_destroy", "lobster_last_error", "lobster_program_load",
            "lobster_facts_push", "lobster_run", "lobster_output_get", "lobster_output_backward",
-           "lobster_num_facts", "lobster_kernel_launches"]
+           "lobster_num_facts", "lobster_kernel_launches", "lobster_facts_groups"]
 
 _lib = None
 
@@ -86,5 +87,7 @@ def load():
     L.lobster_num_facts.restype = ctypes.c_int64
     L.lobster_kernel_launches.argtypes = []
     L.lobster_kernel_launches.restype = ctypes.c_int64
+    L.lobster_facts_groups.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp]
+    L.lobster_facts_groups.restype = ctypes.c_int
     _lib = L
     return L

@@ -142,6 +142,11 @@ struct RelState {
   DBuf<float> acc_p, acc_gval;
   DBuf<int64_t> acc_goff, acc_gfid;
   int64_t acc_n = 0, acc_ng = 0;
+  // diff-top-1-proofs: proof index (keys = the stored tuples, offset + length
+  // into the pool of fact ids) and this round's Δ' proof handles
+  DBuf<uint64_t> pkey, pof, pkey2, pof2, dof;
+  DBuf<uint32_t> pln, pln2, dln, pool, pool2;
+  int64_t npx = 0, pool_n = 0;
 
   void bind(cudaStream_t st) {
     for (auto* b : {&key, &key2, &dkey, &okey, &ckey, &ckey2, &cv64, &cv64b}) b->bind(st);
@@ -162,6 +167,8 @@ struct RelState {
     acc_gval.bind(st);
     acc_goff.bind(st);
     acc_gfid.bind(st);
+    for (auto* b : {&pkey, &pof, &pkey2, &pof2, &dof}) b->bind(st);
+    for (auto* b : {&pln, &pln2, &dln, &pool, &pool2}) b->bind(st);
     in.sid.bind(st);
     in.p.bind(st);
     in.fid.bind(st);
@@ -211,6 +218,9 @@ struct Ctx {
   bool loaded = false, ran = false, dirty = false;
   int semi = 0;
   bool omin = false;  // diff-max-min-prob (semi == S_MAXMULT internally)
+  bool top1 = false;  // diff-top-1-proofs (semi == S_MAXMULT internally; sorted stores, k_top1.cu)
+  DBuf<int32_t> fact_group;  // top-1-proof exclusion group per fact (-1: none)
+  bool has_groups = false;
   Program prog;
   std::vector<std::unique_ptr<RelState>> rels;
   int64_t next_fact = 0;
@@ -360,6 +370,7 @@ struct Ctx {
     cuda_check(cudaMallocHost(&hbuf, 64), "cudaMallocHost");
     arena.bind(st);
     fact_p.bind(st);
+    fact_group.bind(st);
     for (auto* b : {&sl.Rb, &sl.Nb, &sl.dt, &sl.dwi, &sl.dbits, &sl.deg, &sl.pos, &sl.cnt, &sl.scan}) b->bind(st);
     sl.tup.bind(st);
     if (opt.arena_bytes > 0) arena.reserve_initial((size_t)opt.arena_bytes);
@@ -368,14 +379,15 @@ struct Ctx {
   // ---------------------------------------------------------- program load
   void load(const char* text, int semiring) {
     if (loaded) throw Failure(LOBSTER_E_STATE, "program already loaded");
-    if (semiring < 0 || semiring > 4) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 5) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
     if (!text) throw Failure(LOBSTER_E_INVALID_ARG, "program text is NULL");
     prog = parse_program(text);
     // diff-max-min-prob runs on the max-mult machinery (packed (p, stamp,
     // witness) words, strict improvement, tie rules 8a/8b) with ⊗ = min and a
     // one-hot gradient (reading "diff-max-min")
     omin = semiring == LOBSTER_DIFF_MAX_MIN_PROB;
-    semi = omin ? S_MAXMULT : semiring;
+    top1 = semiring == LOBSTER_DIFF_TOP1_PROOFS;
+    semi = (omin || top1) ? S_MAXMULT : semiring;
     for (auto& r : prog.rels)
       if (r.arity > MAXARITY) throw Failure(LOBSTER_E_PARSE, "relation " + r.name + ": arity above 8 is unsupported");
     for (auto& R : prog.rules) {
@@ -419,7 +431,20 @@ struct Ctx {
     }
     static_idx.clear();
     next_fact = 0;
+    has_groups = false;
     ran = false;
+  }
+
+  // top-1-proof exclusion groups of facts [first, first + n)
+  void set_groups(int64_t first, int64_t n, const int32_t* groups) {
+    if (!loaded) throw Failure(LOBSTER_E_STATE, "facts_groups before program_load");
+    if (n < 0 || first < 0 || first + n > next_fact || (n > 0 && !groups))
+      throw Failure(LOBSTER_E_INVALID_ARG, "group range outside the pushed facts");
+    if (ran) throw Failure(LOBSTER_E_STATE, "facts_groups after run (push the next database first)");
+    if (n == 0) return;
+    cuda_check(cudaMemcpyAsync(fact_group.ptr() + first, groups, n * 4, cudaMemcpyDefault, st), "push groups");
+    has_groups = true;
+    dirty = true;
   }
 
   void push(const char* relname, int64_t n, const int32_t* const* columns, const int32_t* sample_ids,
@@ -457,6 +482,8 @@ struct Ctx {
       else
         launch_fill_f32(S.in.p.ptr() + base, n, 1.0f, st);
       launch_iota_i32(S.in.fid.ptr() + base, n, (int32_t)next_fact, st);
+      fact_group.reserve(next_fact + n, next_fact);  // no exclusion group until lobster_facts_groups
+      cuda_check(cudaMemsetAsync(fact_group.ptr() + next_fact, 0xff, n * 4, st), "memset");
       // validation (reading: S:46 range errors)
       uint32_t* flags = reinterpret_cast<uint32_t*>(hbuf);
       uint32_t* dflag = arena.get<uint32_t>(1);
@@ -1228,7 +1255,7 @@ struct Ctx {
 
   // u32 candidate keys whenever the head's packed key fits 31 bits (dense stores
   // always): the dead key ~0 still sorts last, and sorts move 4 B less per key
-  bool c32(const RelState& H) const { return H.dense || (H.L.total <= 31 && !getenv("LOBSTER_C64")); }
+  bool c32(const RelState& H) const { return H.dense || (H.L.total <= 31 && !top1 && !getenv("LOBSTER_C64")); }
 
   void* cand_key(RelState& H) {
     return c32(H) ? (void*)(H.ckey32.ptr() + H.nc) : (void*)(H.ckey.ptr() + H.nc);
@@ -1382,7 +1409,7 @@ struct Ctx {
     S.dense = false;
     S.direct = false;
     S.lazy = false;
-    if (S.build_local || S.L.total > 30 || force_sorted) return;
+    if (S.build_local || S.L.total > 30 || force_sorted || top1) return;
     if (semi != S_ADDMULT && !force_sort_dedup) {  // idempotent ⊕: fused direct store
       const int64_t ns = (int64_t)1 << S.L.total;
       const size_t bytes = semi == S_UNIT ? (size_t)((ns + 31) / 32) * 4 : (size_t)ns * (semi == S_MAXMULT ? 8 : 4);
@@ -1484,6 +1511,7 @@ struct Ctx {
     const int64_t nc = S.nc;
     S.nc = 0;
     if (nc == 0) { S.nd = 0; return 0; }
+    if (top1) top1_candidates(r, S, nc);
     const int tb = S.L.total + 1;  // +1 bit: KEY_DEAD sorts after every key
     if (c32(S)) return settle_sorted32(S, nc, tb);
     S.ckey2.reserve(nc);
@@ -1878,6 +1906,196 @@ struct Ctx {
     return 0;
   }
 
+  // ------------------------------------------------ diff-top-1-proofs
+  // (k_top1.cu).  Linear rules only: a rule reads at most
+  // one relation of its own stratum, whose proofs are then those of Δ (the
+  // relation's proof index at round start); every other atom is external.
+  std::vector<WalkRule> top1_rules;
+  std::vector<int> top1_base;
+  void top1_begin_stratum(const std::vector<int>& strat) {
+    std::set<int> local(strat.begin(), strat.end());
+    for (const Rule& R : prog.rules) {
+      if (!local.count(R.head_rel)) continue;
+      int nloc = 0;
+      for (auto& a : R.body) nloc += local.count(a.rel) ? 1 : 0;
+      if (nloc > 1)
+        throw Failure(LOBSTER_E_SCHEMA, "diff-top-1-proofs: a rule for " + prog.rels[R.head_rel].name +
+                                            " reads its own stratum twice (linear recursion only on the GPU)");
+    }
+    for (int r : strat) {
+      rels[r]->npx = 0;
+      rels[r]->pool_n = 0;
+    }
+    if (top1_rules.empty()) build_walk_rules(top1_rules, top1_base);
+  }
+
+  // device tables of every relation's proof source (rebuilt per use: buffers move)
+  ProofTables top1_tables() {
+    const int nr = (int)prog.rels.size();
+    std::vector<ProofRel> pr(nr);
+    for (int r = 0; r < nr; ++r) {
+      RelState& S = *rels[r];
+      ProofRel& q = pr[r];
+      std::memset(&q, 0, sizeof(q));
+      if (prog.rels[r].input) {
+        q.key = S.key.ptr();
+        q.n = S.n;
+        q.fid = S.fid.ptr();
+      } else {
+        q.key = S.pkey.ptr();
+        q.n = S.npx;
+        q.pof = S.pof.ptr();
+        q.pln = S.pln.ptr();
+        q.pool = S.pool.ptr();
+      }
+      q.has_sample = S.L.has_sample ? 1 : 0;
+      q.sshift = (uint8_t)S.L.sshift;
+      for (int c = 0; c < prog.rels[r].arity; ++c) {
+        q.shift[c] = (uint8_t)S.L.shift[c];
+        q.bits[c] = (uint8_t)S.L.bits[c];
+        q.min[c] = S.L.mins[c];
+      }
+    }
+    ProofTables T{};
+    T.rels = arena.get<ProofRel>(nr);
+    T.rules = arena.get<WalkRule>((int64_t)top1_rules.size());
+    T.rule_base = arena.get<int>(nr);
+    T.rule_bits = arena.get<int>(nr);
+    cuda_check(cudaMemcpyAsync(T.rels, pr.data(), nr * sizeof(ProofRel), cudaMemcpyHostToDevice, st), "H2D");
+    if (!top1_rules.empty())
+      cuda_check(cudaMemcpyAsync(T.rules, top1_rules.data(), top1_rules.size() * sizeof(WalkRule),
+                                 cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(T.rule_base, top1_base.data(), nr * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(T.rule_bits, rule_bits.data(), nr * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    T.fact_p = fact_p.ptr();
+    T.group = has_groups ? fact_group.ptr() : nullptr;
+    T.cap = 300;
+    return T;
+  }
+
+  void top1_check(int* d_err) {
+    const int e = read_dev(d_err);
+    if (e & 8) throw Failure(LOBSTER_E_RANGE, "diff-top-1-proofs: a proof exceeds 300 facts (P:628)");
+    if (e) throw Failure(LOBSTER_E_CUDA, "top-1-proof: inconsistent body tuple (code " + std::to_string(e) + ")");
+  }
+
+  // candidates: the union proof's p replaces the ⊗ of the body tags; conflicting
+  // candidates are dropped (dead keys) before the sort
+  void top1_candidates(int r, RelState& S, int64_t nc) {
+    Phase ph(this, 2);
+    ProofTables T = top1_tables();
+    int* d_err = arena.get<int>(1);
+    cuda_check(cudaMemsetAsync(d_err, 0, 4, st), "memset");
+    launch_top1_cand(T, r, S.ckey.ptr(), S.cv64.ptr(), nc, d_err, st);
+    kcheck("top1 candidates");
+    top1_check(d_err);
+  }
+
+  // after every relation of the round settled: Δ' proofs appended to the
+  // pools, proof indexes updated (in place for improved tuples, merged for new)
+  void top1_commit(const std::vector<int>& strat) {
+    ProofTables T = top1_tables();  // round-start indexes: all Δ' unions read them
+    int* d_err = arena.get<int>(1);
+    cuda_check(cudaMemsetAsync(d_err, 0, 4, st), "memset");
+    std::vector<int64_t> need(strat.size(), 0);
+    for (size_t q = 0; q < strat.size(); ++q) {  // proof lengths -> offsets in the pool
+      RelState& S = *rels[strat[q]];
+      const int64_t nd = S.nd;
+      if (nd <= 0) continue;
+      S.dln.reserve(nd);
+      S.dof.reserve(nd + 1);
+      launch_top1_delta(T, strat[q], S.dkey.ptr(), S.dw.ptr(), nd, S.dln.ptr(), nullptr, nullptr, d_err, st);
+      uint64_t* len64 = arena.get<uint64_t>(nd);
+      launch_widen_u32(S.dln.ptr(), nd, len64, st);
+      exclusive_scan<uint64_t>(len64, S.dof.ptr(), nd, S.dof.ptr() + nd, arena.alloc(scan_tmp_bytes<uint64_t>(nd)), st);
+      kcheck("top1 lengths");
+    }
+    for (size_t q = 0; q < strat.size(); ++q) {
+      RelState& S = *rels[strat[q]];
+      if (S.nd > 0) need[q] = (int64_t)read_dev(S.dof.ptr() + S.nd);
+    }
+    top1_check(d_err);
+    for (size_t q = 0; q < strat.size(); ++q) {
+      RelState& S = *rels[strat[q]];
+      const int64_t nd = S.nd;
+      if (nd <= 0) continue;
+      // the pool grows x1.5 and keeps its contents; live proofs are re-packed
+      // when the garbage (proofs of since-improved tuples) dominates
+      S.pool.reserve(S.pool_n + need[q], S.pool_n);
+      launch_add_i64(reinterpret_cast<const int64_t*>(S.dof.ptr()), nd, S.pool_n,
+                     reinterpret_cast<int64_t*>(S.dof.ptr()), st);
+      launch_top1_delta(T, strat[q], S.dkey.ptr(), S.dw.ptr(), nd, nullptr, S.dof.ptr(), S.pool.ptr(), d_err, st);
+      S.pool_n += need[q];
+      // proof index: improved tuples in place, new tuples merged by rank
+      uint32_t* isnew = arena.get<uint32_t>(nd);
+      uint32_t* pos = arena.get<uint32_t>(nd + 1);
+      launch_top1_update(S.pkey.ptr(), S.npx, S.pof.ptr(), S.pln.ptr(), S.dkey.ptr(), S.dof.ptr(), S.dln.ptr(), nd,
+                         isnew, st);
+      exclusive_scan<uint32_t>(isnew, pos, nd, pos + nd, arena.alloc(scan_tmp_bytes<uint32_t>(nd)), st);
+      const int64_t nnew = (int64_t)read_dev(pos + nd);
+      if (nnew > 0) {
+        uint64_t* nk = arena.get<uint64_t>(nnew);
+        uint64_t* no = arena.get<uint64_t>(nnew);
+        uint32_t* nl = arena.get<uint32_t>(nnew);
+        launch_top1_compact(S.dkey.ptr(), S.dof.ptr(), S.dln.ptr(), isnew, pos, nd, nk, no, nl, st);
+        const int64_t nn = S.npx + nnew;
+        S.pkey2.reserve(nn);
+        S.pof2.reserve(nn);
+        S.pln2.reserve(nn);
+        launch_top1_merge(S.pkey.ptr(), S.pof.ptr(), S.pln.ptr(), S.npx, nk, no, nl, nnew, S.pkey2.ptr(), S.pof2.ptr(),
+                          S.pln2.ptr(), st);
+        S.pkey.swap(S.pkey2);
+        S.pof.swap(S.pof2);
+        S.pln.swap(S.pln2);
+        S.npx = nn;
+      }
+      kcheck("top1 commit");
+      top1_maybe_compact(S);
+    }
+    top1_check(d_err);
+  }
+
+  void top1_maybe_compact(RelState& S) {
+    if (S.pool_n < ((int64_t)1 << 20) || S.npx == 0) return;
+    uint64_t* len64 = arena.get<uint64_t>(S.npx);
+    uint64_t* noff = arena.get<uint64_t>(S.npx + 1);
+    launch_widen_u32(S.pln.ptr(), S.npx, len64, st);
+    exclusive_scan<uint64_t>(len64, noff, S.npx, noff + S.npx, arena.alloc(scan_tmp_bytes<uint64_t>(S.npx)), st);
+    const int64_t live = (int64_t)read_dev(noff + S.npx);
+    if (2 * live >= S.pool_n) return;
+    S.pool2.reserve(live);
+    launch_top1_gather(S.pool.ptr(), S.pof.ptr(), S.pln.ptr(), noff, S.npx, S.pool2.ptr(), st);
+    cuda_check(cudaMemcpyAsync(S.pof.ptr(), noff, S.npx * 8, cudaMemcpyDeviceToDevice, st), "copy");
+    S.pool.swap(S.pool2);
+    S.pool_n = live;
+    kcheck("top1 pool compaction");
+  }
+
+  // gradients of every output relation straight from its proofs
+  void top1_gradients() {
+    for (size_t r = 0; r < prog.rels.size(); ++r) {
+      if (!prog.rels[r].output || prog.rels[r].input) continue;
+      RelState& S = *rels[r];
+      ensure_sorted(S);
+      const int64_t n = S.n;
+      if (n != S.npx) throw Failure(LOBSTER_E_CUDA, "top-1-proof: proof index out of step with the relation");
+      S.goff.reserve(n + 1);
+      uint64_t* len64 = arena.get<uint64_t>(n);
+      uint64_t* noff = arena.get<uint64_t>(n + 1);
+      if (n) launch_widen_u32(S.pln.ptr(), n, len64, st);
+      exclusive_scan<uint64_t>(len64, noff, n, noff + n, arena.alloc(scan_tmp_bytes<uint64_t>(n)), st);
+      const int64_t ng = n ? (int64_t)read_dev(noff + n) : 0;
+      S.gfid.reserve(ng);
+      S.gval.reserve(ng);
+      double* scratch = arena.get<double>(ng);
+      launch_top1_grad(S.pool.ptr(), S.pof.ptr(), S.pln.ptr(), noff, n, fact_p.ptr(), S.goff.ptr(), S.gfid.ptr(),
+                       S.gval.ptr(), scratch, st);
+      kcheck("top1 gradients");
+      S.ng = ng;
+      S.has_grad = true;
+    }
+  }
+
   // ------------------------------------------------ bit-sliced frontier
   // A stratum qualifies when: unit semiring; one batched unary relation R in a
   // direct (bitmap) store; every rule of R is either all-external (the seed
@@ -2018,6 +2236,7 @@ struct Ctx {
     for (size_t si = 0; si < prog.strata.size(); ++si) {
       const std::vector<int>& strat = prog.strata[si];
       std::set<int> local(strat.begin(), strat.end());
+      if (top1) top1_begin_stratum(strat);
       for (int r : strat) {
         RelState& S = *rels[r];
         S.n = S.nd = S.no = S.nc = 0;
@@ -2091,6 +2310,7 @@ struct Ctx {
             }
           }
           for (int r : strat) changed += settle(r);
+          if (top1) top1_commit(strat);
         }
         if (async) {  // |Δ'| of this round -> pinned ring; poll earlier rounds without stalling the GPU
           pending.push_back({rounds, ring_seq});
@@ -2237,8 +2457,48 @@ struct Ctx {
     if (round_cap_hit) throw Failure(LOBSTER_E_ITER_CAP, "max_iters rounds reached");
   }
 
+  // per relation, its rules in local order: how a (head key, witness) names
+  // the body tuples of the derivation (witness walk, top-1-proof unions)
+  void build_walk_rules(std::vector<WalkRule>& ordered, std::vector<int>& base) {
+    const int nr = (int)prog.rels.size();
+    base.assign(nr, 0);
+    {
+      std::vector<int> cnt(nr, 0);
+      for (auto& R : prog.rules) cnt[R.head_rel]++;
+      int acc = 0;
+      for (int r = 0; r < nr; ++r) { base[r] = acc; acc += cnt[r]; }
+    }
+    ordered.assign(prog.rules.size(), WalkRule{});
+    for (auto& R : prog.rules) {
+      WalkRule wrl;
+      std::memset(&wrl, 0, sizeof(wrl));
+      wrl.natoms = (int)R.body.size();
+      for (int a = 0; a < wrl.natoms; ++a) {
+        wrl.atom[a].rel = R.body[a].rel;
+        wrl.atom[a].ncols = (int)R.body[a].args.size();
+        for (int c = 0; c < wrl.atom[a].ncols; ++c) {
+          wrl.atom[a].var[c] = (int8_t)R.body[a].args[c].var;
+          wrl.atom[a].cst[c] = R.body[a].args[c].cst;
+        }
+      }
+      wrl.nvars = (int)R.var_names.size();
+      for (int v = 0; v < 16; ++v) { wrl.head_col[v] = -1; wrl.wfield[v] = -1; }
+      for (size_t c = 0; c < R.head.size(); ++c)
+        if (R.head[c].is_var() && wrl.head_col[R.head[c].var] < 0) wrl.head_col[R.head[c].var] = (int8_t)c;
+      for (size_t i = 0; i < R.nonhead.size(); ++i) {
+        int v = R.nonhead[i];
+        wrl.wfield[v] = (int8_t)i;
+        wrl.wshift[v] = (uint8_t)wshift[R.global_index][i];
+        wrl.wbits[v] = (uint8_t)wbits[R.global_index][i];
+        wrl.wmin[v] = (int32_t)class_min[R.var_class[v]];
+      }
+      ordered[base[R.head_rel] + R.local_index] = wrl;
+    }
+  }
+
   // --------------------------------------------------------- gradients (A11)
   void gradients() {
+    if (top1) return top1_gradients();
     const int nr = (int)prog.rels.size();
     for (int r = 0; r < nr; ++r)  // walks start from the output relations' sorted rows
       if (prog.rels[r].output) ensure_sorted(*rels[r]);
@@ -2278,40 +2538,9 @@ struct Ctx {
         w.min[c] = S.L.mins[c];
       }
     }
-    std::vector<WalkRule> rules(prog.rules.size());
-    std::vector<int> base(nr, 0);
-    {
-      std::vector<int> cnt(nr, 0);
-      for (auto& R : prog.rules) cnt[R.head_rel]++;
-      int acc = 0;
-      for (int r = 0; r < nr; ++r) { base[r] = acc; acc += cnt[r]; }
-    }
-    std::vector<WalkRule> ordered(prog.rules.size());
-    for (auto& R : prog.rules) {
-      WalkRule wrl;
-      std::memset(&wrl, 0, sizeof(wrl));
-      wrl.natoms = (int)R.body.size();
-      for (int a = 0; a < wrl.natoms; ++a) {
-        wrl.atom[a].rel = R.body[a].rel;
-        wrl.atom[a].ncols = (int)R.body[a].args.size();
-        for (int c = 0; c < wrl.atom[a].ncols; ++c) {
-          wrl.atom[a].var[c] = (int8_t)R.body[a].args[c].var;
-          wrl.atom[a].cst[c] = R.body[a].args[c].cst;
-        }
-      }
-      wrl.nvars = (int)R.var_names.size();
-      for (int v = 0; v < 16; ++v) { wrl.head_col[v] = -1; wrl.wfield[v] = -1; }
-      for (size_t c = 0; c < R.head.size(); ++c)
-        if (R.head[c].is_var() && wrl.head_col[R.head[c].var] < 0) wrl.head_col[R.head[c].var] = (int8_t)c;
-      for (size_t i = 0; i < R.nonhead.size(); ++i) {
-        int v = R.nonhead[i];
-        wrl.wfield[v] = (int8_t)i;
-        wrl.wshift[v] = (uint8_t)wshift[R.global_index][i];
-        wrl.wbits[v] = (uint8_t)wbits[R.global_index][i];
-        wrl.wmin[v] = (int32_t)class_min[R.var_class[v]];
-      }
-      ordered[base[R.head_rel] + R.local_index] = wrl;
-    }
+    std::vector<WalkRule> ordered;
+    std::vector<int> base;
+    build_walk_rules(ordered, base);
     WalkRel* d_rels = arena.get<WalkRel>(nr);
     WalkRule* d_rules = arena.get<WalkRule>((int64_t)ordered.size());
     int* d_base = arena.get<int>(nr);
@@ -2637,6 +2866,10 @@ lobster_status lobster_output_backward(lobster_ctx* ctx, const char* relation, c
 }
 
 int64_t lobster_num_facts(const lobster_ctx* ctx) { return ctx ? ctx->c.next_fact : 0; }
+
+lobster_status lobster_facts_groups(lobster_ctx* ctx, int64_t first_fact_id, int64_t n, const int32_t* group_ids) {
+  return guarded(ctx, [&]() { ctx->c.set_groups(first_fact_id, n, group_ids); });
+}
 
 int64_t lobster_kernel_launches(void) { return lob::g_launches.load(); }
 

@@ -370,6 +370,46 @@ void launch_grad(const uint64_t* sorted_tf, const uint32_t* pos, int64_t nleaf, 
                  int64_t ntup, const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
                  cudaStream_t st);
 
+// ---- diff-top-1-proofs (k_top1.cu) ----
+struct ProofRel {
+  const uint64_t* key;   // sorted keys of the relation's stored tuples (input rows / proof index)
+  int64_t n;
+  const int32_t* fid;    // input relation: fact id per row (proof = {fid}); else null
+  const uint64_t* pof;   // IDB: proof offset into pool, per key
+  const uint32_t* pln;   //      proof length
+  const uint32_t* pool;
+  int has_sample;
+  uint8_t sshift;
+  uint8_t shift[8], bits[8];
+  int32_t min[8];
+};
+struct ProofTables {
+  ProofRel* rels;
+  WalkRule* rules;
+  int* rule_base;
+  int* rule_bits;
+  const float* fact_p;
+  const int32_t* group;  // nullable: exclusion group per fact (-1 none)
+  int cap;               // proof size limit (300)
+};
+void launch_top1_cand(const ProofTables& T, int hrel, uint64_t* key, uint64_t* val, int64_t n, int* err,
+                      cudaStream_t st);
+void launch_top1_delta(const ProofTables& T, int hrel, const uint64_t* key, const uint32_t* w, int64_t n,
+                       uint32_t* len, const uint64_t* offs, uint32_t* pool, int* err, cudaStream_t st);
+void launch_top1_update(const uint64_t* pkey, int64_t np, uint64_t* pof, uint32_t* pln, const uint64_t* dkey,
+                        const uint64_t* dof, const uint32_t* dln, int64_t nd, uint32_t* isnew, cudaStream_t st);
+void launch_top1_compact(const uint64_t* dkey, const uint64_t* dof, const uint32_t* dln, const uint32_t* isnew,
+                         const uint32_t* pos, int64_t nd, uint64_t* nkey, uint64_t* nof, uint32_t* nln,
+                         cudaStream_t st);
+void launch_top1_merge(const uint64_t* akey, const uint64_t* aof, const uint32_t* aln, int64_t na,
+                       const uint64_t* bkey, const uint64_t* bof, const uint32_t* bln, int64_t nb, uint64_t* okey,
+                       uint64_t* oof, uint32_t* oln, cudaStream_t st);
+void launch_top1_gather(const uint32_t* pool, const uint64_t* pof, const uint32_t* pln, const uint64_t* noff,
+                        int64_t n, uint32_t* npool, cudaStream_t st);
+void launch_top1_grad(const uint32_t* pool, const uint64_t* pof, const uint32_t* pln, const uint64_t* noff, int64_t n,
+                      const float* fact_p, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
+                      cudaStream_t st);
+
 // diff-max-min: one-hot gradient on each tuple's minimum leaf (goff[t] = t)
 void launch_grad_onehot(const uint64_t* sorted_tf, int64_t nleaf, const float* fact_p, int64_t ntup,
                         const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, cudaStream_t st);

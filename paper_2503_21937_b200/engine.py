@@ -164,6 +164,12 @@ class Engine:
         del keep, k1, k2
         return first.value
 
+    def facts_groups(self, first_fact_id: int, group_ids) -> None:
+        """top-1-proof exclusion groups of facts [first, first + n) (-1 = none)."""
+        g = _as_i32(group_ids)
+        ptr, keep = _ptr(g)
+        self._check(self._L.lobster_facts_groups(self._h, int(first_fact_id), int(len(g)), ptr))
+
     def push_facts(self, facts: Dict[str, object]) -> Dict[str, int]:
         """Push a dict rel -> workloads.Facts (cols, sample_ids, probs) in dict order."""
         return {rel: self.push(rel, f.cols, f.sample_ids, f.probs) for rel, f in facts.items()}
@@ -196,7 +202,7 @@ class Engine:
             out = RelationOutput(n, ar, _np_view(o.sample_ids, n, np.int32, copy), cols,
                                  _np_view(o.probs, n, np.float32, copy) if self.semiring != _lib.UNIT else None,
                                  _np_view(o.sample_offsets, self.local_batch + 1, np.int64, copy))
-            if o.grad_offsets or (self.semiring in (_lib.DIFF_MAX_MULT_PROB, _lib.DIFF_MAX_MIN_PROB) and n == 0 and o.grad_offsets is not None):
+            if o.grad_offsets or (self.semiring in (_lib.DIFF_MAX_MULT_PROB, _lib.DIFF_MAX_MIN_PROB, _lib.DIFF_TOP1_PROOFS) and n == 0 and o.grad_offsets is not None):
                 goff = _np_view(o.grad_offsets, n + 1, np.int64, copy) if n else np.zeros(1, np.int64)
                 ng = int(goff[-1]) if n else 0
                 out.grad_offsets = goff

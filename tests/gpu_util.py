@@ -5,7 +5,7 @@ import numpy as np
 
 import oracle
 
-REL_TOL = {0: 0.0, 1: 0.0, 2: 1e-5, 3: 0.0, 4: 0.0}   # unit / max-min / max-mult / diff-max-min bit-exact; add-mult 1e-5
+REL_TOL = {0: 0.0, 1: 0.0, 2: 1e-5, 3: 0.0, 4: 0.0, 5: 0.0}   # unit / max-min / max-mult / diff-max-min bit-exact; add-mult 1e-5
 GRAD_TOL = 1e-6
 
 
@@ -67,7 +67,7 @@ def assert_parity(eng, res, rel, semiring, samples=None, check_grads=True):
         else:
             err = np.abs(gp.astype(np.float64) - r.tags) / np.maximum(np.abs(r.tags.astype(np.float64)), 1e-30)
             assert float(err.max(initial=0.0)) <= tol, f"{rel}: max rel err {err.max()}"
-    if semiring in (3, 4) and check_grads and r.grad_offsets is not None:
+    if semiring in (3, 4, 5) and check_grads and r.grad_offsets is not None:
         assert o.grad_offsets is not None, "GPU produced no gradients"
         goff = np.asarray(o.grad_offsets, np.int64)
         glen = goff[idx + 1] - goff[idx]

@@ -60,7 +60,7 @@ PROGRAMS = {
     "reach": REACH_PROGRAM,
 }
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB = 0, 1, 2, 3, 4
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
 
 
 @dataclass
