@@ -57,6 +57,10 @@ CONFIGS = {
                make=lambda b, s: G.grid_workload(32, b, 2, G.DIFF_MAX_MULT_PROB, samples=s, name="C2"),
                desc="C2: Pathfinder-shaped 32x32 lattice connectivity (Fig. 3c program), batch 64 per GPU, "
                     "max-min-prob + diff-max-mult-prob with input-fact gradients"),
+    "C2P": dict(per_gpu=64, semirings=[G.DIFF_TOP1_PROOFS], out="endpoints_connected",
+                make=lambda b, s: G.grid_workload(32, b, 2, G.DIFF_TOP1_PROOFS, samples=s, name="C2P"),
+                desc="C2 under the paper's own Pathfinder provenance (P:290): diff-top-1-proofs, proofs of "
+                     "<= 300 facts with input-fact gradients, 32x32 lattice, batch 64 per GPU"),
     "C1": dict(per_gpu=1, semirings=[G.ADD_MULT_PROB], out="path",
                make=lambda b, s: G.c1_workload(G.ADD_MULT_PROB),
                desc="C1: transitive closure over the 6-node dyadic DAG, add-mult-prob (latency-bound)"),
@@ -234,7 +238,8 @@ def cpu_baseline(cfg_name: str, threads: int, sr_indices=None, nsamples: int = 0
             res = oracle.run(w.program, sr, w.batch_size, w.facts, samples=list(range(n)), threads=threads)
             tuples += sum(len(r) for r in res.relations.values())
     dt = time.perf_counter() - t
-    names = {0: "unit", 1: "max-min-prob", 2: "add-mult-prob", 3: "diff-max-mult-prob"}
+    names = {0: "unit", 1: "max-min-prob", 2: "add-mult-prob", 3: "diff-max-mult-prob", 4: "diff-max-min-prob",
+             5: "diff-top-1-proofs"}
     return tuples, dt, (f"{n} of the {cfg['per_gpu']} {cfg_name} samples under {' + '.join(names[x] for x in srs)}"
                         f" on {threads} thread(s)" + (f", repeated {reps}x" if reps > 1 else ""))
 
@@ -276,7 +281,7 @@ def main():
         return run_reference(args)
     import torch
     import torch.distributed as dist
-    from paper_2503_21937_b200 import DIFF_MAX_MULT_PROB, Engine, _lib
+    from paper_2503_21937_b200 import DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, Engine, _lib
     from paper_2503_21937_b200 import dist as D
 
     cfg = CONFIGS[args.config]
@@ -333,7 +338,7 @@ def main():
             eng.push_facts(facts)
             st = eng.run()
             d2h = 0
-            if sr == DIFF_MAX_MULT_PROB:
+            if sr in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS):
                 out_dev = eng.output(rel, device=True)
                 grad_local.zero_()
                 eng.backward(rel, torch.ones(out_dev.n, dtype=torch.float32, device=dev), grad_local)
@@ -369,7 +374,7 @@ def main():
             for sr in engines:
                 _run_one(sr, facts, host_out, box)
         if ws > 1:  # the exchange after the fixpoint
-            if DIFF_MAX_MULT_PROB in engines:
+            if any(x in engines for x in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS)):
                 grad_global.zero_()
                 D.scatter_grad(grad_local, layout, grad_global)
                 D.all_reduce_grad(grad_global)

@@ -240,6 +240,7 @@ struct Ctx {
     DBuf<unsigned long long> tup;
   } sl;
   bool no_slice = getenv("LOBSTER_NO_SLICE") != nullptr;  // A/B: per-sample bitmap rounds
+  bool fj_prefetch = !getenv("LOBSTER_FJ_PREFETCH") || atoi(getenv("LOBSTER_FJ_PREFETCH")) != 0;
   bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
   int32_t batch_cur = 1;  // samples of the (micro-)batch being evaluated
@@ -1075,6 +1076,7 @@ struct Ctx {
       }
       jp.semi = semi;
       jp.omin = omin ? 1 : 0;
+      jp.prefetch = fj_prefetch ? 1 : 0;
       const bool last = s == na - 1;
       jp.final_step = last ? 1 : 0;
       // fused row-centric join + direct ⊕: bounded fan-out, one probe tag

@@ -352,8 +352,14 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
     np = nd < np ? nd : np;
   }
   const int ncmp = jp.ncmp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+    // the next grid-stride row's key and tag into L2 (no registers held): the
+    // chain key -> record -> slot peek then starts from an L2 hit
+    if (jp.prefetch && i + stride < np) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pkey + i + stride));
+      if (SEMI != S_UNIT) asm volatile("prefetch.global.L2 [%0];" ::"l"(jp.ptag[0] + i + stride));
+    }
     const PK pkr = pkey[i];
     if (pkr == dead<PK>()) continue;
     const uint64_t pk = (uint64_t)pkr;
@@ -451,6 +457,148 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
   }
   mycount = __reduce_add_sync(0xffffffffu, mycount);
   if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+}
+
+// 32-bit fast path of the fused join (the C2 / C5 hot kernel): probe keys,
+// record keys, slots and witnesses all fit 32 bits, the rule has no filter
+// and no repeated free variable, every move list has <= 2 moves.  The plan is
+// pre-split on the host into the probe row's part (prefix, slot and witness
+// bits taken from the probe key: once per row) and the build side's part
+// (once per candidate), each move as ((x >> r) & m) << l with unused moves
+// masked to 0, so no loop over move descriptors and no 64-bit bit moves run
+// per candidate (the generic kernel spent ~430 instructions per probe row,
+// 19% of them parameter loads: ncu, profiles/ncu_full_r02_fj_before.txt).
+struct Mv32 {
+  uint32_t r[2], m[2], l[2];
+};
+struct Fast32 {
+  Mv32 pre, slot_a, slot_b, w_a, w_b;
+  uint32_t cprefix, cout, wconst;
+  int tag_first_probe;  // ⊗ order: probe tag first (1) or build tag first (0)
+};
+__device__ __forceinline__ uint32_t mv32(const Mv32& v, uint32_t x) {
+  return (((x >> v.r[0]) & v.m[0]) << v.l[0]) | (((x >> v.r[1]) & v.m[1]) << v.l[1]);
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256, SEMI == S_MAXMULT ? FJ_MINB_MX : FJ_MINB)
+    join_rows_rec32_k(const JoinPlan jp, const Fast32 f, unsigned long long* __restrict__ ncand) {
+  const uint32_t* __restrict__ pkey = reinterpret_cast<const uint32_t*>(jp.pkey);
+  const float* __restrict__ ptag = jp.ptag[0];
+  const uint4* __restrict__ brec = jp.brec;
+  uint32_t* __restrict__ dirty = jp.dirty;
+  const uint32_t nprefix = (uint32_t)jp.nprefix;
+  const bool omin = jp.omin;
+  const unsigned long long stamp = jp.mx.stamp, wmask = jp.mx.wmask;
+  uint32_t mycount = 0;
+  int64_t np = jp.np;
+  if (jp.np_dev) {
+    const int64_t nd = (int64_t)*jp.np_dev;
+    np = nd < np ? nd : np;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+    if (jp.prefetch && i + stride < np) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pkey + i + stride));
+      if (SEMI != S_UNIT) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptag + i + stride));
+    }
+    const uint32_t pk = pkey[i];
+    if (pk == 0xffffffffu) continue;
+    const uint32_t pre = f.cprefix | mv32(f.pre, pk);
+    if (pre >= nprefix) continue;
+    const uint4 kk = __ldg(brec + 2 * (size_t)pre);
+    uint4 tt = make_uint4(0, 0, 0, 0);
+    if (SEMI != S_UNIT) tt = __ldg(brec + 2 * (size_t)pre + 1);
+    const float pt = SEMI != S_UNIT ? ptag[i] : 1.0f;
+    const uint32_t slot_row = f.cout | mv32(f.slot_a, pk);
+    const uint32_t w_row = f.wconst | mv32(f.w_a, pk);
+    const uint32_t rk[4] = {kk.x, kk.y, kk.z, kk.w};
+    const uint32_t rt[4] = {tt.x, tt.y, tt.z, tt.w};
+    using VW = typename std::conditional<SEMI == S_MAXMULT, unsigned long long, uint32_t>::type;
+    VW oldv[4], newv[4];
+    uint32_t slotv[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const uint32_t bk = rk[d];
+      if (bk == 0xffffffffu) { slotv[d] = 0xffffffffu; continue; }
+      ++mycount;
+      const uint32_t slot = slot_row | mv32(f.slot_b, bk);
+      slotv[d] = slot;
+      if (SEMI == S_UNIT) {
+        newv[d] = 1u << (slot & 31u);
+        oldv[d] = PEEK(reinterpret_cast<const uint32_t*>(jp.fdir) + (slot >> 5));
+        continue;
+      }
+      const float bt = __uint_as_float(rt[d]);
+      float t;
+      if (SEMI == S_MAXMIN || omin) t = pt < bt ? pt : bt;
+      else t = f.tag_first_probe ? __fmul_rn(pt, bt) : __fmul_rn(bt, pt);
+      if (SEMI == S_MAXMIN) {
+        newv[d] = mm_word(t);
+        oldv[d] = PEEK(reinterpret_cast<const uint32_t*>(jp.fdir) + slot);
+      } else {
+        const uint32_t w = w_row | mv32(f.w_b, bk);
+        newv[d] = ((unsigned long long)(__float_as_uint(t) + 1u) << 34) | stamp | ((unsigned long long)(~w) & wmask);
+        oldv[d] = PEEK(reinterpret_cast<const unsigned long long*>(jp.fdir) + slot);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (slotv[d] == 0xffffffffu) continue;
+      const VW v = newv[d];
+      if (SEMI == S_UNIT) {
+        if (oldv[d] & v) continue;
+        atomicOr(reinterpret_cast<uint32_t*>(jp.fdir) + (slotv[d] >> 5), (uint32_t)v);
+      } else if (SEMI == S_MAXMIN) {
+        if (v <= oldv[d]) continue;
+        atomicMax(reinterpret_cast<uint32_t*>(jp.fdir) + slotv[d], (uint32_t)v);
+      } else {
+        if (v <= oldv[d]) continue;
+        atomicMax(reinterpret_cast<unsigned long long*>(jp.fdir) + slotv[d], (unsigned long long)v);
+      }
+      atomicOr(dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
+    }
+  }
+  mycount = __reduce_add_sync(0xffffffffu, mycount);
+  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+}
+
+// host: split a move list by source into two 32-bit move pairs; false when a
+// list needs more than two moves per source or a field leaves 32 bits
+static bool split_moves32(const Move* mv, int n, Mv32& a, Mv32& b) {
+  int na = 0, nb = 0;
+  a = Mv32{{0, 0}, {0, 0}, {0, 0}};
+  b = a;
+  for (int i = 0; i < n; ++i) {
+    const Move& m = mv[i];
+    if (m.sshift + m.bits > 32 || m.dshift + m.bits > 32 || m.bits == 0) return false;
+    Mv32& t = m.src ? b : a;
+    int& k = m.src ? nb : na;
+    if (k >= 2) return false;
+    t.r[k] = m.sshift;
+    t.m[k] = m.bits >= 32 ? 0xffffffffu : ((1u << m.bits) - 1u);
+    t.l[k] = m.dshift;
+    ++k;
+  }
+  return true;
+}
+
+static bool fast32_plan(const JoinPlan& jp, Fast32& f) {
+  if (!jp.pk32 || !jp.brec || jp.ncmp || jp.nfeq || jp.npt != 1) return false;
+  if (jp.cprefix >> 32 || jp.cout >> 32 || jp.nprefix > 0xffffffffll) return false;
+  Mv32 dummy;
+  if (!split_moves32(jp.prem, jp.nprem, f.pre, dummy)) return false;
+  for (int k = 0; k < 2; ++k)
+    if (dummy.m[k]) return false;  // the prefix is built from the probe key only
+  if (!split_moves32(jp.om, jp.nom, f.slot_a, f.slot_b)) return false;
+  if (jp.semi == S_MAXMULT && !split_moves32(jp.wm, jp.nwm, f.w_a, f.w_b)) return false;
+  if (jp.semi != S_MAXMULT) f.w_a = f.w_b = Mv32{{0, 0}, {0, 0}, {0, 0}};
+  if (jp.ntag != 2 && jp.semi != S_UNIT) return false;
+  f.cprefix = (uint32_t)jp.cprefix;
+  f.cout = (uint32_t)jp.cout;
+  f.wconst = jp.wconst;
+  f.tag_first_probe = jp.tag_order[0] == 0 ? 1 : 0;
+  return true;
 }
 
 // MODE: LC_CAND = candidates (semiring at run time), LC_DIRECT + semiring =
@@ -704,6 +852,12 @@ void launch_join_write(const JoinPlan& jp, const int64_t* offs, const int64_t* s
   else launch_join_write_t<uint64_t, uint64_t>(jp, offs, start, total, g, tile_row, st);
 }
 
+// LOBSTER_FAST32=0: the generic fused kernel only (A/B)
+static bool getenv_fast32_off() {
+  static const bool off = getenv("LOBSTER_FAST32") && atoi(getenv("LOBSTER_FAST32")) == 0;
+  return off;
+}
+
 template <typename PK, int SEMI, int NM>
 static void launch_rows_direct_t(const JoinPlan& jp, int maxdeg, unsigned long long* ncand, cudaStream_t st, int g) {
   if (maxdeg <= 4 && jp.brec) join_rows_direct_k<PK, 4, SEMI, NM, true><<<g, 256, 0, st>>>(jp, ncand);
@@ -727,6 +881,15 @@ void launch_join_rows_direct(const JoinPlan& jp, int maxdeg, unsigned long long*
   if (jp.np_dev)
     g = std::max(148 * 2, std::min(g, 148 * ((maxdeg <= 4) ? (jp.semi == S_MAXMULT ? FJ_MINB_MX : FJ_MINB) : 4)));
   note_launch();
+  Fast32 f;
+  if (maxdeg <= 4 && !getenv_fast32_off() && fast32_plan(jp, f)) {
+    switch (jp.semi) {
+      case S_UNIT: join_rows_rec32_k<S_UNIT><<<g, 256, 0, st>>>(jp, f, ncand); break;
+      case S_MAXMIN: join_rows_rec32_k<S_MAXMIN><<<g, 256, 0, st>>>(jp, f, ncand); break;
+      default: join_rows_rec32_k<S_MAXMULT><<<g, 256, 0, st>>>(jp, f, ncand); break;
+    }
+    return;
+  }
   switch (jp.semi) {
     case S_UNIT: launch_rows_direct_s<S_UNIT>(jp, maxdeg, ncand, st, g); break;
     case S_MAXMIN: launch_rows_direct_s<S_MAXMIN>(jp, maxdeg, ncand, st, g); break;

@@ -87,6 +87,7 @@ struct JoinPlan {
   int final_step;           // 1: candidates (head key, ⊗, witness); 0: intermediate
   int semi;
   int omin;                 // diff-max-min-prob: max-mult storage and witnesses, ⊗ = min
+  int prefetch;             // fused join: L2 prefetch of the next grid-stride row (LOBSTER_FJ_PREFETCH=0: off)
   // ⊗ in body order over T = [ptag[0..npt-1], btag]: T[tag_order[k]] for k = 0..ntag-1
   int ntag;
   int8_t tag_order[MAXT];

@@ -118,3 +118,15 @@ def test_chain_300_proof():
     f = {"edge": W.Facts([src, src + 1], np.zeros(n - 1, np.int32), rng.uniform(0.95, 1.0, n - 1).astype(np.float32))}
     eng, stats, res = run_both(W.Workload("chain", W.PATH_PROGRAM, SR, 1, f), outputs=["path"])
     assert assert_parity(eng, res, "path", SR) == n * (n - 1) // 2
+
+
+def test_c2_full_size_sampled():
+    """Full C2 batch (64 x 32x32, the paper's Pathfinder provenance)
+    under diff-top-1-proofs; the oracle recomputes samples 0 and 63."""
+    w = W.c2_workload(semiring=SR)
+    eng, stats, _ = engine_run(w)
+    samples = [0, 63]
+    res = oracle.run(w.program, SR, w.batch_size, w.facts, outputs=["path", "endpoints_connected"], samples=samples)
+    assert_parity(eng, res, "path", SR, samples=samples)
+    assert_parity(eng, res, "endpoints_connected", SR, samples=samples)
+    assert stats["tuples_derived"] == 64 * 32 ** 4 + 64
