@@ -53,11 +53,23 @@ rel reach(y) :- reach(x), edge(x, y).
 output reach
 """
 
+# Same Generation (P:756 Table 2, P:802-803: "which nodes in a directed graph
+# are the same distance from a common ancestor"; 2 rules, unit).  One graph =
+# one sample (batch 1); the key-partitioned multi-GPU mode (SURVEY §8(f)
+# NEXT-3) splits its tuples across ranks instead of its samples.
+SG_PROGRAM = """
+type edge(x: i32, y: i32)
+rel sg(x, y) :- edge(p, x), edge(p, y), x != y.
+rel sg(x, y) :- edge(a, x), sg(a, b), edge(b, y).
+output sg
+"""
+
 PROGRAMS = {
     "path": PATH_PROGRAM,
     "pathfinder": PATHFINDER_PROGRAM,
     "kinship": KINSHIP_PROGRAM,
     "reach": REACH_PROGRAM,
+    "sg": SG_PROGRAM,
 }
 
 UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
@@ -362,6 +374,29 @@ def random_dag_workload(nodes: int, p_edge: float, seed: int, semiring: int,
         parts.append(Facts([_i32(a), _i32(b)], np.full(a.shape[0], s), _f32(p)))
     facts = {"edge": _concat(parts)}
     return Workload(f"dag{nodes}", program, semiring, batch, facts)
+
+
+# ---------------------------------------------------------------------------
+# Same Generation over a synthetic SNAP-shaped graph.
+# ---------------------------------------------------------------------------
+def sg_workload(nodes: int = 16384, out_degree: int = 3, seed: int = 6, semiring: int = UNIT,
+                tree_levels: int = 0) -> Workload:
+    """A directed graph of `nodes` nodes in which node i draws `out_degree`
+    distinct successors uniformly among the nodes after it (a DAG, like a
+    citation / hierarchy graph, so same-generation pairs stay finite in
+    number per level).  Unit tags; one sample."""
+    rng = np.random.default_rng(seed)
+    src, dst = [], []
+    for i in range(nodes - 1):
+        k = min(out_degree, nodes - 1 - i)
+        succ = i + 1 + rng.choice(nodes - 1 - i, size=k, replace=False)
+        src.append(np.full(k, i))
+        dst.append(np.sort(succ))
+    src = np.concatenate(src)
+    dst = np.concatenate(dst)
+    facts = {"edge": Facts([_i32(src), _i32(dst)], np.zeros(src.shape[0], np.int32),
+                           _f32(np.ones(src.shape[0])))}
+    return Workload("SG", SG_PROGRAM, semiring, 1, facts, meta={"nodes": nodes, "edges": int(src.shape[0])})
 
 
 def workload_by_name(name: str, semiring: Optional[int] = None, **kw) -> Workload:
