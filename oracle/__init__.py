@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "oracle.cpp")
 LIB = os.path.join(HERE, "liboracle.so")
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS, DIFF_ADD_MULT_PROB = 0, 1, 2, 3, 4, 5, 6
 
 
 def build(force: bool = False) -> str:
@@ -175,7 +175,7 @@ def run(program: str, semiring: int, batch: int, facts: dict, outputs: Sequence[
             if rc:
                 raise OracleError(rc, L.orc_last_error(h).decode())
             r = Relation(sid, cols, tags)
-            if semiring in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS) and want_grads:
+            if semiring in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS, DIFF_ADD_MULT_PROB) and want_grads:
                 g = L.orc_grad_size(h, rel.encode())
                 off = np.zeros(n + 1, dtype=np.int64)
                 fid = np.zeros(max(g, 1), dtype=np.int64)

@@ -49,7 +49,17 @@
 
 namespace orc {
 
-enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3, DMAX_MIN = 4, TOP1 = 5 };
+enum Semiring { UNIT = 0, MAX_MIN = 1, ADD_MULT = 2, MAX_MULT = 3, DMAX_MIN = 4, TOP1 = 5, DADD = 6 };
+
+// diff-add-mult-prob (§3.5 "the differentiable versions of the
+// probabilistic semirings"; P:619 dual numbers; DESIGN.md reading
+// "diff-add-mult"): a tag is a dual number (p, ∇p) over the input facts.
+// p follows add-mult exactly (same fp32 ⊗, fp64 segment sums, same Δ' test);
+// ∇p rides along by the product / sum rules, each entry accumulated in fp64:
+//   ⊗: (t, g) ⊗ (b, h) = (fl32(t·b), b·g + t·h)      ⊕: (a, g) ⊕ (b, h) = (a+b, g+h)
+// and an input fact f has ∇ = e_f (duplicates ⊕-merge: each gets ∂/∂p_f = 1).
+// Output rows are ∇p rounded to fp32, fact ids ascending.
+static bool is_add(int sr) { return sr == ADD_MULT || sr == DADD; }
 
 // Semirings whose tag carries a witness (rule + non-head variables of the
 // winning derivation) and whose ⊕ is max with strict improvement:
@@ -102,6 +112,7 @@ struct Tag {
   Tuple wv;           // witness: non-head variable values in order of first appearance
   int64_t fact = -1;  // EDB tuples: id of the (surviving) input fact
   std::vector<int64_t> proof;  // top-1-proof: sorted fact ids
+  std::map<int64_t, double> g;  // diff-add-mult: ∂p/∂p_f
 };
 
 // ⊗ (Fig. 7b for max-min; SURVEY §8(c) point 6/7 for add-mult and max-mult):
@@ -112,6 +123,7 @@ static float otimes(int sr, float a, float b) {
     case DMAX_MIN: return a < b ? a : b;      // min (diff-max-min-prob)
     case TOP1: return 1.0f;                   // (p comes from the proof set, see eval_rule)
     case ADD_MULT: return a * b;              // ×  (compiled with -ffp-contract=off)
+    case DADD: return a * b;                  // p part of the dual product
     case MAX_MULT: return a * b;              // ×
     default: return 1.0f;                     // unit: ∧ of true facts
   }
@@ -126,6 +138,12 @@ static Tag oplus_state(int sr, const Tag& s, const Tag& b) {
   switch (sr) {
     case MAX_MIN: { Tag r = s; if (b.p > s.p) r.p = b.p; return r; }
     case ADD_MULT: { Tag r = s; r.p = (float)((double)s.p + (double)b.p); return r; }
+    case DADD: {
+      Tag r = s;
+      r.p = (float)((double)s.p + (double)b.p);
+      for (auto& e : b.g) r.g[e.first] += e.second;
+      return r;
+    }
     case MAX_MULT: return (b.p > s.p) ? b : s;
     case DMAX_MIN: return (b.p > s.p) ? b : s;
     case TOP1: return (b.p > s.p) ? b : s;
@@ -372,6 +390,7 @@ using Entry = std::pair<const Tuple, Tag>;
 struct Candidate {
   Tuple head; float p; int rule; Tuple wv; int variant;
   std::vector<int64_t> proof;  // top-1-proof
+  std::map<int64_t, double> g;  // diff-add-mult
   bool operator<(const Candidate& o) const {  // canonical order (SURVEY §8(c) point 8b)
     if (!(head == o.head)) return head < o.head;
     if (rule != o.rule) return rule < o.rule;
@@ -412,7 +431,7 @@ struct Engine {
   std::map<std::pair<const Rel*, std::vector<int>>, std::map<Tuple, std::vector<const Entry*>>> shared_idx;
 
   Engine(const std::string& text, int semiring, int b) : prog(parse_program(text)), sr(semiring), batch(b < 1 ? 1 : b) {
-    if (semiring < 0 || semiring > 5) throw Err(E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 6) throw Err(E_INVALID_ARG, "bad semiring");
   }
 
   void push(const std::string& rel, int64_t n, const int32_t* cols, const int32_t* sids, const float* probs, int64_t* first) {
@@ -452,11 +471,13 @@ struct Engine {
     if (it == r.end()) {
       Tag g; g.p = p; g.fact = fid;
       if (sr == TOP1) g.proof = {fid};
+      if (sr == DADD) g.g[fid] = 1.0;
       r[t] = g;
       return;
     }
     Tag& g = it->second;
-    if (sr == ADD_MULT) g.p = (float)((double)g.p + (double)p);
+    if (is_add(sr)) g.p = (float)((double)g.p + (double)p);
+    if (sr == DADD) g.g[fid] += 1.0;
     else if (sr == MAX_MIN) { if (p > g.p) g.p = p; }
     else if (witnessed(sr)) {
       if (p > g.p || (p == g.p && fid < g.fact)) { g.p = p; g.fact = fid; if (sr == TOP1) g.proof = {fid}; }
@@ -567,7 +588,16 @@ struct Engine {
           cd.head.v[i] = t.var ? val[vid(t.name)] : t.val;
         }
         float t = tags[0];                                   // ⊗ left-deep in body order
-        for (size_t i = 1; i < r.body.size(); ++i) t = otimes(sr, t, tags[i]);
+        if (sr == DADD) cd.g = etag[0]->g;
+        for (size_t i = 1; i < r.body.size(); ++i) {
+          if (sr == DADD) {  // product rule: (t, g) ⊗ (b, h) -> b·g + t·h, entries in fp64
+            std::map<int64_t, double> ng;
+            for (auto& e : cd.g) ng[e.first] += (double)tags[i] * e.second;
+            for (auto& e : etag[i]->g) ng[e.first] += (double)t * e.second;
+            cd.g.swap(ng);
+          }
+          t = otimes(sr, t, tags[i]);
+        }
         cd.p = (sr == UNIT) ? 1.0f : t;
         if (sr == TOP1) {  // ⊗ = union of the body proofs; conflict -> no candidate
           std::vector<int64_t> u;
@@ -692,13 +722,15 @@ struct Engine {
             Tag u; u.p = c[i].p; u.rule = c[i].rule; u.wv = c[i].wv; u.proof = c[i].proof;
             double acc = 0.0;
             for (j = i; j < c.size() && c[j].head == c[i].head; ++j) {
-              if (sr == ADD_MULT) acc += (double)c[j].p;
+              if (sr == DADD)
+                for (auto& e : c[j].g) u.g[e.first] += e.second;
+              if (is_add(sr)) acc += (double)c[j].p;
               else if (sr == MAX_MIN) { if (c[j].p > u.p) u.p = c[j].p; }
               else if (witnessed(sr)) {
                 if (c[j].p > u.p) { u.p = c[j].p; u.rule = c[j].rule; u.wv = c[j].wv; u.proof = c[j].proof; }
               }
             }
-            if (sr == ADD_MULT) u.p = (float)acc;
+            if (is_add(sr)) u.p = (float)acc;
             if (sr == UNIT) u.p = 1.0f;
             auto it = s.find(c[i].head);
             if (it == s.end()) nd[c[i].head] = u;
@@ -718,7 +750,7 @@ struct Engine {
       d.rounds.push_back(rounds);
       d.cands.push_back(cands);
     }
-    if (witnessed(sr)) gradients(d);
+    if (witnessed(sr) || sr == DADD) gradients(d);
   }
 
   // Witness walk (SURVEY §8(c) point 7): multiset {f: m_f} of the winning
@@ -747,6 +779,12 @@ struct Engine {
       if (!kv.second.output || kv.second.input) continue;
       auto& gl = d.grads[kv.first];
       for (auto& e : d.rel[kv.first]) {
+        if (sr == DADD) {  // the dual part, rounded once to fp32 (fact ids ascending: std::map order)
+          std::vector<std::pair<int64_t, float>> g;
+          for (auto& f : e.second.g) g.push_back({f.first, (float)f.second});
+          gl.push_back(g);
+          continue;
+        }
         if (sr == TOP1) {  // ∂p/∂p_f = Π_{g in proof, g != f} p_g (fp64, ascending ids)
           std::vector<std::pair<int64_t, float>> g;
           for (int64_t f : e.second.proof) {
