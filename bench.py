@@ -71,6 +71,12 @@ CONFIGS = {
     "C4": dict(per_gpu=1024, semirings=[G.UNIT], out="reach",
                make=lambda b, s: G.c4_workload(G.UNIT, samples=s, batch=b),
                desc="C4: unit reachability over a shared 100k-node / 1M-edge Chung-Lu graph, 1024 sources per GPU"),
+    # one graph split by key across the ranks: strong scaling
+    "SG": dict(per_gpu=1, semirings=[G.UNIT], out="sg", partition=True,
+               make=lambda b, s: G.sg_workload(nodes=16384, out_degree=3, seed=6),
+               cpu_make=lambda: G.sg_workload(nodes=2048, out_degree=3, seed=6),
+               desc="Same Generation (P:756, P:802-803) over a fe-sphere-sized synthetic DAG (16384 nodes, "
+                    "49149 edges), unit; N > 1: key-partitioned across the ranks (NCCL all-to-all per round)"),
     "C5": dict(per_gpu=512, semirings=[G.DIFF_MAX_MULT_PROB], out="endpoints_connected",
                make=lambda b, s: G.grid_workload(64, b, 5, G.DIFF_MAX_MULT_PROB, samples=s, name="C5"),
                desc="C5: 64x64 lattice connectivity, 512 samples per GPU (the 8-GPU shard of the 4096 batch), "
@@ -227,7 +233,7 @@ def cpu_baseline(cfg_name: str, threads: int, sr_indices=None, nsamples: int = 0
     n = nsamples or max(1, min(threads, cfg["per_gpu"]))
     if cfg_name == "C4":
         n = min(n, 8)
-    w = cfg["make"](cfg["per_gpu"], list(range(n)))
+    w = cfg["cpu_make"]() if "cpu_make" in cfg else cfg["make"](cfg["per_gpu"], list(range(n)))
     if cfg_name == "C1":
         n = 1
     reps = 200 if cfg_name == "C1" else 1  # C1 is one 14-tuple problem: repeat it
@@ -240,7 +246,9 @@ def cpu_baseline(cfg_name: str, threads: int, sr_indices=None, nsamples: int = 0
     dt = time.perf_counter() - t
     names = {0: "unit", 1: "max-min-prob", 2: "add-mult-prob", 3: "diff-max-mult-prob", 4: "diff-max-min-prob",
              5: "diff-top-1-proofs"}
-    return tuples, dt, (f"{n} of the {cfg['per_gpu']} {cfg_name} samples under {' + '.join(names[x] for x in srs)}"
+    what = (f"{n} of the {cfg['per_gpu']} {cfg_name} samples" if "cpu_make" not in cfg else
+            f"the {cfg_name} program on a {w.meta.get('nodes')}-node graph of the same generator")
+    return tuples, dt, (f"{what} under {' + '.join(names[x] for x in srs)}"
                         f" on {threads} thread(s)" + (f", repeated {reps}x" if reps > 1 else ""))
 
 
@@ -281,7 +289,7 @@ def main():
         return run_reference(args)
     import torch
     import torch.distributed as dist
-    from paper_2503_21937_b200 import DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, Engine, _lib
+    from paper_2503_21937_b200 import DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, Engine, Group, _lib
     from paper_2503_21937_b200 import dist as D
 
     cfg = CONFIGS[args.config]
@@ -292,10 +300,11 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
     L = _lib.load()
-    gbatch = per_gpu * ws
-    lo = per_gpu * rank  # == dist.shard(gbatch, rank, ws)[0]
+    part = bool(cfg.get("partition"))  # key-partitioned: every rank holds the whole input
+    gbatch = per_gpu if part else per_gpu * ws
+    lo = 0 if part else per_gpu * rank  # == dist.shard(gbatch, rank, ws)[0]
 
-    w = _rank_batch(cfg["make"], per_gpu, rank)
+    w = cfg["make"](per_gpu, None) if part else _rank_batch(cfg["make"], per_gpu, rank)
     # device-resident inputs (value) and pinned host inputs (e2e)
     dfacts, hfacts, h2d = {}, {}, 0
     for rel, f in w.facts.items():
@@ -315,9 +324,18 @@ def main():
     overlap = len(cfg["semirings"]) > 1 and not args.serial
     streams = {sr: (torch.cuda.Stream(device=dev) if overlap else torch.cuda.current_stream(dev))
                for sr in cfg["semirings"]}
-    engines = {sr: Engine(w.program, sr, batch_size=gbatch, device=local, rank=rank, world_size=ws,
-                          stream=streams[sr].cuda_stream if overlap else None)
+    engines = {sr: Engine(w.program, sr, batch_size=gbatch, device=local, rank=0 if part else rank,
+                          world_size=1 if part else ws, stream=streams[sr].cuda_stream if overlap else None)
                for sr in cfg["semirings"]}
+    group = None
+    if part and ws > 1:  # NCCL group of the ranks; the id travels over torch.distributed
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(Group.nccl_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        group = Group.nccl(bytes(uid.cpu().numpy().tobytes()), rank, ws, local)
+        for e in engines.values():
+            e.partition(group, rank)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     nfacts = w.n_facts()
     rel = cfg["out"]
@@ -373,7 +391,7 @@ def main():
         else:
             for sr in engines:
                 _run_one(sr, facts, host_out, box)
-        if ws > 1:  # the exchange after the fixpoint
+        if ws > 1 and not part:  # the exchange after the fixpoint
             if any(x in engines for x in (DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS)):
                 grad_global.zero_()
                 D.scatter_grad(grad_local, layout, grad_global)
@@ -442,8 +460,13 @@ def main():
 
     tuples_step = sum(s["tuples_derived"] for s in stats_all[-1])
     cands_step = sum(s["candidates"] for s in stats_all[-1])
+    if part and ws > 1:  # each rank holds its owned tuples: the job's total is their sum
+        tt = torch.tensor([tuples_step, cands_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt)
+        tuples_step, cands_step = int(tt[0].item()), int(tt[1].item())
+    mult = 1 if part else ws  # weak scaling: every rank did per-GPU work of the same size
     ms_step = total_ms / args.steps
-    value = tuples_step * ws / (ms_step / 1000.0)
+    value = tuples_step * mult / (ms_step / 1000.0)
     ph = {k: sum(s[k] for s in rf_stats[-1]) for k in ("ms_join", "ms_sort", "ms_reduce", "ms_merge", "ms_grad")}
     peak, peak_src = peaks()
     # Dominant kernel: the fused row-centric join + direct ⊕ (join_rows_direct_k).
@@ -479,19 +502,22 @@ def main():
                     "traffic": None, "kernel": "fixpoint phases (SURVEY §8(d) B_alg / summed phase time)",
                     "peak_source": peak_src}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if part else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "name": args.config, "global_batch": gbatch,
-                       "parallelism": f"dp{ws} (batch sharded, global sample ids; no collective inside the fixpoint)",
+                       "parallelism": (f"key-partitioned x{ws} (tuples owned by key hash; candidate all-to-all "
+                                       f"and Σ|Δ'| all-reduce every round over NCCL)" if part else
+                                       f"dp{ws} (batch sharded, global sample ids; no collective inside the fixpoint)"),
                        "semiring_fixpoints": "overlapped on two streams" if overlap else "serial",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "samples_per_s": gbatch / (ms_step / 1000.0),
-            "candidates_per_s": cands_step * ws / (ms_step / 1000.0),
-            "tuples_per_step": tuples_step * ws, "rounds_per_step": sum(s["rounds_total"] for s in stats_all[-1]),
+            "candidates_per_s": cands_step * mult / (ms_step / 1000.0),
+            "tuples_per_step": tuples_step * mult, "rounds_per_step": sum(s["rounds_total"] for s in stats_all[-1]),
             "per_rank_ms_per_step": [t_ / args.steps for t_ in per_rank],
             "phases_ms": ph, "gpu_launches": launches, "roofline": roofline}
     if e2e_ms is not None:
-        line["e2e"] = {"value": tuples_step * ws / (e2e_ms / args.steps / 1000.0), "unit": UNIT,
+        line["e2e"] = {"value": tuples_step * mult / (e2e_ms / args.steps / 1000.0), "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": e2e_d2h,
                        "ms_per_step": e2e_ms / args.steps}
     line["clocks"] = clk.summary()
@@ -506,6 +532,8 @@ def main():
         print(json.dumps(line), flush=True)
     for e in engines.values():
         e.close()
+    if group is not None:
+        group.close()
     if ws > 1:
         dist.destroy_process_group()
 

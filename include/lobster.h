@@ -152,7 +152,9 @@ typedef struct {
      candidates it processed, and its row bytes (key + tag) for §8(d) bytes   */
   int64_t fj_launches, fj_probe_rows, fj_candidates;
   double ms_fused_join;           /* CUDA-event time of the TIMED fused launches only      */
-  int32_t fj_row_bytes, pad0;
+  int32_t fj_row_bytes;
+  int32_t tile_strata;            /* strata run in ONE launch by the small-domain kernel
+                                     (k_tile.cu: per-sample dense relations in shared memory) */
   /* the fused launches timed with CUDA events (every k-th, LOBSTER_JOIN_TIMING_EVERY,
      default 4) and the probe rows / candidates of exactly those launches: their
      bytes over ms_fused_join is the kernel's measured throughput                   */
@@ -210,6 +212,36 @@ int64_t lobster_num_facts(const lobster_ctx* ctx);
 
 /* Diagnostics: CUDA kernels this library has launched in this process so far. */
 int64_t lobster_kernel_launches(void);
+
+/* ---- Key-partitioned evaluation of ONE database across ranks (SURVEY §8(f)
+ * NEXT-3; the paper's TC / Same Generation inputs outgrow one GPU, P:799-803,
+ * P:1151-1172).  Every rank pushes the SAME facts (inputs are replicated);
+ * each IDB tuple is owned by the rank its packed key hashes to.  Each round the
+ * candidates travel to their owners (an all-to-all over the group) and Σ|Δ'| is
+ * summed over all ranks, so every rank runs the same rounds (Alg. 1).
+ * A relation read by a later stratum is gathered whole onto every rank at the
+ * end of its stratum; the others stay partitioned: lobster_output_get returns
+ * this rank's tuples, and the union over ranks is the relation.
+ * Limits: unit, max-min, add-mult; linear recursion (a rule reads at most one
+ * relation of its own stratum); not combined with batch sharding. */
+typedef struct lobster_group lobster_group;
+/* world_size contexts of THIS process, one host thread each (any devices):
+ * exchanges are peer copies between two host barriers.  Owned by the caller;
+ * must outlive the contexts that use it. */
+lobster_status lobster_group_local(int32_t world_size, lobster_group** out);
+/* One process per GPU over NCCL (libnccl.so.2, loaded at run time): rank 0
+ * calls lobster_nccl_id and hands the 128 bytes to every rank (e.g. a
+ * torch.distributed broadcast); each rank then creates its group member on
+ * `device`.  Errors: NCCL (library missing, init failure), INVALID_ARG. */
+lobster_status lobster_nccl_id(uint8_t* id /* 128 bytes */);
+lobster_status lobster_group_nccl(const uint8_t* id, int32_t rank, int32_t world_size, int32_t device,
+                                  lobster_group** out);
+void lobster_group_destroy(lobster_group* group);
+/* Evaluate ctx's databases as `rank` of `group` (NULL group: off).  Call after
+ * lobster_program_load.  Every rank of the group must call lobster_run for
+ * the same database.  Errors: STATE (no program), INVALID_ARG (rank, semiring,
+ * world_size > 1), SCHEMA (a rule reading its own stratum twice). */
+lobster_status lobster_partition(lobster_ctx* ctx, lobster_group* group, int32_t rank);
 
 #ifdef __cplusplus
 }

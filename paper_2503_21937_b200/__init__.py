@@ -12,7 +12,7 @@ this package only marshals arguments.
 """
 from ._lib import (ADD_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, EXPORTS, LIB_PATH, MAX_MIN_PROB,  # noqa: F401
                    SEMIRINGS, UNIT)
-from .engine import Engine, LobsterError, RelationOutput  # noqa: F401
+from .engine import Engine, Group, LobsterError, RelationOutput  # noqa: F401
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 FLAGS += os.environ.get("LOBSTER_NVCC_EXTRA", "").split()  # A/B builds only (e.g. -DFJ_MINB=8)
-SOURCES = ["program.cpp", "engine.cu", "k_scan.cu", "k_sort.cu", "k_join.cu", "k_reduce.cu", "k_walk.cu", "k_slice.cu", "k_top1.cu"]
+SOURCES = ["program.cpp", "engine.cu", "k_scan.cu", "k_sort.cu", "k_join.cu", "k_reduce.cu", "k_walk.cu", "k_slice.cu", "k_top1.cu", "k_tile.cu", "k_part.cu", "xfer.cpp"]
 
 
 def _newest_input() -> float:

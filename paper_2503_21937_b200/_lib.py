@@ -33,7 +33,7 @@ class RunStats(ctypes.Structure):
                 ("ms_grad", ctypes.c_double), ("ms_comm", ctypes.c_double), ("bytes_algorithmic", ctypes.c_int64),
                 ("fj_launches", ctypes.c_int64), ("fj_probe_rows", ctypes.c_int64),
                 ("fj_candidates", ctypes.c_int64), ("ms_fused_join", ctypes.c_double),
-                ("fj_row_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("fj_row_bytes", ctypes.c_int32), ("tile_strata", ctypes.c_int32),
                 ("fj_timed_launches", ctypes.c_int64), ("fj_timed_probe_rows", ctypes.c_int64),
                 ("fj_timed_candidates", ctypes.c_int64)]
 
@@ -51,7 +51,8 @@ class Output(ctypes.Structure):
 
 EXPORTS = ["lobster_create", "lobster_destroy", "lobster_last_error", "lobster_program_load",
            "lobster_facts_push", "lobster_run", "lobster_output_get", "lobster_output_backward",
-           "lobster_num_facts", "lobster_kernel_launches", "lobster_facts_groups"]
+           "lobster_num_facts", "lobster_kernel_launches", "lobster_facts_groups", "lobster_group_local",
+           "lobster_nccl_id", "lobster_group_nccl", "lobster_group_destroy", "lobster_partition"]
 
 _lib = None
 
@@ -89,5 +90,15 @@ def load():
     L.lobster_kernel_launches.restype = ctypes.c_int64
     L.lobster_facts_groups.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp]
     L.lobster_facts_groups.restype = ctypes.c_int
+    L.lobster_group_local.argtypes = [ctypes.c_int32, ctypes.POINTER(vp)]
+    L.lobster_group_local.restype = ctypes.c_int
+    L.lobster_nccl_id.argtypes = [ctypes.c_char_p]
+    L.lobster_nccl_id.restype = ctypes.c_int
+    L.lobster_group_nccl.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(vp)]
+    L.lobster_group_nccl.restype = ctypes.c_int
+    L.lobster_group_destroy.argtypes = [vp]
+    L.lobster_group_destroy.restype = None
+    L.lobster_partition.argtypes = [vp, vp, ctypes.c_int32]
+    L.lobster_partition.restype = ctypes.c_int
     _lib = L
     return L

@@ -31,6 +31,7 @@
 #include "kernels.cuh"
 #include "lobster.h"
 #include "program.hpp"
+#include "xfer.hpp"
 
 namespace lob {
 
@@ -243,6 +244,11 @@ struct Ctx {
   bool fj_prefetch = !getenv("LOBSTER_FJ_PREFETCH") || atoi(getenv("LOBSTER_FJ_PREFETCH")) != 0;
   bool force_slot_join = getenv("LOBSTER_SLOT_JOIN") != nullptr;  // A/B: slot-balanced join only
   int max_iters = 100000;
+  // key-partitioned evaluation of one database (lobster_partition; SURVEY §8(f)
+  // NEXT-3): every IDB tuple lives on the rank its key hashes to
+  Xfer* xfer = nullptr;
+  int part_rank = 0;
+  int64_t* hx = nullptr;  // pinned: per-peer counts (3 x 64)
   int32_t batch_cur = 1;  // samples of the (micro-)batch being evaluated
   bool micro = false;     // the last run was split into sample chunks
   int log_level = getenv("LOBSTER_LOG") ? atoi(getenv("LOBSTER_LOG")) : 0;  // 1: per-run timing line, 2: + rounds
@@ -338,6 +344,7 @@ struct Ctx {
     if (d_ncand) cudaFree(d_ncand);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (hbuf) cudaFreeHost(hbuf);
+    if (hx) cudaFreeHost(hx);
     if (hring) cudaFreeHost(hring);
   }
 
@@ -446,6 +453,27 @@ struct Ctx {
     cuda_check(cudaMemcpyAsync(fact_group.ptr() + first, groups, n * 4, cudaMemcpyDefault, st), "push groups");
     has_groups = true;
     dirty = true;
+  }
+
+  // key-partitioned evaluation of this context's database as `rank` of the group
+  void set_partition(Xfer* x, int rank) {
+    if (!loaded) throw Failure(LOBSTER_E_STATE, "partition before program_load");
+    if (x && (rank < 0 || rank >= x->world)) throw Failure(LOBSTER_E_INVALID_ARG, "rank outside the group");
+    if (x && opt.world_size > 1)
+      throw Failure(LOBSTER_E_INVALID_ARG, "key partitioning and batch sharding (world_size > 1) are exclusive");
+    if (x && semi == S_MAXMULT)
+      throw Failure(LOBSTER_E_INVALID_ARG, "key partitioning supports unit, max-min and add-mult (no witnesses)");
+    if (x)
+      for (const Rule& R : prog.rules) {
+        const int s = prog.rels[R.head_rel].stratum;
+        int nloc = 0;
+        for (auto& a : R.body) nloc += (!prog.rels[a.rel].input && prog.rels[a.rel].stratum == s) ? 1 : 0;
+        if (nloc > 1)
+          throw Failure(LOBSTER_E_SCHEMA, "key partitioning: a rule for " + prog.rels[R.head_rel].name +
+                                              " reads its own stratum twice (linear recursion only)");
+      }
+    xfer = x;
+    part_rank = x ? rank : 0;
   }
 
   void push(const char* relname, int64_t n, const int32_t* const* columns, const int32_t* sample_ids,
@@ -1411,7 +1439,7 @@ struct Ctx {
     S.dense = false;
     S.direct = false;
     S.lazy = false;
-    if (S.build_local || S.L.total > 30 || force_sorted || top1) return;
+    if (S.build_local || S.L.total > 30 || force_sorted || top1 || xfer) return;
     if (semi != S_ADDMULT && !force_sort_dedup) {  // idempotent ⊕: fused direct store
       const int64_t ns = (int64_t)1 << S.L.total;
       const size_t bytes = semi == S_UNIT ? (size_t)((ns + 31) / 32) * 4 : (size_t)ns * (semi == S_MAXMULT ? 8 : 4);
@@ -1510,6 +1538,7 @@ struct Ctx {
       S.no = S.n;
     }
     if (S.dense) return settle_dense(S);
+    if (xfer) S.nc = part_exchange(S, S.nc);  // collective: every rank, every relation, every round
     const int64_t nc = S.nc;
     S.nc = 0;
     if (nc == 0) { S.nd = 0; return 0; }
@@ -2233,12 +2262,401 @@ struct Ctx {
   bool round_cap_hit_slice = false;
   int64_t sl_items = 0;  // (edge, word) items of the sliced joins in this run (diagnostics)
 
+  // ------------------------------------------------ key-partitioned evaluation
+  // (xfer.hpp).  Inputs are replicated, IDB tuples owned
+  // by the hash of their packed key.  Seed-round candidates are derived on
+  // every rank, so each keeps the ones it owns; later rounds derive each
+  // candidate once (linear rules: the Δ atom's tuple lives on one rank) and
+  // send it to its owner.  Buckets are stable (radix sort by owner), so a
+  // receiver's candidate order is deterministic.
+  int64_t* host_counts() {
+    if (!hx) cuda_check(cudaMallocHost(&hx, 3 * 64 * sizeof(int64_t)), "cudaMallocHost");
+    return hx;
+  }
+
+  int64_t part_exchange(RelState& S, int64_t nc) {
+    const bool k32 = c32(S);
+    void* keys = k32 ? (void*)S.ckey32.ptr() : (void*)S.ckey.ptr();
+    const int W = xfer->world;
+    if (cur_round == 1) {
+      launch_part_keep(keys, k32, nc, (uint32_t)W, (uint32_t)part_rank, st);
+      kcheck("part keep");
+      return nc;
+    }
+    const int kb = k32 ? 4 : 8;
+    const bool tags = semi != S_UNIT;
+    uint32_t* dest = arena.get<uint32_t>(nc);
+    uint32_t* idx = arena.get<uint32_t>(nc);
+    uint32_t* dest2 = arena.get<uint32_t>(nc);
+    uint32_t* idx2 = arena.get<uint32_t>(nc);
+    unsigned long long* cnt = arena.get<unsigned long long>(W + 1);
+    int64_t* h = host_counts();
+    cuda_check(cudaMemsetAsync(cnt, 0, (W + 1) * 8, st), "memset");
+    launch_part_dest(keys, k32, nc, (uint32_t)W, dest, idx, cnt, st);
+    const int which = radix_sort(dest, idx, dest2, idx2, nc, bits_for((uint64_t)W), arena.alloc(sort_tmp_bytes(nc)), st);
+    const uint32_t* perm = which ? idx2 : idx;
+    cuda_check(cudaMemcpyAsync(h, cnt, (W + 1) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    int64_t nsend = 0;
+    void* sk = arena.alloc((size_t)std::max<int64_t>(nc, 1) * kb);
+    void* sv = tags ? arena.alloc((size_t)std::max<int64_t>(nc, 1) * 4) : nullptr;
+    sync();
+    for (int d = 0; d < W; ++d) nsend += h[d];  // dead candidates (bucket W) are dropped
+    launch_part_gather(keys, perm, sk, nsend, kb, st);
+    if (tags) launch_part_gather(S.cv32.ptr(), perm, sv, nsend, 4, st);
+    kcheck("part gather");
+    int64_t* rc = h + 64;
+    Phase ph(this, 6);
+    xfer->counts(part_rank, h, rc, st);
+    int64_t nr = 0;
+    for (int d = 0; d < W; ++d) nr += rc[d];
+    std::vector<int64_t> scnt(h, h + W), rcnt(rc, rc + W);
+    reserve_candidates_for(S, nr);
+    void* rk = k32 ? (void*)S.ckey32.ptr() : (void*)S.ckey.ptr();
+    xfer->alltoallv(part_rank, sk, scnt.data(), rk, rcnt.data(), kb, st);
+    if (tags) xfer->alltoallv(part_rank, sv, scnt.data(), S.cv32.ptr(), rcnt.data(), 4, st);
+    return nr;
+  }
+
+  void reserve_candidates_for(RelState& S, int64_t n) {
+    if (c32(S)) S.ckey32.reserve(n);
+    else S.ckey.reserve(n);
+    if (semi != S_UNIT) S.cv32.reserve(n);
+  }
+
+  int64_t part_sum(int64_t v) {
+    int64_t* h = host_counts();
+    const int W = xfer->world;
+    for (int d = 0; d < W; ++d) h[d] = v;
+    xfer->counts(part_rank, h, h + 64, st);
+    int64_t s = 0;
+    for (int d = 0; d < W; ++d) s += h[64 + d];
+    return s;
+  }
+
+  bool read_later(int r, size_t si) const {
+    for (const Rule& R : prog.rules) {
+      if ((size_t)prog.rels[R.head_rel].stratum <= si) continue;
+      for (auto& a : R.body)
+        if (a.rel == r) return true;
+    }
+    return false;
+  }
+
+  // every rank gets the whole relation (sorted, keys disjoint across ranks)
+  void part_gather(RelState& S) {
+    ensure_sorted(S);
+    const int W = xfer->world;
+    int64_t* h = host_counts();
+    for (int d = 0; d < W; ++d) h[d] = S.n;
+    xfer->counts(part_rank, h, h + 64, st);
+    int64_t nr = 0;
+    for (int d = 0; d < W; ++d) nr += h[64 + d];
+    std::vector<int64_t> scnt(h, h + W), rcnt(h + 64, h + 64 + W);
+    const bool tags = semi != S_UNIT;
+    uint64_t* sk = arena.get<uint64_t>(std::max<int64_t>(1, S.n * W));
+    uint32_t* sv = tags ? arena.get<uint32_t>(std::max<int64_t>(1, S.n * W)) : nullptr;
+    for (int d = 0; d < W && S.n; ++d) {
+      cuda_check(cudaMemcpyAsync(sk + d * S.n, S.key.ptr(), S.n * 8, cudaMemcpyDeviceToDevice, st), "gather");
+      if (tags) cuda_check(cudaMemcpyAsync(sv + d * S.n, S.p.ptr(), S.n * 4, cudaMemcpyDeviceToDevice, st), "gather");
+    }
+    uint64_t* k0 = arena.get<uint64_t>(nr);
+    uint64_t* k1 = arena.get<uint64_t>(nr);
+    uint32_t* v0 = tags ? arena.get<uint32_t>(nr) : nullptr;
+    uint32_t* v1 = tags ? arena.get<uint32_t>(nr) : nullptr;
+    xfer->alltoallv(part_rank, sk, scnt.data(), k0, rcnt.data(), 8, st);
+    if (tags) xfer->alltoallv(part_rank, sv, scnt.data(), v0, rcnt.data(), 4, st);
+    void* stmp = arena.alloc(sort_tmp_bytes(nr));
+    int which;
+    if (tags) which = radix_sort(k0, v0, k1, v1, nr, S.L.total, stmp, st);
+    else which = radix_sort<uint64_t, void>(k0, nullptr, k1, nullptr, nr, S.L.total, stmp, st);
+    S.key.reserve(nr);
+    cuda_check(cudaMemcpyAsync(S.key.ptr(), which ? k1 : k0, nr * 8, cudaMemcpyDeviceToDevice, st), "gather");
+    if (tags) {
+      S.p.reserve(nr);
+      cuda_check(cudaMemcpyAsync(S.p.ptr(), which ? v1 : v0, nr * 4, cudaMemcpyDeviceToDevice, st), "gather");
+    }
+    kcheck("part gather");
+    S.n = nr;
+  }
+
+  // ------------------------------------------------ small dense strata (k_tile.cu)
+  // A stratum qualifies when: unit / max-min / add-mult; every relation of it
+  // batched with arity <= 4; every rule within the plan limits, the variable
+  // that closes an atom appears once in it and has a domain <= 64; and the
+  // stratum's S / Δ / U arrays plus fibers fit one CTA's shared memory.
+  bool no_tile = getenv("LOBSTER_NO_TILE") != nullptr;  // A/B: the per-round path
+  int64_t tile_max_slots = getenv("LOBSTER_TILE") ? INT64_MAX : 65536;
+  int64_t class_dom(int cl) const { return class_max[cl] - class_min[cl] + 1; }
+
+  bool tile_plan(const std::vector<int>& strat, TilePlan& P, std::vector<int>& prel) {
+    if (no_tile || top1 || omin || semi == S_MAXMULT || xfer) return false;
+    std::memset(&P, 0, sizeof(P));
+    P.semi = semi;
+    P.nsamples = batch_cur;
+    P.max_iters = max_iters;
+    std::set<int> local(strat.begin(), strat.end());
+    prel.clear();
+    auto plan_rel = [&](int r) -> int {
+      for (size_t i = 0; i < prel.size(); ++i)
+        if (prel[i] == r) return (int)i;
+      if ((int)prel.size() >= TILE_MAXREL) return -1;
+      const Relation& R = prog.rels[r];
+      if (R.arity > TILE_MAXCOL) return -1;
+      TileRel& T = P.rel[prel.size()];
+      T.ncols = (int8_t)R.arity;
+      T.local = local.count(r) ? 1 : 0;
+      T.shared = R.shared ? 1 : 0;
+      if (T.local && (R.shared || rels[r]->L.total > 30)) return -1;
+      int64_t D = 1;
+      for (int c = R.arity - 1; c >= 0; --c) {
+        T.stride[c] = (int32_t)D;
+        T.dom[c] = (int32_t)class_dom(R.col_class[c]);
+        D *= T.dom[c];
+        if (D > (1 << 20)) return -1;
+      }
+      T.D = (int32_t)D;
+      for (int c = 0; c < TILE_MAXCOL; ++c) {
+        for (int k = 0; k < 3; ++k) T.sm_tag[k] = T.sm_bits[k] = -1;
+        T.sm_fib[0][c] = T.sm_fib[1][c] = -1;
+      }
+      prel.push_back(r);
+      return (int)prel.size() - 1;
+    };
+    for (int r : strat) {
+      const int i = plan_rel(r);
+      if (i < 0 || !rels[r]->L.has_sample) return false;
+      P.local_rel[P.nlocal++] = (int8_t)i;
+    }
+    for (const Rule& R : prog.rules) {
+      if (!local.count(R.head_rel)) continue;
+      if (P.nrule >= TILE_MAXRULE || (int)R.var_names.size() > TILE_MAXV || (int)R.nonhead.size() > TILE_MAXLEV ||
+          (int)R.body.size() > MAXT || (int)R.cmps.size() > MAXC)
+        return false;
+      TileRule& T = P.rule[P.nrule++];
+      T.head = (int8_t)plan_rel(R.head_rel);
+      std::vector<int> lev(R.var_names.size(), -1);
+      for (size_t i = 0; i < R.nonhead.size(); ++i) {
+        lev[R.nonhead[i]] = (int)i;
+        T.lev_var[i] = (int8_t)R.nonhead[i];
+      }
+      T.nlev = (int8_t)R.nonhead.size();
+      for (size_t v = 0; v < R.var_names.size(); ++v) {
+        if (class_dom(R.var_class[v]) > 64) return false;  // values are packed 6 bits per variable
+        T.vdom[v] = (int32_t)class_dom(R.var_class[v]);
+        T.vmin[v] = (int32_t)class_min[R.var_class[v]];
+      }
+      const Relation& HR = prog.rels[R.head_rel];
+      for (int c = 0; c < HR.arity; ++c) {
+        T.hvar[c] = (int8_t)R.head[c].var;
+        if (!R.head[c].is_var()) {
+          const int64_t x = (int64_t)R.head[c].cst - class_min[HR.col_class[c]];
+          T.hcst[c] = (x < 0 || x >= class_dom(HR.col_class[c])) ? -1 : (int32_t)x;
+        }
+      }
+      T.natoms = (int8_t)R.body.size();
+      std::vector<int> lpos;
+      for (int a = 0; a < (int)R.body.size(); ++a) {
+        const BodyAtom& B = R.body[a];
+        const int pi = plan_rel(B.rel);
+        if (pi < 0) return false;
+        if (local.count(B.rel)) lpos.push_back(a);
+        TileAtom& A = T.atom[a];
+        A.rel = (int8_t)pi;
+        A.level = -1;
+        A.fcol = -1;
+        for (int c = 0; c < (int)B.args.size(); ++c) {
+          A.var[c] = (int8_t)B.args[c].var;
+          if (!B.args[c].is_var()) {
+            A.cst[c] = (int32_t)((int64_t)B.args[c].cst - class_min[prog.rels[B.rel].col_class[c]]);
+          } else if (lev[B.args[c].var] > A.level) {
+            A.level = (int8_t)lev[B.args[c].var];
+            A.fcol = (int8_t)c;
+          }
+        }
+        A.chk = -1;
+        if (A.level >= 0)
+          for (int c = 0; c < (int)B.args.size(); ++c)
+            if (B.args[c].is_var() && c != A.fcol && lev[B.args[c].var] > A.chk) A.chk = (int8_t)lev[B.args[c].var];
+        if (A.level >= 0) {  // the closing variable: one column, domain <= 64
+          int occ = 0;
+          for (auto& t : B.args) occ += t.is_var() && t.var == B.args[A.fcol].var;
+          TileRel& TR = P.rel[pi];
+          if (occ != 1 || TR.dom[A.fcol] > 64) return false;
+          TR.nfib[A.fcol] = TR.D / TR.dom[A.fcol];
+        }
+      }
+      if ((int)lpos.size() > TILE_MAXVAR) return false;
+      if (lpos.empty()) {
+        T.seed = 1;
+        T.nvariant = 1;
+        for (int a = 0; a < T.natoms; ++a) T.ver[0][a] = TV_EXT;
+      } else {
+        T.nvariant = (int8_t)lpos.size();
+        for (size_t j = 0; j < lpos.size(); ++j) {
+          for (int a = 0; a < T.natoms; ++a) T.ver[j][a] = TV_EXT;
+          for (size_t q = 0; q < lpos.size(); ++q)
+            T.ver[j][lpos[q]] = q == j ? TV_DELTA : (q < j ? TV_NEW : TV_OLD);
+        }
+      }
+      T.ncmp = (int8_t)R.cmps.size();
+      for (size_t i = 0; i < R.cmps.size(); ++i) {
+        const Compare& c = R.cmps[i];
+        TileCmp& t = T.cmp[i];
+        t.va = (int8_t)c.a.var;
+        t.vb = (int8_t)c.b.var;
+        t.ca = c.a.cst;
+        t.cb = c.b.cst;
+        t.neq = c.neq ? 1 : 0;
+        t.level = (int8_t)std::max(c.a.is_var() ? lev[c.a.var] : -1, c.b.is_var() ? lev[c.b.var] : -1);
+      }
+    }
+    P.nrel = (int)prel.size();
+    // fiber strides (row-major over the other columns) and the shared-memory layout:
+    // [fibers S, Δ | bits S, Δ] (zeroed per sample) then [bits U | tags S, Δ, U]
+    int64_t off = 0;
+    for (int i = 0; i < P.nrel; ++i) {
+      TileRel& T = P.rel[i];
+      for (int c = 0; c < T.ncols; ++c) {
+        int64_t m = 1;
+        for (int q = T.ncols - 1; q >= 0; --q) {
+          if (q == c) continue;
+          T.fstride[c][q] = (int32_t)m;
+          m *= T.dom[q];
+        }
+      }
+      if (!T.local) continue;
+      for (int c = 0; c < T.ncols; ++c)
+        for (int k = 0; k < 2 && T.nfib[c]; ++k) {
+          T.sm_fib[k][c] = (int32_t)off;
+          off += (int64_t)T.nfib[c] * 8;
+        }
+    }
+    for (int i = 0; i < P.nrel; ++i) {
+      TileRel& T = P.rel[i];
+      if (!T.local) continue;
+      for (int k = 0; k < 2; ++k) {
+        T.sm_bits[k] = (int32_t)off;
+        off += (int64_t)((T.D + 31) / 32) * 4;
+      }
+    }
+    P.clear_words = (int32_t)(off / 4);
+    for (int i = 0; i < P.nrel; ++i) {
+      TileRel& T = P.rel[i];
+      if (!T.local) continue;
+      T.sm_bits[2] = (int32_t)off;
+      off += (int64_t)((T.D + 31) / 32) * 4;
+      if (semi != S_UNIT)
+        for (int k = 0; k < 3; ++k) {
+          T.sm_tag[k] = (int32_t)off;
+          off += (int64_t)T.D * 4;
+        }
+    }
+    if (off > 200 * 1024) return false;
+    // Each round pulls every head slot of every sample through an interpreted
+    // enumeration: a win for tiny problems (one launch instead of ~20 per
+    // round and a host sync per join), a loss once the batch holds more than
+    // ~64k head slots (measured: C3, 2M slots, 210 ms vs 32 ms per step).
+    // LOBSTER_TILE=1 forces the path (parity tests at full size).
+    int64_t slots = 0;
+    for (int i = 0; i < P.nrel; ++i)
+      if (P.rel[i].local) slots += (int64_t)P.rel[i].D * batch_cur;
+    if (slots > tile_max_slots) return false;
+    P.smem_bytes = (int32_t)std::max<int64_t>(off, 16);
+    return true;
+  }
+
+  // Run a qualifying stratum in one launch; its relations end in dense stores
+  // (compacted by the caller).  Returns the stratum's rounds (max over samples).
+  int run_tile(TilePlan& P, const std::vector<int>& prel, bool& cap) {
+    const int B = batch_cur;
+    for (int i = 0; i < P.nrel; ++i) {  // external relations -> dense per-sample arrays
+      TileRel& T = P.rel[i];
+      const int r = prel[i];
+      RelState& S = *rels[r];
+      if (T.local) {
+        S.dense = true;
+        S.direct = false;
+        S.lazy = false;
+        S.nslots = (int64_t)1 << S.L.total;
+        if (semi == S_UNIT) S.dfbits.reserve((S.nslots + 31) / 32);
+        else S.dfp.reserve(S.nslots);
+        launch_dense_fill(S.dfp.ptr(), S.dfbits.ptr(), S.nslots, semi, st);
+        T.dfp = semi == S_UNIT ? nullptr : S.dfp.ptr();
+        T.dfbits = semi == S_UNIT ? S.dfbits.ptr() : nullptr;
+        for (int c = 0; c < T.ncols; ++c) T.pshift[c] = (uint8_t)S.L.shift[c];
+        T.psshift = (uint8_t)S.L.sshift;
+        continue;
+      }
+      ensure_sorted(S);
+      const int64_t ns = T.shared ? 1 : B;
+      const int64_t nbw = (T.D + 31) / 32;
+      int64_t nf = 0;
+      for (int c = 0; c < T.ncols; ++c) nf += T.nfib[c];
+      const size_t bytes = (size_t)ns * ((semi == S_UNIT ? 0 : (size_t)T.D * 4) + nbw * 4 + nf * 8);
+      uint8_t* base = reinterpret_cast<uint8_t*>(arena.alloc(bytes));
+      cuda_check(cudaMemsetAsync(base, 0, bytes, st), "memset");
+      size_t o = 0;
+      for (int c = 0; c < T.ncols; ++c) {
+        T.fib[c] = T.nfib[c] ? reinterpret_cast<const unsigned long long*>(base + o) : nullptr;
+        o += (size_t)ns * T.nfib[c] * 8;
+      }
+      T.bits = reinterpret_cast<const uint32_t*>(base + o);
+      o += (size_t)ns * nbw * 4;
+      T.tag = semi == S_UNIT ? nullptr : reinterpret_cast<const float*>(base + o);
+      TileScatter sc{};
+      sc.key = S.key.ptr();
+      sc.p = semi == S_UNIT ? nullptr : S.p.ptr();
+      sc.n = S.n;
+      sc.has_sample = S.L.has_sample ? 1 : 0;
+      sc.sshift = (uint8_t)S.L.sshift;
+      sc.sbits = (uint8_t)S.L.sbits;
+      sc.ncols = T.ncols;
+      for (int c = 0; c < T.ncols; ++c) {
+        sc.shift[c] = (uint8_t)S.L.shift[c];
+        sc.bits[c] = (uint8_t)S.L.bits[c];
+      }
+      sc.rel = T;
+      launch_tile_scatter(sc, st);
+      stats.bytes_algorithmic += S.n * (8 + (semi == S_UNIT ? 0 : 4));
+    }
+    int* d = arena.get<int>(B + 2);  // [max rounds, cap hit, rounds per sample...]
+    cuda_check(cudaMemsetAsync(d, 0, 8, st), "memset");
+    std::vector<uint32_t> htr;
+    if (getenv("LOBSTER_TILE_TRACE")) {  // debug: per (sample, round) candidates and |Δ'|
+      P.trace = arena.get<uint32_t>((int64_t)B * 128);
+      cuda_check(cudaMemsetAsync(P.trace, 0, (size_t)B * 128 * 4, st), "memset");
+    }
+    {
+      Phase ph(this, 0);
+      launch_tile_fixpoint(P, reinterpret_cast<TilePlan*>(arena.alloc(sizeof(TilePlan))), d + 2, d_ncand, d + 1, st);
+      kcheck("tile fixpoint");
+    }
+    if (P.trace) {
+      htr.resize((size_t)B * 128);
+      cuda_check(cudaMemcpyAsync(htr.data(), P.trace, htr.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      sync();
+      for (int s = 0; s < B; ++s) {
+        fprintf(stderr, "[tile] sample %d:", s);
+        for (int r = 1; r < 64 && (htr[(s * 64 + r) * 2] || htr[(s * 64 + r) * 2 + 1]); ++r)
+          fprintf(stderr, " r%d c%u d%u", r, htr[(s * 64 + r) * 2], htr[(s * 64 + r) * 2 + 1]);
+        fprintf(stderr, "\n");
+      }
+    }
+    launch_max_i32(d + 2, B, d, st);
+    const int64_t both = read_dev(reinterpret_cast<const int64_t*>(d));
+    cap = (both >> 32) != 0;
+    return (int)(both & 0xffffffff);
+  }
+
   int64_t run_strata() {
     int64_t round_cap_hit = 0;
     for (size_t si = 0; si < prog.strata.size(); ++si) {
       const std::vector<int>& strat = prog.strata[si];
       std::set<int> local(strat.begin(), strat.end());
       if (top1) top1_begin_stratum(strat);
+      TilePlan tplan;
+      std::vector<int> tprel;
+      const bool tiled = tile_plan(strat, tplan, tprel);
       for (int r : strat) {
         RelState& S = *rels[r];
         S.n = S.nd = S.no = S.nc = 0;
@@ -2246,7 +2664,7 @@ struct Ctx {
         if (semi != S_UNIT) S.p.reserve(1);
         if (semi == S_MAXMULT) S.w.reserve(1);
         HostTimer hts(host_ms[4]);
-        choose_store(S, r);
+        if (!tiled) choose_store(S, r);
       }
       mark("store setup");
       int rounds = 0;
@@ -2256,7 +2674,13 @@ struct Ctx {
       timed_rounds.clear();
       const size_t trace_base = trace.size();
       async_nd0 = 0;
-      for (;;) {
+      if (tiled) {  // the whole stratum in one launch (k_tile.cu)
+        bool cap = false;
+        rounds = run_tile(tplan, tprel, cap);
+        stats.tile_strata++;
+        if (cap) round_cap_hit = 1;
+      }
+      for (; !tiled;) {
         if (rounds >= max_iters) {
           if (async && (done = drain_async(pending, trace_base, true)) > 0) { rounds = (int)done; break; }
           round_cap_hit = 1;
@@ -2312,6 +2736,7 @@ struct Ctx {
             }
           }
           for (int r : strat) changed += settle(r);
+          if (xfer) changed = part_sum(changed);  // Σ|Δ'| over every rank (Alg. 1's test, globally)
           if (top1) top1_commit(strat);
         }
         if (async) {  // |Δ'| of this round -> pinned ring; poll earlier rounds without stalling the GPU
@@ -2377,6 +2802,9 @@ struct Ctx {
         }
       }
       mark("dense->sorted");
+      if (xfer && !round_cap_hit)  // later strata read this stratum's relations whole
+        for (int r : strat)
+          if (read_later(r, si)) part_gather(*rels[r]);
       stats.rounds_total += rounds;
       stats.strata++;
       if (round_cap_hit) break;
@@ -2405,6 +2833,7 @@ struct Ctx {
         case 5:  // timed fused joins (every join_timing_every-th launch)
           stats.ms_fused_join += m;
           break;
+        case 6: stats.ms_comm += m; break;  // key-partitioned exchange
         default: stats.ms_grad += m; break;
       }
     }
@@ -2799,6 +3228,10 @@ struct lobster_ctx {
   lob::Ctx c;
 };
 
+struct lobster_group {
+  std::unique_ptr<lob::Xfer> x;
+};
+
 namespace {
 template <typename F>
 lobster_status guarded(lobster_ctx* ctx, F&& f) {
@@ -2874,5 +3307,38 @@ lobster_status lobster_facts_groups(lobster_ctx* ctx, int64_t first_fact_id, int
 }
 
 int64_t lobster_kernel_launches(void) { return lob::g_launches.load(); }
+
+lobster_status lobster_group_local(int32_t world_size, lobster_group** out) {
+  if (!out || world_size < 1 || world_size > 64) return LOBSTER_E_INVALID_ARG;
+  *out = new lobster_group{std::unique_ptr<lob::Xfer>(new lob::LocalXfer(world_size))};
+  return LOBSTER_OK;
+}
+
+lobster_status lobster_nccl_id(uint8_t* id) {
+  if (!id) return LOBSTER_E_INVALID_ARG;
+  try {
+    lob::NcclXfer::unique_id(id);
+  } catch (lob::Failure& e) {
+    return (lobster_status)e.code;
+  }
+  return LOBSTER_OK;
+}
+
+lobster_status lobster_group_nccl(const uint8_t* id, int32_t rank, int32_t world_size, int32_t device,
+                                  lobster_group** out) {
+  if (!out || !id || world_size < 1 || world_size > 64 || rank < 0 || rank >= world_size) return LOBSTER_E_INVALID_ARG;
+  try {
+    *out = new lobster_group{std::unique_ptr<lob::Xfer>(new lob::NcclXfer(id, rank, world_size, device))};
+  } catch (lob::Failure& e) {
+    return (lobster_status)e.code;
+  }
+  return LOBSTER_OK;
+}
+
+void lobster_group_destroy(lobster_group* g) { delete g; }
+
+lobster_status lobster_partition(lobster_ctx* ctx, lobster_group* group, int32_t rank) {
+  return guarded(ctx, [&]() { ctx->c.set_partition(group ? group->x.get() : nullptr, rank); });
+}
 
 }  // extern "C"

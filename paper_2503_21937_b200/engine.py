@@ -88,6 +88,56 @@ class RelationOutput:
     grad_values: object = None
 
 
+class Group:
+    """The ranks of one key-partitioned evaluation (include/lobster.h
+    lobster_group_*).  `Group.local(W)`: W engines of this process (one host
+    thread each); `Group.nccl(id, rank, W, device)`: one process per GPU, `id`
+    from `Group.nccl_id()` on rank 0 (128 bytes, distributed by the caller)."""
+
+    def __init__(self, handle):
+        self._L = _lib.load()
+        self._h = handle
+
+    @classmethod
+    def local(cls, world_size: int) -> "Group":
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        rc = L.lobster_group_local(int(world_size), ctypes.byref(h))
+        if rc != 0:
+            raise LobsterError(rc, "lobster_group_local failed")
+        return cls(h)
+
+    @staticmethod
+    def nccl_id() -> bytes:
+        L = _lib.load()
+        buf = ctypes.create_string_buffer(128)
+        rc = L.lobster_nccl_id(buf)
+        if rc != 0:
+            raise LobsterError(rc, "lobster_nccl_id failed (libnccl.so.2 missing?)")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, world_size: int, device: int) -> "Group":
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        rc = L.lobster_group_nccl(ctypes.create_string_buffer(bytes(uid), 128), int(rank), int(world_size),
+                                  int(device), ctypes.byref(h))
+        if rc != 0:
+            raise LobsterError(rc, "lobster_group_nccl failed")
+        return cls(h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.lobster_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """One lobster context: program_load -> facts_push* -> run -> output_get*."""
 
@@ -118,6 +168,13 @@ class Engine:
             raise LobsterError(rc, "lobster_create failed (no CUDA device?)")
         self._h = h
         self._check(self._L.lobster_program_load(self._h, program.encode(), semiring))
+        self._group = None
+
+    def partition(self, group: "Group", rank: int) -> None:
+        """Key-partitioned evaluation of this engine's databases as `rank` of `group`
+        (lobster_partition): push the same facts on every rank, run every rank."""
+        self._check(self._L.lobster_partition(self._h, group._h if group is not None else None, int(rank)))
+        self._group = group  # the group must outlive the context
 
     def _check(self, rc):
         if rc != 0:

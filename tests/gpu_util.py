@@ -39,7 +39,7 @@ def oracle_rel(res, rel):
     return r, keys
 
 
-def assert_parity(eng, res, rel, semiring, samples=None, check_grads=True):
+def assert_parity(eng, res, rel, semiring, samples=None, check_grads=True, exact=False):
     """Tuple sets bit-exact; tags within the semiring's tolerance; gradients
     (fact ids exact, values 1e-6 rel).  `samples`: restrict the GPU side to
     the oracle's sample subset.  Vectorised: full-size outputs (C2 `path`,
@@ -60,7 +60,7 @@ def assert_parity(eng, res, rel, semiring, samples=None, check_grads=True):
     gk = G
     if semiring != 0:
         gp = o.probs[idx]
-        tol = REL_TOL[semiring]
+        tol = 0.0 if exact else REL_TOL[semiring]
         if tol == 0.0:
             bad = np.nonzero(gp.view(np.uint32) != r.tags.view(np.uint32))[0]
             assert bad.size == 0, f"{rel}: {bad.size} tags differ, e.g. {[(gk[i].tolist(), gp[i], r.tags[i]) for i in bad[:5]]}"

@@ -32,9 +32,12 @@ def test_c1_all_semirings(sr):
     assert stats["rounds_total"] == int(res.rounds.sum())
 
 
+@pytest.mark.parametrize("tile", [True, False])
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("sr", [0, 1, 3])
-def test_random_digraphs(seed, sr):
+def test_random_digraphs(seed, sr, tile, monkeypatch):
+    if not tile:
+        monkeypatch.setenv("LOBSTER_NO_TILE", "1")
     rng = np.random.default_rng(seed)
     n = int(rng.integers(2, 40))
     w = W.random_digraph_workload(n, float(rng.uniform(0.02, 0.25)), seed, sr, batch=3,
@@ -55,10 +58,12 @@ output even
 
 @pytest.mark.parametrize("seed", range(3))
 @pytest.mark.parametrize("sr", [0, 1, 3])
-def test_mutual_recursion_async_rounds(seed, sr):
+def test_mutual_recursion_async_rounds(seed, sr, monkeypatch):
     """Two relations in one recursive stratum (odd / even path lengths): the
     asynchronous rounds count both relations' Δ' (one ring word each) and stop
-    on the same round as the oracle."""
+    on the same round as the oracle.  (Per-round path: the one-launch small-
+    domain stratum is tested in test_gpu_tile.py.)"""
+    monkeypatch.setenv("LOBSTER_NO_TILE", "1")
     w = W.random_digraph_workload(24, 0.12, 700 + seed, sr, batch=4, program=EVEN_ODD_PROGRAM)
     eng, stats, res = run_both(w, outputs=["odd", "even"])
     assert_parity(eng, res, "odd", sr)
@@ -325,6 +330,7 @@ def test_iteration_cap_async_rounds(sr, monkeypatch):
     the readable state equals the host-synchronised engine's at the same cap."""
     from paper_2503_21937_b200 import Engine, LobsterError, _lib
     w = W.c2_workload(semiring=sr, n=8, batch=3)
+    monkeypatch.setenv("LOBSTER_NO_TILE", "1")  # the per-round path (tiles: test_gpu_tile.py)
     outs = []
     for sync in (False, True):
         if sync:
@@ -378,6 +384,7 @@ def test_store_paths_match(sr, env, monkeypatch):
     instead of atomically claimed sorted runs, and stores compacted at stratum
     end instead of on first use) matches the oracle."""
     monkeypatch.setenv(env, "1")
+    monkeypatch.setenv("LOBSTER_NO_TILE", "1")  # small domains would take the one-launch tile path
     w = W.c2_workload(semiring=sr, n=8, batch=5)
     eng, stats, res = run_both(w, outputs=["path", "endpoints_connected"])
     assert_parity(eng, res, "path", sr, check_grads=False)

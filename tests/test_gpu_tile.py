@@ -1,0 +1,208 @@
+"""GPU parity of the one-launch small-domain strata (k_tile.cu) against the
+oracle: tuple sets bit-exact and tags bit-exact under unit, max-min AND
+add-mult — the kernel forms each head's add-mult sum over its candidates in the
+oracle's canonical order (rule, non-head variables, variant) in fp64 and rounds
+once (SURVEY §8(c) points 8b, 9).  Every test also checks that the strata it
+targets really took the tile path (stats['tile_strata'])."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.gpu_util import assert_parity, engine_run, run_both
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_21937_b200 import build
+    build()
+    oracle.build()
+
+
+def _facts(cols, sids=None, probs=None):
+    cols = [np.asarray(c, np.int32) for c in cols]
+    n = cols[0].shape[0] if cols else (0 if sids is None else len(sids))
+    return W.Facts(cols, np.zeros(n, np.int32) if sids is None else np.asarray(sids, np.int32),
+                   None if probs is None else np.asarray(probs, np.float32))
+
+
+def _check(w, rels, sr=None, tiles=None, samples=None):
+    sr = w.semiring if sr is None else sr
+    eng, stats, _ = engine_run(w, sr)
+    res = oracle.run(w.program, sr, w.batch_size, w.facts, outputs=rels, samples=samples)
+    for r in rels:
+        assert_parity(eng, res, r, sr, samples=samples, exact=True)
+    if tiles is not None:
+        assert stats["tile_strata"] == tiles, stats["tile_strata"]
+    if samples is None:
+        assert stats["rounds_total"] == int(res.rounds.sum())
+    return eng, stats, res
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2])
+def test_c1_bit_exact(sr):
+    """The §8(c) worked example, add-mult included, bit-exact in one launch."""
+    w = W.c1_workload(sr)
+    eng, stats, res = _check(w, ["path"], tiles=1)
+    assert eng.output("path").n == 14
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_random_dag_addmult_bit_exact(seed):
+    w = W.random_dag_workload(int(12 + 9 * seed), 0.2, 50 + seed, 2, batch=4)
+    _check(w, ["path"], tiles=1)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("sr", [0, 1])
+def test_random_digraphs_tile(seed, sr):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2, 64))
+    w = W.random_digraph_workload(n, float(rng.uniform(0.02, 0.25)), 100 + seed, sr, batch=5,
+                                  self_loops=bool(seed % 2), dyadic=seed % 2 == 0)
+    _check(w, ["path"], tiles=1)
+
+
+def test_c3_reduced_bit_exact():
+    w = W.c3_workload(batch=6, entities=10, rtypes=6, skips=5, ncomp=20)
+    _check(w, ["kinship", "answer"], tiles=2)
+
+
+def test_c3_full_size_sampled_bit_exact(monkeypatch):
+    """The full 256-sample C3 batch in two launches (kinship, answer); three
+    samples recomputed by the oracle, add-mult tags bit-exact.  (Forced: by
+    default a batch this large takes the per-round path, which is faster.)"""
+    monkeypatch.setenv("LOBSTER_TILE", "1")
+    w = W.c3_workload()
+    _check(w, ["kinship", "answer"], tiles=2, samples=[0, 100, 255])
+
+
+def test_c3_max_min():
+    w = W.c3_workload(semiring=1, batch=4, entities=12, rtypes=8, skips=6, ncomp=30)
+    _check(w, ["kinship", "answer"], tiles=2)
+
+
+NONLINEAR_PROGRAM = """
+type edge(x: i32, y: i32)
+rel path(x, y) :- edge(x, y) or (path(x, z) and path(z, y)).
+output path
+"""
+
+EVEN_ODD_PROGRAM = """
+type edge(x: i32, y: i32)
+rel odd(x, y) :- edge(x, y) or (even(x, z) and edge(z, y)).
+rel even(x, y) :- odd(x, z), edge(z, y).
+output odd
+output even
+"""
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2])
+def test_nonlinear_and_mutual_recursion(sr):
+    """Two variants per rule (Δ⋈S, NEW⋈Δ) and two relations in one stratum."""
+    mk = W.random_dag_workload if sr == 2 else W.random_digraph_workload
+    w = mk(18, 0.15, 7, sr, batch=3, program=NONLINEAR_PROGRAM)
+    _check(w, ["path"], tiles=1)
+    w = mk(20, 0.15, 8, sr, batch=3, program=EVEN_ODD_PROGRAM)
+    _check(w, ["odd", "even"], tiles=1)
+
+
+def test_constants_repeats_filters_arity0():
+    prog = """
+    type e(x: i32, y: i32)
+    type lab(x: i32, l: i32)
+    rel loop(x) :- e(x, x).
+    rel two(x, y) :- e(x, z), e(z, y), x != y, lab(z, 7).
+    rel same(x) :- e(x, y), lab(y, l), x == l.
+    rel tgt(y) :- e(3, y).
+    rel pair(x, 5) :- e(x, 5).
+    rel any() :- two(x, y), x != 4.
+    output two
+    """
+    e = _facts([[0, 1, 1, 2, 3, 3, 4, 5, 5], [1, 1, 2, 0, 4, 5, 3, 5, 0]], [0] * 9,
+               [0.5, 0.9, 0.25, 0.75, 0.5, 0.625, 0.125, 1.0, 0.375])
+    lab = _facts([[1, 2, 4, 5, 0], [7, 7, 7, 0, 9]], [0] * 5, [1.0, 0.5, 0.75, 1.0, 0.5])
+    for sr in (0, 1, 2):
+        w = W.Workload("t", prog, sr, 1, {"e": e, "lab": lab})
+        _check(w, ["loop", "two", "same", "tgt", "pair", "any"], tiles=6)
+
+
+def test_shared_relation_and_empty_samples():
+    prog = """
+    shared type e(x: i32, y: i32)
+    type src(x: i32)
+    rel r(y) :- src(x), e(x, y).
+    rel r(y) :- r(x), e(x, y).
+    output r
+    """
+    e = W.Facts([np.array([0, 1, 2, 3, 1], np.int32), np.array([1, 2, 3, 0, 4], np.int32)], None,
+                np.array([0.5, 0.5, 0.75, 0.25, 0.125], np.float32))
+    src = _facts([[0, 2, 4]], [0, 2, 4], [1.0, 0.5, 1.0])  # samples 1 and 3 have no source
+    for sr in (0, 1):
+        w = W.Workload("t", prog, sr, 5, {"e": e, "src": src})
+        _check(w, ["r"], tiles=1)
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2])
+def test_empty_and_duplicates(sr):
+    w = W.Workload("t", W.PATH_PROGRAM, sr, 2, {"edge": _facts([[], []])})
+    _check(w, ["path"])
+    f = _facts([[0, 0, 1, 2, 2, 3], [1, 1, 2, 2, 0, 3]], [0, 0, 0, 1, 1, 1],
+               [0.5, 0.75, 0.0, 0.25, 1.0, 0.5])
+    w = W.Workload("t", W.PATH_PROGRAM, sr, 2, {"edge": f})
+    if sr != 2:  # (cyclic under add-mult: defined by the algorithm; covered below)
+        _check(w, ["path"], tiles=1)
+
+
+def test_cyclic_addmult_algorithmic():
+    """add-mult on a cycle converges by fp32 absorption: the tile path equals the
+    oracle bit for bit (same canonical summation order)."""
+    f = _facts([[0, 1, 2], [1, 2, 0]], [0, 0, 0], [0.5, 0.5, 0.5])
+    w = W.Workload("t", W.PATH_PROGRAM, 2, 1, {"edge": f})
+    _check(w, ["path"], tiles=1)
+
+
+def test_tile_equals_per_round_path(monkeypatch):
+    """Same inputs through the one-launch tile stratum and the per-round path:
+    identical tuples; add-mult tags within 1 ulp (the per-round path sums in
+    candidate order, the tile path in canonical order)."""
+    monkeypatch.setenv("LOBSTER_TILE", "1")
+    w = W.c3_workload(batch=8, entities=12, rtypes=8, skips=6, ncomp=30)
+    eng, st, _ = engine_run(w)
+    a = eng.output("kinship")
+    monkeypatch.setenv("LOBSTER_NO_TILE", "1")
+    eng2, st2, _ = engine_run(w)
+    b = eng2.output("kinship")
+    assert st["tile_strata"] == 2 and st2["tile_strata"] == 0
+    assert np.array_equal(a.sample_ids, b.sample_ids) and np.array_equal(a.cols, b.cols)
+    ulp = np.abs(a.probs.view(np.int32).astype(np.int64) - b.probs.view(np.int32).astype(np.int64))
+    assert int(ulp.max(initial=0)) <= 1
+    assert st["rounds_total"] == st2["rounds_total"]
+
+
+def test_iteration_cap():
+    from paper_2503_21937_b200 import Engine, LobsterError, _lib
+    w = W.c1_workload(2)
+    eng = Engine(w.program, 2, batch_size=1, max_iters=2)
+    eng.push_facts(w.facts)
+    with pytest.raises(LobsterError) as e:
+        eng.run()
+    assert e.value.status == _lib.E_ITER_CAP
+
+
+def test_determinism():
+    w = W.c3_workload(batch=16, entities=14, rtypes=10, skips=6, ncomp=50)
+    outs = []
+    for _ in range(2):
+        eng, _, _ = engine_run(w)
+        o = eng.output("kinship")
+        outs.append((o.cols.tobytes(), o.probs.tobytes()))
+        eng.close()
+    assert outs[0] == outs[1]
