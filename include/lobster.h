@@ -71,14 +71,21 @@ typedef enum {
  *                        more likely proof, tie rules as DIFF_MAX_MULT_PROB;
  *                        gradient ∂p/∂p_f = Π of the proof's other facts
  *                        (§2, 617-628 §3.5).  GPU: rules may read
- *                        their own stratum at most once (linear recursion)  */
+ *                        their own stratum at most once (linear recursion)
+ *   DIFF_ADD_MULT_PROB : dual numbers (p, ∂p/∂p_f): p exactly as
+ *                        ADD_MULT_PROB; gradients of every `output` relation are
+ *                        the derivative of the add-mult result (finite
+ *                        derivations, e.g. DAG inputs), computed in reverse mode
+ *                        by a generated adjoint program over the final relations
+ *                        (reading "diff-add-mult")                  */
 typedef enum {
   LOBSTER_UNIT = 0,
   LOBSTER_MAX_MIN_PROB = 1,
   LOBSTER_ADD_MULT_PROB = 2,
   LOBSTER_DIFF_MAX_MULT_PROB = 3,
   LOBSTER_DIFF_MAX_MIN_PROB = 4,
-  LOBSTER_DIFF_TOP1_PROOFS = 5
+  LOBSTER_DIFF_TOP1_PROOFS = 5,
+  LOBSTER_DIFF_ADD_MULT_PROB = 6
 } lobster_semiring;
 
 typedef struct {

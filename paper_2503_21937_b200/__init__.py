@@ -10,7 +10,7 @@
 The compute path is the CUDA library liblobster.so (csrc/, include/lobster.h);
 this package only marshals arguments.
 """
-from ._lib import (ADD_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, EXPORTS, LIB_PATH, MAX_MIN_PROB,  # noqa: F401
+from ._lib import (ADD_MULT_PROB, DIFF_ADD_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_MAX_MULT_PROB, DIFF_TOP1_PROOFS, EXPORTS, LIB_PATH, MAX_MIN_PROB,  # noqa: F401
                    SEMIRINGS, UNIT)
 from .engine import Engine, Group, LobsterError, RelationOutput  # noqa: F401
 

@@ -14,10 +14,10 @@ LIB_PATH = os.path.join(HERE, "liblobster.so")
 OK, E_INVALID_ARG, E_PARSE, E_SCHEMA, E_RANGE, E_STATE, E_OOM, E_ITER_CAP, E_CUDA, E_NCCL = range(10)
 STATUS_NAMES = ["OK", "INVALID_ARG", "PARSE", "SCHEMA", "RANGE", "STATE", "OOM", "ITER_CAP", "CUDA", "NCCL"]
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS, DIFF_ADD_MULT_PROB = 0, 1, 2, 3, 4, 5, 6
 SEMIRINGS = {"unit": UNIT, "max-min-prob": MAX_MIN_PROB, "add-mult-prob": ADD_MULT_PROB,
              "diff-max-mult-prob": DIFF_MAX_MULT_PROB, "diff-max-min-prob": DIFF_MAX_MIN_PROB,
-             "diff-top-1-proofs": DIFF_TOP1_PROOFS}
+             "diff-top-1-proofs": DIFF_TOP1_PROOFS, "diff-add-mult-prob": DIFF_ADD_MULT_PROB}
 
 
 class Options(ctypes.Structure):

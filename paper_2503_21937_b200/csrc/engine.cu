@@ -220,6 +220,9 @@ struct Ctx {
   int semi = 0;
   bool omin = false;  // diff-max-min-prob (semi == S_MAXMULT internally)
   bool top1 = false;  // diff-top-1-proofs (semi == S_MAXMULT internally; sorted stores, k_top1.cu)
+  bool dadd = false;  // diff-add-mult-prob (semi == S_ADDMULT internally; adjoint-program gradients)
+  bool unbounded_tags = false;  // internal child contexts: pushed tags are unclamped add-mult values
+  std::string program_text;
   DBuf<int32_t> fact_group;  // top-1-proof exclusion group per fact (-1: none)
   bool has_groups = false;
   Program prog;
@@ -387,7 +390,7 @@ struct Ctx {
   // ---------------------------------------------------------- program load
   void load(const char* text, int semiring) {
     if (loaded) throw Failure(LOBSTER_E_STATE, "program already loaded");
-    if (semiring < 0 || semiring > 5) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
+    if (semiring < 0 || semiring > 6) throw Failure(LOBSTER_E_INVALID_ARG, "bad semiring");
     if (!text) throw Failure(LOBSTER_E_INVALID_ARG, "program text is NULL");
     prog = parse_program(text);
     // diff-max-min-prob runs on the max-mult machinery (packed (p, stamp,
@@ -395,7 +398,11 @@ struct Ctx {
     // one-hot gradient (reading "diff-max-min")
     omin = semiring == LOBSTER_DIFF_MAX_MIN_PROB;
     top1 = semiring == LOBSTER_DIFF_TOP1_PROOFS;
-    semi = (omin || top1) ? S_MAXMULT : semiring;
+    // diff-add-mult-prob: the forward fixpoint is add-mult; gradients come from
+    // the adjoint program (dadd_gradients)
+    dadd = semiring == LOBSTER_DIFF_ADD_MULT_PROB;
+    semi = (omin || top1) ? S_MAXMULT : (dadd ? S_ADDMULT : semiring);
+    program_text = text;
     for (auto& r : prog.rels)
       if (r.arity > MAXARITY) throw Failure(LOBSTER_E_PARSE, "relation " + r.name + ": arity above 8 is unsupported");
     for (auto& R : prog.rules) {
@@ -461,8 +468,8 @@ struct Ctx {
     if (x && (rank < 0 || rank >= x->world)) throw Failure(LOBSTER_E_INVALID_ARG, "rank outside the group");
     if (x && opt.world_size > 1)
       throw Failure(LOBSTER_E_INVALID_ARG, "key partitioning and batch sharding (world_size > 1) are exclusive");
-    if (x && semi == S_MAXMULT)
-      throw Failure(LOBSTER_E_INVALID_ARG, "key partitioning supports unit, max-min and add-mult (no witnesses)");
+    if (x && (semi == S_MAXMULT || dadd))
+      throw Failure(LOBSTER_E_INVALID_ARG, "key partitioning supports unit, max-min and add-mult (no gradients)");
     if (x)
       for (const Rule& R : prog.rules) {
         const int s = prog.rels[R.head_rel].stratum;
@@ -518,7 +525,7 @@ struct Ctx {
       uint32_t* dflag = arena.get<uint32_t>(1);
       cuda_check(cudaMemsetAsync(dflag, 0, 4, st), "memset");
       if (sample_base && !R.shared) launch_add_i32(S.in.sid.ptr() + base, n, -sample_base, st);
-      launch_validate((probs && semi != S_UNIT) ? S.in.p.ptr() + base : nullptr,
+      launch_validate((probs && semi != S_UNIT && !unbounded_tags) ? S.in.p.ptr() + base : nullptr,
                       R.shared ? nullptr : S.in.sid.ptr() + base, n, opt.batch_size, dflag, st);
       kcheck("validate");
       cuda_check(cudaMemcpyAsync(flags, dflag, 4, cudaMemcpyDeviceToHost, st), "D2H");
@@ -1740,7 +1747,7 @@ struct Ctx {
       round_cap_hit = run_strata();
       for (size_t r = 0; r < prog.rels.size(); ++r)
         if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
-      if (!round_cap_hit && semi == S_MAXMULT) {
+      if (!round_cap_hit && (semi == S_MAXMULT || dadd)) {
         Phase ph(this, 4);
         HostTimer htg(host_ms[5]);
         gradients();
@@ -1760,6 +1767,7 @@ struct Ctx {
   // largest power-of-two sample range whose dense-eligible relations fit 30 bits
   int32_t choose_micro_batch() {
     const int32_t B = opt.batch_size;
+    if (dadd) return B;  // the adjoint program reads the pushed facts of the whole batch
     if (opt.micro_batch > 0) return std::min(opt.micro_batch, B);
     const int sb_full = bits_for((uint64_t)B - 1);
     int excess = 0;
@@ -2927,9 +2935,190 @@ struct Ctx {
     }
   }
 
+  // ------------------------------------------- diff-add-mult: adjoint program
+  // Reverse mode over the final relations.  For an output relation O (arity k)
+  // every relation X it depends on gets an adjoint __adj_X(o1..ok, x...) =
+  // ∂O(o)/∂tag(X(x)); for each rule H(h) :- B1, .., Bn and each atom j:
+  //   __adj_Bj(o, bj) :- __adj_H(o, h), __fwd_B1, .., (no Bj), .., __fwd_Bn, __dom_Bj(bj), filters
+  // (__fwd_X: X's final tuples and tags; __dom_X: the same tuples, tag 1, so
+  // every variable of Bj is bound and only existing tuples get adjoints), seeded
+  // by __adj_O(o, o) = 1, and the input facts read their entries through
+  //   __grad(o, f) :- __adj_E(o, e), __fid_E(e, f)
+  // (duplicate facts are ⊕-merged by +, so each gets ∂ = 1 · adjoint).  The
+  // program is evaluated by a child context under add-mult on this stream:
+  // the same kernels, no CPU path.  On finite derivation sets the adjoint sums
+  // equal the dual-number derivative of the add-mult result.
+  static std::string cols_decl(int n, const char* pfx) {
+    std::string t;
+    for (int c = 0; c < n; ++c) t += (c ? ", " : "") + std::string(pfx) + std::to_string(c) + ": i32";
+    return t;
+  }
+  std::string term_text(const Rule& R, const Term& t) const {
+    return t.is_var() ? R.var_names[t.var] : std::to_string(t.cst);
+  }
+  static std::string join_args(const std::vector<std::string>& v) {
+    std::string t;
+    for (size_t i = 0; i < v.size(); ++i) t += (i ? ", " : "") + v[i];
+    return t;
+  }
+  std::string adjoint_program(int O, std::vector<int>& deps) const {
+    const int nr = (int)prog.rels.size();
+    std::vector<char> in(nr, 0);
+    in[O] = 1;
+    for (bool grew = true; grew;) {  // relations O depends on
+      grew = false;
+      for (const Rule& R : prog.rules)
+        if (in[R.head_rel])
+          for (auto& a : R.body)
+            if (!in[a.rel]) in[a.rel] = grew = true;
+    }
+    deps.clear();
+    for (int r = 0; r < nr; ++r)
+      if (in[r]) deps.push_back(r);
+    const int k = prog.rels[O].arity;
+    std::vector<std::string> ov;
+    for (int c = 0; c < k; ++c) ov.push_back("__o" + std::to_string(c));
+    auto with_o = [&](const std::vector<std::string>& rest) {
+      std::vector<std::string> v = ov;
+      v.insert(v.end(), rest.begin(), rest.end());
+      return join_args(v);
+    };
+    auto atom_args = [&](const Rule& R, const std::vector<Term>& ts) {
+      std::vector<std::string> v;
+      for (auto& t : ts) v.push_back(term_text(R, t));
+      return v;
+    };
+    std::string t = "type __seed(" + cols_decl(k, "c") + ")\n";
+    for (int r : deps) {
+      const Relation& X = prog.rels[r];
+      const std::string sh = X.shared ? "shared " : "";
+      t += sh + "type __fwd_" + X.name + "(" + cols_decl(X.arity, "c") + ")\n";
+      t += sh + "type __dom_" + X.name + "(" + cols_decl(X.arity, "c") + ")\n";
+      if (X.input) t += sh + "type __fid_" + X.name + "(" + cols_decl(X.arity + 1, "c") + ")\n";
+    }
+    // seed: ∂O(o)/∂O(x) = [o == x]
+    t += "rel __adj_" + prog.rels[O].name + "(" + with_o(ov) + ") :- __seed(" + join_args(ov) + ").\n";
+    for (const Rule& R : prog.rules) {
+      if (!in[R.head_rel]) continue;
+      const std::vector<std::string> hargs = atom_args(R, R.head);
+      for (size_t j = 0; j < R.body.size(); ++j) {
+        const BodyAtom& Bj = R.body[j];
+        const std::vector<std::string> bargs = atom_args(R, Bj.args);
+        std::string body = "__adj_" + prog.rels[R.head_rel].name + "(" + with_o(hargs) + ")";
+        for (size_t i = 0; i < R.body.size(); ++i)
+          if (i != j)
+            body += ", __fwd_" + prog.rels[R.body[i].rel].name + "(" + join_args(atom_args(R, R.body[i].args)) + ")";
+        body += ", __dom_" + prog.rels[Bj.rel].name + "(" + join_args(bargs) + ")";
+        for (const Compare& cp : R.cmps)
+          body += ", " + term_text(R, cp.a) + (cp.neq ? " != " : " == ") + term_text(R, cp.b);
+        t += "rel __adj_" + prog.rels[Bj.rel].name + "(" + with_o(bargs) + ") :- " + body + ".\n";
+      }
+    }
+    for (int r : deps) {
+      const Relation& X = prog.rels[r];
+      if (!X.input) continue;
+      std::vector<std::string> e;
+      for (int c = 0; c < X.arity; ++c) e.push_back("__e" + std::to_string(c));
+      std::vector<std::string> ef = e;
+      ef.push_back("__f");
+      t += "rel __grad(" + with_o({"__f"}) + ") :- __adj_" + X.name + "(" + with_o(e) + "), __fid_" + X.name + "(" +
+           join_args(ef) + ").\n";
+    }
+    return t;
+  }
+
+  // relation r's stored tuples unpacked (sample ids local to the batch, columns SoA)
+  void unpack_local(RelState& S, int r, int32_t* sid, int32_t* cols) {
+    ensure_sorted(S);
+    const int ar = prog.rels[r].arity;
+    uint8_t* dsh = arena.get<uint8_t>(3 * 8 + 64);
+    std::vector<uint8_t> hb(16 + 32, 0);
+    for (int c = 0; c < ar; ++c) { hb[c] = (uint8_t)S.L.shift[c]; hb[8 + c] = (uint8_t)S.L.bits[c]; }
+    std::memcpy(hb.data() + 16, S.L.mins.data(), ar * 4);
+    cuda_check(cudaMemcpyAsync(dsh, hb.data(), hb.size(), cudaMemcpyHostToDevice, st), "H2D");
+    launch_unpack(S.key.ptr(), S.n, S.L.has_sample, (uint8_t)S.L.sshift, ar, dsh, dsh + 8,
+                  reinterpret_cast<int32_t*>(dsh + 16), sid, cols, st);
+    kcheck("unpack");
+  }
+
+  void dadd_gradients() {
+    for (int O = 0; O < (int)prog.rels.size(); ++O) {
+      const Relation& OR = prog.rels[O];
+      if (!OR.output || OR.input) continue;
+      std::vector<int> deps;
+      const std::string text = adjoint_program(O, deps);
+      if (log_level >= 2) fprintf(stderr, "[lobster] adjoint program of %s:\n%s", OR.name.c_str(), text.c_str());
+      lobster_options o = opt;
+      o.batch_size = batch_cur;
+      o.world_size = 1;
+      o.rank = 0;
+      o.micro_batch = 0;
+      o.arena_bytes = 0;
+      std::unique_ptr<Ctx> ch(new Ctx());
+      ch->create(&o);
+      ch->unbounded_tags = true;
+      ch->load(text.c_str(), LOBSTER_ADD_MULT_PROB);
+      int64_t first = 0;
+      auto push = [&](const std::string& name, int64_t n, int ar, const int32_t* cols, const int32_t* sid,
+                      const float* p) {
+        std::vector<const int32_t*> cp(std::max(ar, 1), nullptr);
+        for (int c = 0; c < ar; ++c) cp[c] = cols + (int64_t)c * n;
+        ch->push(name.c_str(), n, cp.data(), sid, p, &first);
+      };
+      for (int r : deps) {
+        RelState& X = *rels[r];
+        const Relation& XR = prog.rels[r];
+        const int64_t n = (ensure_sorted(X), X.n);
+        int32_t* sid = arena.get<int32_t>(n);
+        int32_t* cols = arena.get<int32_t>(std::max<int64_t>(1, (int64_t)XR.arity * n));
+        unpack_local(X, r, sid, cols);
+        push("__fwd_" + XR.name, n, XR.arity, cols, XR.shared ? nullptr : sid, X.p.ptr());
+        push("__dom_" + XR.name, n, XR.arity, cols, XR.shared ? nullptr : sid, nullptr);
+        if (r == O) push("__seed", n, XR.arity, cols, sid, nullptr);  // O's tuples, tag 1
+        if (XR.input) {  // every pushed fact with its id (duplicates included)
+          const int64_t m = X.in.n;
+          int32_t* fc = arena.get<int32_t>(std::max<int64_t>(1, (int64_t)(XR.arity + 1) * m));
+          for (int c = 0; c < XR.arity && m; ++c)
+            cuda_check(cudaMemcpyAsync(fc + (int64_t)c * m, X.in.cols[c].ptr(), m * 4, cudaMemcpyDeviceToDevice, st), "fid");
+          if (m) cuda_check(cudaMemcpyAsync(fc + (int64_t)XR.arity * m, X.in.fid.ptr(), m * 4, cudaMemcpyDeviceToDevice, st), "fid");
+          push("__fid_" + XR.name, m, XR.arity + 1, fc, XR.shared ? nullptr : X.in.sid.ptr(), nullptr);
+        }
+      }
+      ch->run(nullptr);
+      lobster_output g{};
+      const auto git = ch->prog.rel_id.find("__grad");
+      RelState& S = *rels[O];
+      const int k = OR.arity;
+      const int64_t n = S.n;
+      S.goff.reserve(n + 1);
+      if (git == ch->prog.rel_id.end() || !n) {  // no input facts reach O
+        cuda_check(cudaMemsetAsync(S.goff.ptr(), 0, (n + 1) * 8, st), "memset");
+        S.ng = 0;
+        S.gfid.reserve(1);
+        S.gval.reserve(1);
+      } else {
+        ch->output_get("__grad", 1, &g);
+        int32_t* osid = arena.get<int32_t>(n);
+        int32_t* ocols = arena.get<int32_t>(std::max<int64_t>(1, (int64_t)k * n));
+        unpack_local(S, O, osid, ocols);
+        S.ng = g.n;
+        S.gfid.reserve(std::max<int64_t>(1, g.n));
+        S.gval.reserve(std::max<int64_t>(1, g.n));
+        launch_grad_rows(osid, ocols, n, k, g.sample_ids, g.columns[0], g.n, S.goff.ptr(), st);
+        launch_widen_i32(g.columns[k], g.n, S.gfid.ptr(), st);
+        if (g.n) cuda_check(cudaMemcpyAsync(S.gval.ptr(), g.probs, g.n * 4, cudaMemcpyDeviceToDevice, st), "grad");
+        kcheck("adjoint rows");
+      }
+      sync();  // the child's buffers are released with it
+      S.has_grad = true;
+      stats.candidates += ch->stats.candidates;
+    }
+  }
+
   // --------------------------------------------------------- gradients (A11)
   void gradients() {
     if (top1) return top1_gradients();
+    if (dadd) return dadd_gradients();
     const int nr = (int)prog.rels.size();
     for (int r = 0; r < nr; ++r)  // walks start from the output relations' sorted rows
       if (prog.rels[r].output) ensure_sorted(*rels[r]);
@@ -3163,7 +3352,8 @@ struct Ctx {
     if (it == prog.rel_id.end()) throw Failure(LOBSTER_E_INVALID_ARG, std::string("unknown relation ") + relname);
     if (!ran) throw Failure(LOBSTER_E_STATE, "backward before a successful run");
     RelState& S = *rels[it->second];
-    if (semi != S_MAXMULT || !S.has_grad) throw Failure(LOBSTER_E_INVALID_ARG, "no gradients for this relation");
+    if ((semi != S_MAXMULT && !dadd) || !S.has_grad)
+      throw Failure(LOBSTER_E_INVALID_ARG, "no gradients for this relation");
     const int64_t nf = num_facts_db;
     cuda_check(cudaMemsetAsync(grad_facts, 0, nf * sizeof(float), st), "memset");
     const int64_t ng = S.ng;

@@ -243,6 +243,37 @@ __global__ void sample_offsets_i32_k(const int32_t* __restrict__ sid, int64_t n,
   off[s] = lo;
 }
 
+
+// diff-add-mult: per output row i (sorted by (sample, cols)), the first row of
+// the adjoint's __grad relation (sorted by (sample, cols, fact)) with the same
+// (sample, cols) prefix; goff[n] = ng.  Columns are SoA (column c at c * rows).
+__global__ void grad_rows_k(const int32_t* __restrict__ osid, const int32_t* __restrict__ ocols, int64_t n, int k,
+                            const int32_t* __restrict__ gsid, const int32_t* __restrict__ gcols, int64_t ng,
+                            int64_t* __restrict__ goff) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) {
+      goff[n] = ng;
+      continue;
+    }
+    int64_t lo = 0, hi = ng;
+    while (lo < hi) {  // first g with (gsid, gcols[0..k)) >= (osid, ocols)
+      const int64_t mid = (lo + hi) >> 1;
+      int cmp = gsid[mid] < osid[i] ? -1 : (gsid[mid] > osid[i] ? 1 : 0);
+      for (int c = 0; c < k && cmp == 0; ++c) {
+        const int32_t a = gcols[(int64_t)c * ng + mid], b = ocols[(int64_t)c * n + i];
+        cmp = a < b ? -1 : (a > b ? 1 : 0);
+      }
+      if (cmp < 0) lo = mid + 1; else hi = mid;
+    }
+    goff[i] = lo;
+  }
+}
+
+__global__ void widen_i32_k(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
 }  // namespace
 
 void launch_add_i32(int32_t* a, int64_t n, int32_t v, cudaStream_t st) {
@@ -315,6 +346,18 @@ void launch_dense_sum(const uint64_t* key, const uint32_t* val, const uint32_t* 
     note_launch();
     dense_sum_k<<<grid_for(n, 256), 256, 0, st>>>(key, val, n, dense);
   }
+}
+
+void launch_grad_rows(const int32_t* osid, const int32_t* ocols, int64_t n, int k, const int32_t* gsid,
+                      const int32_t* gcols, int64_t ng, int64_t* goff, cudaStream_t st) {
+  note_launch();
+  grad_rows_k<<<grid_for(n + 1, 256), 256, 0, st>>>(osid, ocols, n, k, gsid, gcols, ng, goff);
+}
+
+void launch_widen_i32(const int32_t* in, int64_t n, int64_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch();
+  widen_i32_k<<<grid_for(n, 256), 256, 0, st>>>(in, n, out);
 }
 
 }  // namespace lob

@@ -411,6 +411,11 @@ void launch_top1_grad(const uint32_t* pool, const uint64_t* pof, const uint32_t*
                       const float* fact_p, int64_t* goff, int64_t* gfid, float* gval, double* scratch,
                       cudaStream_t st);
 
+// diff-add-mult: CSR offsets of output rows into the adjoint program's __grad rows
+void launch_grad_rows(const int32_t* osid, const int32_t* ocols, int64_t n, int k, const int32_t* gsid,
+                      const int32_t* gcols, int64_t ng, int64_t* goff, cudaStream_t st);
+void launch_widen_i32(const int32_t* in, int64_t n, int64_t* out, cudaStream_t st);
+
 // diff-max-min: one-hot gradient on each tuple's minimum leaf (goff[t] = t)
 void launch_grad_onehot(const uint64_t* sorted_tf, int64_t nleaf, const float* fact_p, int64_t ntup,
                         const int64_t* loff, int64_t* goff, int64_t* gfid, float* gval, cudaStream_t st);

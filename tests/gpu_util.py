@@ -5,7 +5,7 @@ import numpy as np
 
 import oracle
 
-REL_TOL = {0: 0.0, 1: 0.0, 2: 1e-5, 3: 0.0, 4: 0.0, 5: 0.0}   # unit / max-min / max-mult / diff-max-min bit-exact; add-mult 1e-5
+REL_TOL = {0: 0.0, 1: 0.0, 2: 1e-5, 3: 0.0, 4: 0.0, 5: 0.0, 6: 1e-5}   # unit / max-min / max-mult / diff-max-min bit-exact; add-mult 1e-5
 GRAD_TOL = 1e-6
 
 

@@ -72,7 +72,7 @@ PROGRAMS = {
     "sg": SG_PROGRAM,
 }
 
-UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS = 0, 1, 2, 3, 4, 5
+UNIT, MAX_MIN_PROB, ADD_MULT_PROB, DIFF_MAX_MULT_PROB, DIFF_MAX_MIN_PROB, DIFF_TOP1_PROOFS, DIFF_ADD_MULT_PROB = 0, 1, 2, 3, 4, 5, 6
 
 
 @dataclass
