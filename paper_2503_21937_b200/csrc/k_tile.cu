@@ -32,368 +32,26 @@
 
 #include "devmem.hpp"
 #include "device_util.cuh"
+#include "tile_device.cuh"
 
 namespace lob {
 namespace {
 
 constexpr int TILE_THREADS = 512;
 
-__device__ __forceinline__ bool tbit(const uint32_t* b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
-
-template <int SEMI>
-__device__ __forceinline__ float oplus_state(float s, float b) {
-  if constexpr (SEMI == S_ADDMULT) return (float)__dadd_rn((double)s, (double)b);
-  else return b > s ? b : s;  // max-min (unit has no tags)
-}
-
-// Per-thread enumeration state.  Variable values (domains <= 64) are packed
-// 6 bits each into one register word so that nothing is indexed dynamically:
-// the whole enumeration stays in registers (arrays indexed by runtime
-// variable ids or levels went to local memory, which thrashed through L2).
-struct Frame {
-  const TilePlan* P;
-  const uint8_t* sm;
-  int s;
-  unsigned long long vals;
-  double acc;
-  float mx;
-  bool any;
-  uint32_t ncand;
-};
-
-__device__ __forceinline__ int getv(unsigned long long vals, int v) { return (int)((vals >> (6 * v)) & 63ull); }
-__device__ __forceinline__ void setv(unsigned long long& vals, int v, int x) {
-  vals = (vals & ~(63ull << (6 * v))) | ((unsigned long long)x << (6 * v));
-}
-
-__device__ __forceinline__ int32_t arg_coord(const TileAtom& A, int c, unsigned long long vals) {
-  return A.var[c] >= 0 ? getv(vals, A.var[c]) : A.cst[c];
-}
-
-__device__ __forceinline__ unsigned long long fiber(const Frame& F, const TileAtom& A, int ver) {
-  const TileRel& T = F.P->rel[A.rel];
-  const int c = A.fcol;
-  int f = 0;
-  for (int q = 0; q < T.ncols; ++q)
-    if (q != c) f += arg_coord(A, q, F.vals) * T.fstride[c][q];
-  if (!T.local) return __ldg(T.fib[c] + (T.shared ? 0 : (int64_t)F.s * T.nfib[c]) + f);
-  const unsigned long long* S = reinterpret_cast<const unsigned long long*>(F.sm + T.sm_fib[0][c]);
-  const unsigned long long* D = reinterpret_cast<const unsigned long long*>(F.sm + T.sm_fib[1][c]);
-  return ver == TV_OLD ? S[f] : (ver == TV_DELTA ? D[f] : (S[f] | D[f]));
-}
-
-__device__ __forceinline__ int atom_slot(const TileRel& T, const TileAtom& A, unsigned long long vals) {
-  int slot = 0;
-  for (int q = 0; q < T.ncols; ++q) slot += arg_coord(A, q, vals) * T.stride[q];
-  return slot;
-}
-
-__device__ __forceinline__ bool present(const Frame& F, const TileAtom& A, int ver) {
-  const TileRel& T = F.P->rel[A.rel];
-  const int slot = atom_slot(T, A, F.vals);
-  if (!T.local) return tbit(T.bits + (T.shared ? 0 : (int64_t)F.s * ((T.D + 31) >> 5)), slot);
-  const uint32_t* Sb = reinterpret_cast<const uint32_t*>(F.sm + T.sm_bits[0]);
-  const uint32_t* Db = reinterpret_cast<const uint32_t*>(F.sm + T.sm_bits[1]);
-  if (ver == TV_OLD) return tbit(Sb, slot);
-  if (ver == TV_DELTA) return tbit(Db, slot);
-  return tbit(Sb, slot) || tbit(Db, slot);
-}
-
-template <int SEMI>
-__device__ __forceinline__ float atom_tag(const Frame& F, const TileAtom& A, int ver) {
-  const TileRel& T = F.P->rel[A.rel];
-  const int slot = atom_slot(T, A, F.vals);
-  if (!T.local) return __ldg(T.tag + (T.shared ? 0 : (int64_t)F.s * T.D) + slot);
-  const float* St = reinterpret_cast<const float*>(F.sm + T.sm_tag[0]);
-  const float* Dt = reinterpret_cast<const float*>(F.sm + T.sm_tag[1]);
-  if (ver == TV_OLD) return St[slot];
-  if (ver == TV_DELTA) return Dt[slot];
-  const uint32_t* Sb = reinterpret_cast<const uint32_t*>(F.sm + T.sm_bits[0]);
-  const uint32_t* Db = reinterpret_cast<const uint32_t*>(F.sm + T.sm_bits[1]);
-  const bool sp = tbit(Sb, slot), dp = tbit(Db, slot);
-  return sp ? (dp ? oplus_state<SEMI>(St[slot], Dt[slot]) : St[slot]) : Dt[slot];
-}
-
-__device__ __forceinline__ int32_t cmp_value(int8_t v, int32_t c, const TileRule& R, unsigned long long vals) {
-  return v >= 0 ? getv(vals, v) + R.vmin[v] : c;
-}
-
-__device__ __forceinline__ bool cmps_ok(const TileRule& R, int level, unsigned long long vals) {
-  for (int i = 0; i < R.ncmp; ++i) {
-    const TileCmp& c = R.cmp[i];
-    if (c.level != level) continue;
-    const bool eq = cmp_value(c.va, c.ca, R, vals) == cmp_value(c.vb, c.cb, R, vals);
-    if (c.neq ? eq : !eq) return false;
-  }
-  return true;
-}
-
-// leaf: every alive variant in order; ⊗ left-deep in body order (reading 9)
-template <int SEMI>
-__device__ __forceinline__ void leaf(Frame& F, const TileRule& R, uint32_t alive) {
-  for (int j = 0; j < R.nvariant; ++j) {
-    if (!((alive >> j) & 1u)) continue;
-    F.any = true;
-    F.ncand++;
-    if constexpr (SEMI != S_UNIT) {
-      float t = atom_tag<SEMI>(F, R.atom[0], R.ver[j][0]);
-      for (int a = 1; a < R.natoms; ++a) t = otimes(SEMI, t, atom_tag<SEMI>(F, R.atom[a], R.ver[j][a]));
-      if constexpr (SEMI == S_ADDMULT) F.acc = __dadd_rn(F.acc, (double)t);
-      else F.mx = (F.ncand == 1 || t > F.mx) ? t : F.mx;
-    }
-  }
-}
-
-// Semi-join pruning: an atom whose other variables are all bound at level L
-// (chk == L) but which closes later needs a non-empty fiber in each variant's
-// version, else that variant has no candidate below this value.
-__device__ __forceinline__ uint32_t prune(const Frame& F, const TileRule& R, int L, uint32_t al) {
-  for (int a = 0; a < R.natoms && al; ++a) {
-    const TileAtom& A = R.atom[a];
-    if (A.chk != L || A.level <= L) continue;
-    for (int j = 0; j < R.nvariant; ++j)
-      if (((al >> j) & 1u) && !fiber(F, A, R.ver[j][a])) al &= ~(1u << j);
-  }
-  return al;
-}
-
-// Level L of the canonical enumeration (non-head variables by first
-// appearance, ascending values; reading 8b): per variant, the values of the
-// level's variable are the AND of the fibers of the atoms it closes.  NLEV is
-// a compile-time bound so every per-level mask stays in registers.
-template <int SEMI, int L, int NLEV>
-__device__ __forceinline__ void level(Frame& F, const TileRule& R, uint32_t alive) {
-  if constexpr (L == NLEV) {
-    leaf<SEMI>(F, R, alive);
-  } else {
-    const int v = R.lev_var[L];
-    const unsigned long long full = R.vdom[v] >= 64 ? ~0ull : ((1ull << R.vdom[v]) - 1ull);
-    unsigned long long m[TILE_MAXVAR];
-#pragma unroll
-    for (int j = 0; j < TILE_MAXVAR; ++j) {
-      unsigned long long x = 0;
-      if (j < R.nvariant && ((alive >> j) & 1u)) {
-        x = full;
-        for (int a = 0; a < R.natoms && x; ++a)
-          if (R.atom[a].level == L) x &= fiber(F, R.atom[a], R.ver[j][a]);
-      }
-      m[j] = x;
-    }
-    unsigned long long rem = m[0] | m[1] | m[2] | m[3];
-    while (rem) {
-      const int b = __ffsll((long long)rem) - 1;
-      rem &= rem - 1;
-      setv(F.vals, v, b);
-      if (!cmps_ok(R, L, F.vals)) continue;
-      uint32_t al = 0;
-#pragma unroll
-      for (int j = 0; j < TILE_MAXVAR; ++j) al |= (uint32_t)((m[j] >> b) & 1ull) << j;
-      al = prune(F, R, L, al);
-      if (al) level<SEMI, L + 1, NLEV>(F, R, al);
-    }
-  }
-}
-
-template <int SEMI>
-__device__ __forceinline__ void enumerate(Frame& F, const TileRule& R, uint32_t alive) {
-  switch (R.nlev) {
-    case 0: level<SEMI, 0, 0>(F, R, alive); break;
-    case 1: level<SEMI, 0, 1>(F, R, alive); break;
-    case 2: level<SEMI, 0, 2>(F, R, alive); break;
-    case 3: level<SEMI, 0, 3>(F, R, alive); break;
-    case 4: level<SEMI, 0, 4>(F, R, alive); break;
-    default: level<SEMI, 0, 5>(F, R, alive); break;
-  }
-}
-
-// U of head slot h of local relation `hr` (one round; seed = round 1)
-template <int SEMI>
-__device__ __forceinline__ void eval_head(Frame& F, int hr, int h, bool seed) {
-  const TilePlan& P = *F.P;
-  const TileRel& H = P.rel[hr];
-  for (int ri = 0; ri < P.nrule; ++ri) {
-    const TileRule& R = P.rule[ri];
-    if (R.head != hr || (R.seed != 0) != seed) continue;
-    bool ok = true;
-    uint32_t bound = 0;
-    F.vals = 0;
-    int x = h;
-    for (int c = H.ncols - 1; c >= 0 && ok; --c) {  // head slot -> column coordinates -> variables
-      const int co = x % H.dom[c];
-      x /= H.dom[c];
-      const int v = R.hvar[c];
-      if (v < 0) {
-        ok = R.hcst[c] == co;
-      } else if ((bound >> v) & 1u) {
-        ok = getv(F.vals, v) == co;  // repeated head variable
-      } else {
-        bound |= 1u << v;
-        setv(F.vals, v, co);
-      }
-    }
-    if (!ok || !cmps_ok(R, -1, F.vals)) continue;
-    uint32_t alive = (1u << R.nvariant) - 1u;
-    for (int a = 0; a < R.natoms && alive; ++a) {
-      if (R.atom[a].level >= 0) continue;
-      for (int j = 0; j < R.nvariant; ++j)
-        if (((alive >> j) & 1u) && !present(F, R.atom[a], R.ver[j][a])) alive &= ~(1u << j);
-    }
-    if (alive) alive = prune(F, R, -1, alive);
-    if (alive) enumerate<SEMI>(F, R, alive);
-  }
-}
-
 template <int SEMI>
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_fixpoint_k(const TilePlan* __restrict__ Pg, int* rounds_out,
-                                                                unsigned long long* ncand, int* cap_hit) {
+                                                                   unsigned long long* ncand, int* cap_hit) {
   extern __shared__ __align__(16) uint8_t sm[];
   // The plan (~5.5 KB) is copied to shared memory: every enumeration step
   // indexes it.  (Reading it through a pointer to a > 4 KB __grid_constant__
   // parameter returned garbage under load on sm_100a: out-of-range fiber
   // indexes with >= 8 warps per CTA, found by compute-sanitizer memcheck.)
-  __shared__ __align__(16) TilePlan P;
+  __shared__ __align__(16) TilePlan Q;
   for (int i = threadIdx.x; i < (int)(sizeof(TilePlan) / 4); i += blockDim.x)
-    reinterpret_cast<uint32_t*>(&P)[i] = reinterpret_cast<const uint32_t*>(Pg)[i];
+    reinterpret_cast<uint32_t*>(&Q)[i] = reinterpret_cast<const uint32_t*>(Pg)[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  Frame F;
-  F.P = &P;
-  F.sm = sm;
-  uint64_t my_cand = 0;
-  for (int s = blockIdx.x; s < P.nsamples; s += gridDim.x) {
-    F.s = s;
-    for (int i = threadIdx.x; i < P.clear_words; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0u;
-    __syncthreads();
-    int round = 1;
-    for (;;) {
-      const bool seed = round == 1;
-      // (i) + (iii): U per head slot
-      for (int li = 0; li < P.nlocal; ++li) {
-        const int hr = P.local_rel[li];
-        const TileRel& H = P.rel[hr];
-        uint32_t* Ub = reinterpret_cast<uint32_t*>(sm + H.sm_bits[2]);
-        float* Ut = reinterpret_cast<float*>(sm + H.sm_tag[2]);
-        const int nw = (H.D + 31) >> 5;
-        for (int w = warp; w < nw; w += nwarps) {
-          const int h = (w << 5) + lane;
-          F.acc = 0.0;
-          F.mx = 0.0f;
-          F.any = false;
-          F.ncand = 0;
-          if (h < H.D) eval_head<SEMI>(F, hr, h, seed);
-          my_cand += F.ncand;
-          if (P.trace && F.ncand) atomicAdd(P.trace + ((int64_t)s * 64 + min(round, 63)) * 2, F.ncand);
-          const uint32_t word = __ballot_sync(~0u, F.any);
-          if (lane == 0) Ub[w] = word;
-          if constexpr (SEMI != S_UNIT) {
-            if (F.any) Ut[h] = SEMI == S_ADDMULT ? (float)F.acc : F.mx;
-          }
-        }
-      }
-      __syncthreads();
-      // (ii) S <- S ⊕ Δ; (iv) Δ' = changed or new U
-      int grew = 0;
-      for (int li = 0; li < P.nlocal; ++li) {
-        const TileRel& H = P.rel[P.local_rel[li]];
-        uint32_t* Sb = reinterpret_cast<uint32_t*>(sm + H.sm_bits[0]);
-        uint32_t* Db = reinterpret_cast<uint32_t*>(sm + H.sm_bits[1]);
-        const uint32_t* Ub = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[2]);
-        const int nw = (H.D + 31) >> 5;
-        for (int w = warp; w < nw; w += nwarps) {
-          const int h = (w << 5) + lane;
-          const uint32_t Sw = Sb[w], Dw = Db[w], Uw = Ub[w], bit = 1u << lane;
-          const bool sp = Sw & bit, dp = Dw & bit, up = Uw & bit;
-          bool nd;
-          if constexpr (SEMI == S_UNIT) {
-            nd = up && !(sp || dp);
-          } else {
-            float* St = reinterpret_cast<float*>(sm + H.sm_tag[0]);
-            float* Dt = reinterpret_cast<float*>(sm + H.sm_tag[1]);
-            const float* Ut = reinterpret_cast<const float*>(sm + H.sm_tag[2]);
-            nd = false;
-            if (h < H.D) {
-              float sv = St[h];
-              if (dp) sv = sp ? oplus_state<SEMI>(sv, Dt[h]) : Dt[h];
-              if (dp) St[h] = sv;
-              if (up) {
-                const float u = Ut[h];
-                nd = !(sp || dp) || __float_as_uint(oplus_state<SEMI>(sv, u)) != __float_as_uint(sv);
-                if (nd) Dt[h] = u;
-              }
-            }
-          }
-          const uint32_t dword = __ballot_sync(~0u, nd);
-          if (lane == 0) {
-            Sb[w] = Sw | Dw;
-            Db[w] = dword;
-          }
-          grew |= nd;
-          if (P.trace && nd) atomicAdd(P.trace + ((int64_t)s * 64 + min(round, 63)) * 2 + 1, 1u);
-        }
-      }
-      __syncthreads();
-      // fibers of S and Δ from the bitmaps
-      for (int li = 0; li < P.nlocal; ++li) {
-        const TileRel& H = P.rel[P.local_rel[li]];
-        const uint32_t* Sb = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[0]);
-        const uint32_t* Db = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[1]);
-        for (int c = 0; c < H.ncols; ++c) {
-          if (!H.nfib[c]) continue;
-          unsigned long long* Sf = reinterpret_cast<unsigned long long*>(sm + H.sm_fib[0][c]);
-          unsigned long long* Df = reinterpret_cast<unsigned long long*>(sm + H.sm_fib[1][c]);
-          for (int f = threadIdx.x; f < H.nfib[c]; f += blockDim.x) {
-            int base = 0, x = f;  // decode the other columns (row-major, c skipped)
-            for (int q = H.ncols - 1; q >= 0; --q) {
-              if (q == c) continue;
-              base += (x % H.dom[q]) * H.stride[q];
-              x /= H.dom[q];
-            }
-            unsigned long long ws = 0, wd = 0;
-            for (int k = 0; k < H.dom[c]; ++k) {
-              const int slot = base + k * H.stride[c];
-              ws |= (unsigned long long)tbit(Sb, slot) << k;
-              wd |= (unsigned long long)tbit(Db, slot) << k;
-            }
-            Sf[f] = ws;
-            Df[f] = wd;
-          }
-        }
-      }
-#ifdef TILE_EXTRA_SYNC
-      __syncthreads();
-#endif
-      if (!__syncthreads_or(grew)) break;
-      if (round >= P.max_iters) {
-        if (threadIdx.x == 0) atomicExch(cap_hit, 1);
-        break;
-      }
-      ++round;
-    }
-    if (threadIdx.x == 0) rounds_out[s] = round;
-    // the final relation -> dense store of the packed layout (present slots only)
-    for (int li = 0; li < P.nlocal; ++li) {
-      const TileRel& H = P.rel[P.local_rel[li]];
-      const uint32_t* Sb = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[0]);
-      const uint32_t* Db = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[1]);
-      const float* St = reinterpret_cast<const float*>(sm + H.sm_tag[0]);
-      for (int h = threadIdx.x; h < H.D; h += blockDim.x) {
-        if (!tbit(Sb, h)) continue;  // Δ' was empty: S holds every tuple
-        (void)Db;
-        uint64_t pk = (uint64_t)s << H.psshift;
-        int x = h;
-        for (int c = H.ncols - 1; c >= 0; --c) {
-          pk |= (uint64_t)(x % H.dom[c]) << H.pshift[c];
-          x /= H.dom[c];
-        }
-        if constexpr (SEMI == S_UNIT) atomicOr(H.dfbits + (pk >> 5), 1u << (pk & 31u));
-        else H.dfp[pk] = St[h];
-      }
-    }
-    __syncthreads();
-  }
-  // candidates: one atomic per warp
-  for (int o = 16; o; o >>= 1) my_cand += __shfl_down_sync(~0u, my_cand, o);
-  if (lane == 0 && my_cand) atomicAdd(ncand, (unsigned long long)my_cand);
+  tile_body<SEMI>(Q, sm, rounds_out, ncand, cap_hit);
 }
 
 __global__ void tile_scatter_k(const __grid_constant__ TileScatter S) {
@@ -448,10 +106,9 @@ void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, un
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_fixpoint_k<SEMI>, TILE_THREADS, P.smem_bytes);
-  if (const char* e = getenv("LOBSTER_TILE_STACK")) cudaDeviceSetLimit(cudaLimitStackSize, (size_t)atoi(e));
-  int grid = std::max(1, std::min(P.nsamples, std::max(1, per_sm) * sms));
   int threads = TILE_THREADS;
   if (const char* e = getenv("LOBSTER_TILE_THREADS")) threads = std::max(32, std::min(TILE_THREADS, atoi(e)));
+  int grid = std::max(1, std::min(P.nsamples, std::max(1, per_sm) * sms));
   if (const char* e = getenv("LOBSTER_TILE_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
   tile_fixpoint_k<SEMI><<<grid, threads, P.smem_bytes, st>>>(dplan, rounds_out, ncand, cap_hit);
 }

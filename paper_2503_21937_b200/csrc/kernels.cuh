@@ -10,6 +10,8 @@
 
 #include <cstdint>
 
+#include "tile_plan.h"
+
 namespace lob {
 
 constexpr uint64_t KEY_DEAD = ~0ull;
@@ -436,83 +438,8 @@ void launch_slice_expand(const uint32_t* dt, const uint32_t* dwi, const uint32_t
                          const uint32_t* Rb, uint32_t* Nb, int W, uint32_t* dirty, unsigned long long* cands,
                          cudaStream_t st);
 
-// ---- small dense per-sample strata (k_tile.cu) ----
-// A stratum whose relations have small per-sample domains runs to fixpoint in
-// ONE launch: one CTA per sample (grid-stride), the stratum's relations dense
-// in shared memory (compact slot = row-major over the true column domains),
-// every round pull-evaluated per head slot.  Non-head variables are enumerated
-// in the oracle's canonical order (rule, non-head variables by first
-// appearance, variant), each level's values taken from 64-bit presence fibers
-// of the atoms its variable closes, so add-mult sums are formed in exactly the
-// oracle's fp64 order.
-constexpr int TILE_MAXREL = 6, TILE_MAXRULE = 8, TILE_MAXLEV = 5, TILE_MAXVAR = 4, TILE_MAXCOL = 4, TILE_MAXV = 10;
-enum TileVer : int8_t { TV_EXT = 0, TV_NEW = 1, TV_OLD = 2, TV_DELTA = 3 };
-struct TileRel {
-  int8_t ncols;
-  int8_t local;                 // 1: a relation of the stratum (shared memory), 0: external (global)
-  int8_t shared;                // external shared relation: one copy for all samples
-  int32_t dom[TILE_MAXCOL];
-  int32_t stride[TILE_MAXCOL];  // compact slot = Σ coord_c · stride_c
-  int32_t D;                    // slots per sample
-  int32_t fstride[TILE_MAXCOL][TILE_MAXCOL];  // fiber along c: id = Σ_{c' != c} coord_c' · fstride[c][c']
-  int32_t nfib[TILE_MAXCOL];    // fibers along column c (D / dom[c]); 0 = not needed
-  // external: global dense arrays per sample
-  const float* tag;                       // [samples][D] (null under unit)
-  const uint32_t* bits;                   // [samples][ceil(D/32)] presence
-  const unsigned long long* fib[TILE_MAXCOL];  // [samples][nfib[c]] presence words along column c
-  // local: shared-memory byte offsets (S, Δ, U)
-  int32_t sm_tag[3];
-  int32_t sm_bits[3];
-  int32_t sm_fib[2][TILE_MAXCOL];  // S, Δ fibers along column c (-1 unused)
-  // local: the final relation goes to the dense store of the packed layout
-  float* dfp;                   // slot tags (DENSE_ABSENT prefilled), non-unit
-  uint32_t* dfbits;             // unit: presence bitmap (zero prefilled)
-  uint8_t pshift[TILE_MAXCOL];
-  uint8_t psshift;
-};
-struct TileAtom {
-  int8_t rel;                   // index into TilePlan::rel
-  int8_t var[TILE_MAXCOL];      // variable id, or -1: constant coordinate cst
-  int32_t cst[TILE_MAXCOL];
-  int8_t level;                 // level whose variable closes the atom; -1: bound by the head
-  int8_t fcol;                  // column of that variable (fiber column)
-  int8_t chk;                   // level binding its other variables (< level; -1: the head): from then on its
-                                // fiber must be non-empty, so a value whose fiber is empty prunes the subtree
-};
-struct TileCmp {
-  int8_t va, vb;                // variable ids, -1: constant value
-  int32_t ca, cb;               // constant values (value space)
-  int8_t neq;
-  int8_t level;                 // -1: head variables / constants only
-};
-struct TileRule {
-  int8_t head;                  // TilePlan::rel index
-  int8_t hvar[TILE_MAXCOL];     // head args: variable id or -1 (constant coordinate hcst)
-  int32_t hcst[TILE_MAXCOL];
-  int8_t natoms;
-  TileAtom atom[MAXT];
-  int8_t nlev;
-  int8_t lev_var[TILE_MAXLEV];  // non-head variables, canonical order (first appearance)
-  int32_t vdom[TILE_MAXV];      // variable domain sizes
-  int32_t vmin[TILE_MAXV];      // class minimum (comparisons are made on values)
-  int8_t nvariant;              // 1 for a seed rule
-  int8_t ver[TILE_MAXVAR][MAXT];
-  int8_t seed;                  // all-external rule: round 1 only
-  int8_t ncmp;
-  TileCmp cmp[MAXC];
-};
-struct TilePlan {
-  int semi;
-  int nsamples;
-  int max_iters;
-  int nrel, nrule, nlocal;
-  int8_t local_rel[TILE_MAXREL];  // TilePlan::rel indexes of the stratum's relations
-  TileRel rel[TILE_MAXREL];
-  TileRule rule[TILE_MAXRULE];
-  int32_t smem_bytes;
-  int32_t clear_words;           // leading u32 words of shared memory zeroed per sample (bits + fibers)
-  uint32_t* trace;               // debug (LOBSTER_TILE_TRACE): per (sample, round < 64) candidates, |Δ'|
-};
+// ---- small dense per-sample strata (k_tile.cu; plan structs in tile_plan.h) ----
+static_assert(TILE_MAXT == MAXT && TILE_MAXC == MAXC, "tile_plan.h limits");
 // rounds_out[s]: rounds of sample s (the last one empty); cap_hit: max_iters reached
 // dplan: device scratch for the plan (sizeof(TilePlan), 16-B aligned)
 void launch_tile_fixpoint(const TilePlan& P, TilePlan* dplan, int* rounds_out, unsigned long long* ncand,
