@@ -154,9 +154,25 @@ static Tag oplus_state(int sr, const Tag& s, const Tag& b) {
 // ---------------------------------------------------------------------------
 // Parser for the Fig. 3c subset (own implementation; see DESIGN.md grammar)
 // ---------------------------------------------------------------------------
-struct Term { bool var = true; std::string name; int32_t val = 0; };
+// Integer expressions (§5.2: "Project expressions that contain
+// arithmetic or comparison of tuple elements"; reading "eval"):
+// int32 two's-complement +, -, * and unary -, / and % truncating toward zero;
+// a division or remainder by 0 (or INT32_MIN / -1) makes the candidate fail.
+struct Expr {
+  char op = '#';  // '#' constant, 'v' variable, '+', '-', '*', '/', '%', 'n' (negation)
+  std::string name;
+  int32_t val = 0;
+  std::vector<Expr> kids;
+};
+struct Term { bool var = true; std::string name; int32_t val = 0; std::shared_ptr<Expr> ex; };  // ex: head expression
 struct Atom { std::string rel; std::vector<Term> args; };
-struct Cons { Term a, b; bool neq = true; };
+enum RelOp { R_NE = 0, R_EQ = 1, R_LT = 2, R_LE = 3, R_GT = 4, R_GE = 5 };
+struct Cons { Expr a, b; int rel = R_NE; };
+
+static void expr_vars(const Expr& e, std::vector<std::string>& out) {
+  if (e.op == 'v') out.push_back(e.name);
+  for (auto& k : e.kids) expr_vars(k, out);
+}
 struct Rule {
   Atom head;
   std::vector<Atom> body;
@@ -184,14 +200,15 @@ static std::vector<Tok> lex(const std::string& t) {
       size_t j = i; while (j < t.size() && (std::isalnum((unsigned char)t[j]) || t[j] == '_')) j++;
       out.push_back({0, t.substr(i, j - i), l, cc}); adv(j - i); continue;
     }
-    if (std::isdigit((unsigned char)c) || (c == '-' && i + 1 < t.size() && std::isdigit((unsigned char)t[i + 1]))) {
+    if (std::isdigit((unsigned char)c)) {
       size_t j = i + 1; while (j < t.size() && std::isdigit((unsigned char)t[j])) j++;
       out.push_back({1, t.substr(i, j - i), l, cc}); adv(j - i); continue;
     }
-    if (t.compare(i, 2, ":-") == 0 || t.compare(i, 2, "!=") == 0 || t.compare(i, 2, "==") == 0) {
+    if (t.compare(i, 2, ":-") == 0 || t.compare(i, 2, "!=") == 0 || t.compare(i, 2, "==") == 0 ||
+        t.compare(i, 2, "<=") == 0 || t.compare(i, 2, ">=") == 0) {
       out.push_back({2, t.substr(i, 2), l, cc}); adv(2); continue;
     }
-    if (std::strchr("(),.:=", c)) { out.push_back({2, std::string(1, c), l, cc}); adv(1); continue; }
+    if (std::strchr("(),.:=<>+-*/%", c)) { out.push_back({2, std::string(1, c), l, cc}); adv(1); continue; }
     throw Err(E_PARSE, std::to_string(l) + ":" + std::to_string(cc) + ": unexpected character '" + std::string(1, c) + "'");
   }
   out.push_back({3, "", line, col});
@@ -219,8 +236,52 @@ struct Parser {
   std::string ident() { if (cur().kind != 0) fail("expected identifier"); return tk[p++].s; }
   Term term() {
     Term t;
-    if (cur().kind == 1) { t.var = false; t.val = (int32_t)std::stoll(tk[p++].s); return t; }
+    bool neg = false;
+    if (is("-") && tk[p + 1].kind == 1) { neg = true; p++; }
+    if (cur().kind == 1) {
+      long long v = std::stoll(tk[p++].s);
+      t.var = false; t.val = (int32_t)(neg ? -v : v); return t;
+    }
+    if (neg) fail("expected an integer after '-'");
     t.var = true; t.name = ident(); return t;
+  }
+  // expr := mul (('+'|'-') mul)* ; mul := un (('*'|'/'|'%') un)* ; un := '-' un | prim
+  // prim := integer | variable | '(' expr ')'
+  Expr prim() {
+    Expr e;
+    if (is("(")) { p++; e = expr(); expect(")"); return e; }
+    if (cur().kind == 1) { e.op = '#'; e.val = (int32_t)std::stoll(tk[p++].s); return e; }
+    e.op = 'v'; e.name = ident(); return e;
+  }
+  Expr un() {
+    if (is("-")) {
+      p++;
+      if (cur().kind == 1) { Expr e; e.op = '#'; e.val = (int32_t)(-std::stoll(tk[p++].s)); return e; }
+      Expr e; e.op = 'n'; e.kids.push_back(un()); return e;
+    }
+    return prim();
+  }
+  Expr mul() {
+    Expr e = un();
+    while (is("*") || is("/") || is("%")) { Expr b; b.op = cur().s[0]; p++; b.kids = {e, un()}; e = b; }
+    return e;
+  }
+  Expr expr() {
+    Expr e = mul();
+    while (is("+") || is("-")) { Expr b; b.op = cur().s[0]; p++; b.kids = {e, mul()}; e = b; }
+    return e;
+  }
+  Term head_term() {  // a bare variable / constant, or an expression
+    Expr e = expr();
+    Term t;
+    if (e.op == 'v') { t.var = true; t.name = e.name; return t; }
+    if (e.op == '#') { t.var = false; t.val = e.val; return t; }
+    t.var = false; t.ex = std::make_shared<Expr>(e); return t;
+  }
+  Atom head_atom(const std::string& name) {
+    Atom a; a.rel = name; expect("(");
+    if (!is(")")) { a.args.push_back(head_term()); while (is(",")) { p++; a.args.push_back(head_term()); } }
+    expect(")"); return a;
   }
   Atom atom(const std::string& name) {
     Atom a; a.rel = name; expect("(");
@@ -250,17 +311,35 @@ struct Parser {
     }
     return acc;
   }
+  // '(' opens a group of conjunctions, unless the token after its matching
+  // ')' continues an expression: then it starts a comparison, e.g. (x - y) % 3 == 0
+  bool paren_is_expr() const {
+    int depth = 0;
+    for (size_t q = p; q < tk.size(); ++q) {
+      if (tk[q].kind == 2 && tk[q].s == "(") depth++;
+      if (tk[q].kind == 2 && tk[q].s == ")" && --depth == 0) {
+        const Tok& n = tk[q + 1];
+        if (n.kind != 2) return false;
+        for (const char* o : {"+", "-", "*", "/", "%", "<", "<=", ">", ">=", "==", "!="})
+          if (n.s == o) return true;
+        return false;
+      }
+    }
+    return false;
+  }
   std::vector<Conj> unit() {
-    if (is("(")) { p++; auto r = disj(); expect(")"); return r; }
+    if (is("(") && !paren_is_expr()) { p++; auto r = disj(); expect(")"); return r; }
     if (cur().kind == 0 && tk[p + 1].kind == 2 && tk[p + 1].s == "(") {
       std::string n = ident(); Conj c; c.atoms.push_back(atom(n)); return {c};
     }
-    Term a = term();
-    bool neq;
-    if (is("!=")) neq = true; else if (is("==")) neq = false; else fail("expected atom or comparison");
+    Expr a = expr();
+    int rel;
+    if (is("!=")) rel = R_NE; else if (is("==")) rel = R_EQ; else if (is("<")) rel = R_LT;
+    else if (is("<=")) rel = R_LE; else if (is(">")) rel = R_GT; else if (is(">=")) rel = R_GE;
+    else fail("expected atom or comparison");
     p++;
-    Term b = term();
-    Conj c; c.cons.push_back({a, b, neq}); return {c};
+    Expr b = expr();
+    Conj c; c.cons.push_back({a, b, rel}); return {c};
   }
 };
 
@@ -302,7 +381,7 @@ static Program parse_program(const std::string& text) {
     if (ps.is("rel")) {
       ps.p++;
       std::string hn = ps.ident();
-      Atom head = ps.atom(hn);
+      Atom head = ps.head_atom(hn);
       ps.expect(":-");
       auto conjs = ps.disj();
       if (ps.is(".")) ps.p++;
@@ -336,9 +415,19 @@ static Program parse_program(const std::string& text) {
     // variables in order of first appearance in the body
     for (auto& a : r.body) for (auto& t : a.args)
       if (t.var && std::find(r.vars.begin(), r.vars.end(), t.name) == r.vars.end()) r.vars.push_back(t.name);
-    auto bound = [&](const Term& t) { return !t.var || std::find(r.vars.begin(), r.vars.end(), t.name) != r.vars.end(); };
-    for (auto& t : r.head.args) if (!bound(t)) throw Err(E_PARSE, "unbound head variable " + t.name + " in rule for " + r.head.rel);
-    for (auto& c : r.cons) if (!bound(c.a) || !bound(c.b)) throw Err(E_PARSE, "unbound variable in comparison in rule for " + r.head.rel);
+    auto known = [&](const std::string& n) { return std::find(r.vars.begin(), r.vars.end(), n) != r.vars.end(); };
+    auto bound = [&](const Term& t) { return !t.var || known(t.name); };
+    auto ebound = [&](const Expr& e) {
+      std::vector<std::string> vs;
+      expr_vars(e, vs);
+      for (auto& v : vs) if (!known(v)) return false;
+      return true;
+    };
+    for (auto& t : r.head.args) {
+      if (!bound(t)) throw Err(E_PARSE, "unbound head variable " + t.name + " in rule for " + r.head.rel);
+      if (t.ex && !ebound(*t.ex)) throw Err(E_PARSE, "unbound variable in a head expression of " + r.head.rel);
+    }
+    for (auto& c : r.cons) if (!ebound(c.a) || !ebound(c.b)) throw Err(E_PARSE, "unbound variable in comparison in rule for " + r.head.rel);
     for (size_t i = 0; i < r.vars.size(); ++i) {
       bool inhead = false;
       for (auto& t : r.head.args) if (t.var && t.name == r.vars[i]) inhead = true;
@@ -576,16 +665,39 @@ struct Engine {
     }
     std::function<void(size_t)> rec = [&](size_t k) {
       if (k == r.body.size()) {
+        std::function<bool(const Expr&, int32_t&)> ev = [&](const Expr& e, int32_t& out) -> bool {
+          if (e.op == '#') { out = e.val; return true; }
+          if (e.op == 'v') { out = val[vid(e.name)]; return true; }
+          int32_t x = 0, y = 0;
+          if (!ev(e.kids[0], x)) return false;
+          if (e.op == 'n') { out = (int32_t)(0u - (uint32_t)x); return true; }
+          if (!ev(e.kids[1], y)) return false;
+          switch (e.op) {
+            case '+': out = (int32_t)((uint32_t)x + (uint32_t)y); return true;
+            case '-': out = (int32_t)((uint32_t)x - (uint32_t)y); return true;
+            case '*': out = (int32_t)((uint32_t)x * (uint32_t)y); return true;
+            default:
+              if (y == 0 || (x == INT32_MIN && y == -1)) return false;  // the candidate fails
+              out = e.op == '/' ? x / y : x % y;
+              return true;
+          }
+        };
         for (auto& c : r.cons) {
-          int32_t a = c.a.var ? val[vid(c.a.name)] : c.a.val;
-          int32_t b = c.b.var ? val[vid(c.b.name)] : c.b.val;
-          if (c.neq ? (a == b) : (a != b)) return;
+          int32_t a = 0, b = 0;
+          if (!ev(c.a, a) || !ev(c.b, b)) return;
+          const bool ok = c.rel == R_NE ? a != b : c.rel == R_EQ ? a == b : c.rel == R_LT ? a < b
+                        : c.rel == R_LE ? a <= b : c.rel == R_GT ? a > b : a >= b;
+          if (!ok) return;
         }
         Candidate cd;
         cd.head.n = (int)r.head.args.size();
         for (size_t i = 0; i < r.head.args.size(); ++i) {
           const Term& t = r.head.args[i];
-          cd.head.v[i] = t.var ? val[vid(t.name)] : t.val;
+          if (t.ex) {
+            if (!ev(*t.ex, cd.head.v[i])) return;
+          } else {
+            cd.head.v[i] = t.var ? val[vid(t.name)] : t.val;
+          }
         }
         float t = tags[0];                                   // ⊗ left-deep in body order
         if (sr == DADD) cd.g = etag[0]->g;
