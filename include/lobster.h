@@ -47,7 +47,8 @@ typedef enum {
   LOBSTER_E_OOM = 6,         /* device allocation failed                                      */
   LOBSTER_E_ITER_CAP = 7,    /* max_iters rounds reached in a stratum (state readable)        */
   LOBSTER_E_CUDA = 8,        /* CUDA error; sticky: the context must be destroyed             */
-  LOBSTER_E_NCCL = 9         /* collective failure (reserved for the multi-GPU layer)         */
+  LOBSTER_E_NCCL = 9         /* NCCL missing or a collective failed (lobster_group_nccl, key-
+                                partitioned runs)                                             */
 } lobster_status;
 
 /* Provenance semirings (PAPER.md:445-456 Fig. 7b; :616-617 §3.5).
@@ -106,7 +107,8 @@ typedef struct {
                            local to the context (the distributed layer, dist.py, maps
                            them to global ids).  The fixpoint has no collective.       */
   int32_t world_size;   /* number of ranks sharing the batch (0 or 1 = unsharded)          */
-  void* nccl_comm;      /* reserved (collectives run above the ABI, on torch.distributed) */
+  void* nccl_comm;      /* unused: batch-sharded collectives run above the ABI (dist.py);
+                           key-partitioned runs take a lobster_group (below)            */
 } lobster_options;
 
 /* Create a context on options->device.  options may be NULL (device 0, default
@@ -124,9 +126,19 @@ const char* lobster_last_error(const lobster_ctx* ctx);
  *     rel endpoints_connected() :- is_endpoint(x), is_endpoint(y), path(x, y), x != y.
  *     output endpoints_connected                       -- gradients are produced for outputs
  * Bodies are conjunctions (',' or 'and') and disjunctions ('or', split into one
- * rule per disjunct, left to right) of atoms and comparisons `a != b`, `a == b`
- * between variables or integer constants.  Atom arguments are variables or
- * integer constants.  Every rule needs at least one batched body atom.
+ * rule per disjunct, left to right) of atoms and comparisons `e1 op e2`, op one
+ * of == != < <= > >=.  Atom arguments are variables or integer constants.
+ * Integer expressions (§5.2 "eval"): head arguments and
+ * comparison sides may be expressions over the rule's variables and
+ * constants with + - * / % and unary - (C precedence, parentheses), int32
+ * two's-complement; / and % truncate toward zero and a division by zero fails
+ * the derivation.  Comparisons between variables / constants run in every
+ * kernel; a rule with an arithmetic head or an arithmetic comparison must not
+ * be recursive (its body is evaluated into an internal relation __eval<k>,
+ * whose projection evaluates the expressions as bytecode), and the domain of a
+ * computed column is inferred by interval arithmetic (RANGE if a computed
+ * column feeds its own domain).  Every rule needs at least one batched body
+ * atom.
  * Stratification: SCCs of the predicate dependency graph in topological order
  * (PAPER.md:383-389).  Errors: PARSE ("line:col: msg"; unbound head variable,
  * unknown relation, arity mismatch); INVALID_ARG (bad semiring); STATE (called

@@ -47,6 +47,49 @@ __device__ __forceinline__ int64_t operand_value(const Operand& o, uint64_t a, u
   return (int64_t)((s >> o.shift) & bmask(o.bits)) + (int64_t)o.base;
 }
 
+// relation encoded as Cmp::neq: 0 ==, 1 !=, 2 <, 3 <=, 4 >, 5 >=
+__device__ __forceinline__ bool cmp_holds(int rel, int64_t a, int64_t b) {
+  switch (rel) {
+    case 0: return a == b;
+    case 1: return a != b;
+    case 2: return a < b;
+    case 3: return a <= b;
+    case 4: return a > b;
+    default: return a >= b;
+  }
+}
+
+// The eval stack machine (kernels.cuh Bc): false if the program fails
+// (division / remainder by zero, INT32_MIN / -1).  Fixed 8-entry stack.
+__device__ __forceinline__ bool bc_eval(const Bc& b, uint64_t key, int32_t& out) {
+  int32_t st[8];
+  int sp = 0;
+  for (int i = 0; i < b.n; ++i) {
+    const BcIns in = b.ins[i];
+    if (in.op == BC_FIELD) {
+      st[sp++] = (int32_t)((uint32_t)((key >> in.shift) & bmask(in.bits)) + (uint32_t)in.v);
+    } else if (in.op == BC_CONST) {
+      st[sp++] = in.v;
+    } else if (in.op == BC_NEG) {
+      st[sp - 1] = (int32_t)(0u - (uint32_t)st[sp - 1]);
+    } else {
+      const int32_t y = st[--sp], x = st[sp - 1];
+      int32_t r;
+      switch (in.op) {
+        case BC_ADD: r = (int32_t)((uint32_t)x + (uint32_t)y); break;
+        case BC_SUB: r = (int32_t)((uint32_t)x - (uint32_t)y); break;
+        case BC_MUL: r = (int32_t)((uint32_t)x * (uint32_t)y); break;
+        default:
+          if (y == 0 || (x == INT32_MIN && y == -1)) return false;
+          r = in.op == BC_DIV ? x / y : x % y;
+      }
+      st[sp - 1] = r;
+    }
+  }
+  out = st[0];
+  return true;
+}
+
 // first index in [0, n) with key[idx] >= x (n if none)
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ key, int64_t n, uint64_t x) {
   int64_t lo = 0, hi = n;

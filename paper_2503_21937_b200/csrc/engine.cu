@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -401,6 +402,13 @@ struct Ctx {
     // diff-add-mult-prob: the forward fixpoint is add-mult; gradients come from
     // the adjoint program (dadd_gradients)
     dadd = semiring == LOBSTER_DIFF_ADD_MULT_PROB;
+    if (dadd)
+      for (auto& R : prog.rules) {
+        bool arith = false;
+        for (auto& e : R.head_expr) arith |= e.op != 0;
+        for (auto& c : R.cmps) arith |= c.is_expr;
+        if (arith) throw Failure(LOBSTER_E_PARSE, "diff-add-mult-prob with arithmetic (eval) rules is not supported");
+      }
     semi = (omin || top1) ? S_MAXMULT : (dadd ? S_ADDMULT : semiring);
     program_text = text;
     for (auto& r : prog.rels)
@@ -602,7 +610,66 @@ struct Ctx {
         class_min[cl] = std::min(class_min[cl], prog.class_cmin[cl]);
         class_max[cl] = std::max(class_max[cl], prog.class_cmax[cl]);
       }
+    }
+    computed_domains();
+    for (int cl = 0; cl < prog.nclasses; ++cl)
       if (class_min[cl] > class_max[cl]) class_min[cl] = class_max[cl] = 0;
+  }
+
+  // Domains of computed head columns (arithmetic): interval
+  // arithmetic over the operand variables' domain classes, unioned into the
+  // column's class until nothing grows.  An expression over its own column's
+  // class (a value feeding its own domain) is refused.
+  void computed_domains() {
+    struct Iv { int64_t lo, hi; bool empty; };
+    auto clamp32 = [](Iv v) {
+      if (v.lo < INT32_MIN || v.hi > INT32_MAX) v.lo = INT32_MIN, v.hi = INT32_MAX;  // int32 wrap: anything
+      return v;
+    };
+    for (int iter = 0;; ++iter) {
+      bool grew = false;
+      for (const Rule& R : prog.rules)
+        for (size_t c = 0; c < R.head_expr.size(); ++c) {
+          if (!R.head_expr[c].op) continue;
+          const int tcl = prog.rels[R.head_rel].col_class[c];
+          std::function<Iv(const Expr&)> iv = [&](const Expr& e) -> Iv {
+            if (e.op == '#') return {e.cst, e.cst, false};
+            if (e.op == 'v') {
+              const int cl = R.var_class[e.var];
+              if (cl == tcl)
+                throw Failure(LOBSTER_E_RANGE, "a computed column of " + prog.rels[R.head_rel].name +
+                                                   " feeds its own domain (unsupported)");
+              return {class_min[cl], class_max[cl], class_min[cl] > class_max[cl]};
+            }
+            const Iv a = iv(e.kids[0]);
+            if (e.op == 'n') return clamp32({-a.hi, -a.lo, a.empty});
+            const Iv b = iv(e.kids[1]);
+            const bool em = a.empty || b.empty;
+            switch (e.op) {
+              case '+': return clamp32({a.lo + b.lo, a.hi + b.hi, em});
+              case '-': return clamp32({a.lo - b.hi, a.hi - b.lo, em});
+              case '*': {
+                const int64_t p[4] = {a.lo * b.lo, a.lo * b.hi, a.hi * b.lo, a.hi * b.hi};
+                return clamp32({*std::min_element(p, p + 4), *std::max_element(p, p + 4), em});
+              }
+              case '/': {  // |x / y| <= |x| for |y| >= 1
+                const int64_t m = std::max(std::llabs(a.lo), std::llabs(a.hi));
+                return clamp32({a.lo >= 0 ? 0 : -m, a.hi <= 0 ? 0 : m, em});
+              }
+              default: {  // % : |r| < |y|, |r| <= |x|, sign of x
+                const int64_t m = std::min(std::max(std::llabs(a.lo), std::llabs(a.hi)),
+                                           std::max(std::llabs(b.lo), std::llabs(b.hi)) - 1);
+                return {a.lo >= 0 ? 0 : -std::max<int64_t>(m, 0), a.hi <= 0 ? 0 : std::max<int64_t>(m, 0), em};
+              }
+            }
+          };
+          const Iv v = iv(R.head_expr[c]);
+          if (v.empty) continue;  // an operand class without values: the rule derives nothing
+          if (v.lo < class_min[tcl]) { class_min[tcl] = v.lo; grew = true; }
+          if (v.hi > class_max[tcl]) { class_max[tcl] = v.hi; grew = true; }
+        }
+      if (!grew) return;
+      if (iter >= 64) throw Failure(LOBSTER_E_RANGE, "domains of computed columns do not settle");
     }
   }
 
@@ -958,7 +1025,7 @@ struct Ctx {
           return Operand{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
         };
         if (lp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
-        lp.cmp[lp.ncmp++] = Cmp{op(R.cmps[i].a), op(R.cmps[i].b), (int8_t)R.cmps[i].neq};
+        lp.cmp[lp.ncmp++] = Cmp{op(R.cmps[i].a), op(R.cmps[i].b), R.cmps[i].rel};
       }
       head_moves(R, H, T, nullptr, lp.om, lp.nom, lp.cout);
       witness_moves(R, T, nullptr, lp.wm, lp.nwm, lp.wconst);
@@ -1001,14 +1068,33 @@ struct Ctx {
       for (auto& c : pending_start) pp.cmp[pp.ncmp++] = c;
       for (size_t i = 0; i < R.cmps.size(); ++i) {
         const Compare& cm = R.cmps[i];
+        if (cm.is_expr) continue;  // bytecode filters (below)
         auto op = [&](const Term& t) -> Operand {
           if (!t.is_var()) return Operand{2, 0, 0, t.cst};
           return Operand{0, (uint8_t)T.vshift[t.var], (uint8_t)T.vbits[t.var], class_base(R.var_class[t.var])};
         };
         if (pp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
-        pp.cmp[pp.ncmp++] = Cmp{op(cm.a), op(cm.b), (int8_t)cm.neq};
+        pp.cmp[pp.ncmp++] = Cmp{op(cm.a), op(cm.b), cm.rel};
       }
       head_moves(R, H, T, nullptr, pp.om, pp.nom, pp.cout);
+      // arithmetic (P:707-712 eval): head expressions and expression filters as bytecode
+      for (size_t c = 0; c < R.head_expr.size(); ++c) {
+        if (!R.head_expr[c].op) continue;
+        if (pp.nbh >= MAXBH) throw Failure(LOBSTER_E_PARSE, "too many computed head columns in one rule");
+        BcHead& b = pp.bh[pp.nbh++];
+        compile_expr(R, R.head_expr[c], T, b.e);
+        b.dshift = (uint8_t)H.L.shift[c];
+        b.bits = (uint8_t)H.L.bits[c];
+        b.base = H.L.mins[c];
+      }
+      for (const Compare& cm : R.cmps) {
+        if (!cm.is_expr) continue;
+        if (pp.nbf >= MAXBF) throw Failure(LOBSTER_E_PARSE, "too many expression comparisons in one rule");
+        BcFilter& f = pp.bf[pp.nbf++];
+        compile_expr(R, cm.ea, T, f.lhs);
+        compile_expr(R, cm.eb, T, f.rhs);
+        f.rel = cm.rel;
+      }
       pp.semi = semi;
       witness_moves(R, T, nullptr, pp.wm, pp.nwm, pp.wconst);
       if (H.direct) {
@@ -1106,7 +1192,7 @@ struct Ctx {
       for (size_t i = 0; i < R.cmps.size(); ++i) {
         if (cmp_done[i] || !avail(R.cmps[i].a) || !avail(R.cmps[i].b)) continue;
         if (jp.ncmp >= MAXC) throw Failure(LOBSTER_E_PARSE, "too many comparisons in one rule");
-        jp.cmp[jp.ncmp++] = Cmp{operand(R.cmps[i].a), operand(R.cmps[i].b), (int8_t)R.cmps[i].neq};
+        jp.cmp[jp.ncmp++] = Cmp{operand(R.cmps[i].a), operand(R.cmps[i].b), R.cmps[i].rel};
         cmp_done[i] = 1;
       }
       jp.semi = semi;
@@ -1251,6 +1337,33 @@ struct Ctx {
   }
 
   // head key moves (src 0 = probe table T, src 1 = build fields given by nshift)
+  // postfix bytecode of an expression over the probe key's variable fields
+  void compile_expr(const Rule& R, const Expr& e, const Table& T, Bc& out) {
+    out.n = 0;
+    std::function<void(const Expr&)> emit = [&](const Expr& x) {
+      if (out.n >= MAXBC) throw Failure(LOBSTER_E_PARSE, "expression too long (more than 16 operations)");
+      for (auto& k : x.kids) emit(k);
+      BcIns& i = out.ins[out.n++];
+      i = BcIns{};
+      switch (x.op) {
+        case '#': i.op = BC_CONST; i.v = x.cst; break;
+        case 'v':
+          i.op = BC_FIELD;
+          i.shift = (uint8_t)T.vshift[x.var];
+          i.bits = (uint8_t)T.vbits[x.var];
+          i.v = class_base(R.var_class[x.var]);
+          break;
+        case '+': i.op = BC_ADD; break;
+        case '-': i.op = BC_SUB; break;
+        case '*': i.op = BC_MUL; break;
+        case '/': i.op = BC_DIV; break;
+        case '%': i.op = BC_MOD; break;
+        default: i.op = BC_NEG; break;
+      }
+    };
+    emit(e);
+  }
+
   void head_moves(const Rule& R, RelState& H, const Table& T, const std::vector<int>* nshift, Move* om, int& nom,
                   uint64_t& cout, const std::vector<int>* nbits = nullptr) {
     const Layout& HL = H.L;
@@ -1259,6 +1372,7 @@ struct Ctx {
     if (HL.has_sample && HL.sbits) om[nom++] = Move{0, (uint8_t)T.sshift, (uint8_t)T.sbits, (uint8_t)HL.sshift};
     for (size_t c = 0; c < R.head.size(); ++c) {
       const Term& t = R.head[c];
+      if (c < R.head_expr.size() && R.head_expr[c].op) continue;  // computed by bytecode (project_k)
       if (!t.is_var()) {
         cout |= (uint64_t)((int64_t)t.cst - HL.mins[c]) << HL.shift[c];
         continue;
@@ -1746,7 +1860,7 @@ struct Ctx {
       mark("ingest");
       round_cap_hit = run_strata();
       for (size_t r = 0; r < prog.rels.size(); ++r)
-        if (!prog.rels[r].input) stats.tuples_derived += rels[r]->n;
+        if (!prog.rels[r].input && !prog.rels[r].internal) stats.tuples_derived += rels[r]->n;
       if (!round_cap_hit && (semi == S_MAXMULT || dadd)) {
         Phase ph(this, 4);
         HostTimer htg(host_ms[5]);
@@ -2440,6 +2554,10 @@ struct Ctx {
       if (P.nrule >= TILE_MAXRULE || (int)R.var_names.size() > TILE_MAXV || (int)R.nonhead.size() > TILE_MAXLEV ||
           (int)R.body.size() > MAXT || (int)R.cmps.size() > MAXC)
         return false;
+      for (auto& e : R.head_expr)
+        if (e.op) return false;  // arithmetic: the projection kernel's bytecode
+      for (auto& c : R.cmps)
+        if (c.is_expr) return false;
       TileRule& T = P.rule[P.nrule++];
       T.head = (int8_t)plan_rel(R.head_rel);
       std::vector<int> lev(R.var_names.size(), -1);
@@ -2514,7 +2632,7 @@ struct Ctx {
         t.vb = (int8_t)c.b.var;
         t.ca = c.a.cst;
         t.cb = c.b.cst;
-        t.neq = c.neq ? 1 : 0;
+        t.neq = c.rel;  // relational operator (program.hpp RelOp)
         t.level = (int8_t)std::max(c.a.is_var() ? lev[c.a.var] : -1, c.b.is_var() ? lev[c.b.var] : -1);
       }
     }
@@ -2813,8 +2931,10 @@ struct Ctx {
       if (xfer && !round_cap_hit)  // later strata read this stratum's relations whole
         for (int r : strat)
           if (read_later(r, si)) part_gather(*rels[r]);
-      stats.rounds_total += rounds;
-      stats.strata++;
+      if (!prog.rels[strat[0]].internal) {  // __eval<k> strata are an implementation detail
+        stats.rounds_total += rounds;
+        stats.strata++;
+      }
       if (round_cap_hit) break;
     }
     return round_cap_hit;
@@ -2948,6 +3068,7 @@ struct Ctx {
   // program is evaluated by a child context under add-mult on this stream:
   // the same kernels, no CPU path.  On finite derivation sets the adjoint sums
   // equal the dual-number derivative of the add-mult result.
+  static constexpr const char* kRelText[6] = {" == ", " != ", " < ", " <= ", " > ", " >= "};
   static std::string cols_decl(int n, const char* pfx) {
     std::string t;
     for (int c = 0; c < n; ++c) t += (c ? ", " : "") + std::string(pfx) + std::to_string(c) + ": i32";
@@ -3010,7 +3131,7 @@ struct Ctx {
             body += ", __fwd_" + prog.rels[R.body[i].rel].name + "(" + join_args(atom_args(R, R.body[i].args)) + ")";
         body += ", __dom_" + prog.rels[Bj.rel].name + "(" + join_args(bargs) + ")";
         for (const Compare& cp : R.cmps)
-          body += ", " + term_text(R, cp.a) + (cp.neq ? " != " : " == ") + term_text(R, cp.b);
+          body += ", " + term_text(R, cp.a) + kRelText[cp.rel] + term_text(R, cp.b);
         t += "rel __adj_" + prog.rels[Bj.rel].name + "(" + with_o(bargs) + ") :- " + body + ".\n";
       }
     }

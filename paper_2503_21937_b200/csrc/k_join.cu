@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) join_write_k(const JoinPlan jp, const int
     for (int c = 0; c < jp.ncmp; ++c) {
       const int64_t a = operand_value(jp.cmp[c].a, pk, bk);
       const int64_t b = operand_value(jp.cmp[c].b, pk, bk);
-      ok &= jp.cmp[c].neq ? (a != b) : (a == b);
+      ok &= cmp_holds(jp.cmp[c].neq, a, b);
     }
     okv[k] = ok;
     keyv[k] = jp.cout | apply_moves(jp.om, jp.nom, pk, bk);
@@ -266,9 +266,20 @@ __global__ void __launch_bounds__(256) project_k(const ProjectPlan pp) {
     for (int c = 0; c < pp.ncmp; ++c) {
       const int64_t a = operand_value(pp.cmp[c].a, k, 0);
       const int64_t b = operand_value(pp.cmp[c].b, k, 0);
-      ok &= pp.cmp[c].neq ? (a != b) : (a == b);
+      ok &= cmp_holds(pp.cmp[c].neq, a, b);
     }
-    const uint64_t hk = pp.cout | apply_moves(pp.om, pp.nom, k, 0);
+    uint64_t hk = pp.cout | apply_moves(pp.om, pp.nom, k, 0);
+    for (int f = 0; f < pp.nbf && ok; ++f) {  // expression comparisons (bytecode)
+      int32_t a, b;
+      ok = bc_eval(pp.bf[f].lhs, k, a) && bc_eval(pp.bf[f].rhs, k, b) && cmp_holds(pp.bf[f].rel, a, b);
+    }
+    for (int e = 0; e < pp.nbh && ok; ++e) {  // computed head columns (bytecode)
+      int32_t v;
+      ok = bc_eval(pp.bh[e].e, k, v);
+      const int64_t f = (int64_t)v - pp.bh[e].base;
+      ok = ok && f >= 0 && f < ((int64_t)1 << pp.bh[e].bits);
+      if (ok) hk |= (uint64_t)f << pp.bh[e].dshift;
+    }
     if (pp.direct) {
       if (ok) {
         const float t = (pp.semi != S_UNIT && pp.tag) ? pp.tag[i] : 1.0f;
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
       for (int c = 0; c < ncmp; ++c) {
         const int64_t a = operand_value(jp.cmp[c].a, pk, bk);
         const int64_t b = operand_value(jp.cmp[c].b, pk, bk);
-        ok &= jp.cmp[c].neq ? (a != b) : (a == b);
+        ok &= cmp_holds(jp.cmp[c].neq, a, b);
       }
       if (!ok) continue;
       const uint32_t slot = (uint32_t)(jp.cout | moves_n<NM>(jp.om, jp.nom, pk, bk));
@@ -642,7 +653,7 @@ __device__ __forceinline__ bool lookup_row(const LookupPlan& lp, int semi, PK pk
   for (int c = 0; c < lp.ncmp; ++c) {
     const int64_t a = operand_value(lp.cmp[c].a, pk, 0);
     const int64_t b = operand_value(lp.cmp[c].b, pk, 0);
-    ok &= lp.cmp[c].neq ? (a != b) : (a == b);
+    ok &= cmp_holds(lp.cmp[c].neq, a, b);
   }
   float tags[MAXL + 1];
   tags[0] = p0;

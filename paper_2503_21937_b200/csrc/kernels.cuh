@@ -52,7 +52,33 @@ struct Operand {
 };
 struct Cmp {
   Operand a, b;
-  int8_t neq;
+  int8_t neq;      // relation: 0 ==, 1 !=, 2 <, 3 <=, 4 >, 5 >= (program.hpp RelOp)
+};
+
+// Arithmetic (§5.2 eval): "compiled to bytecode for a simple stack
+// machine, and each GPU thread executes this bytecode program against one
+// fact with a small fixed-size stack".  Postfix programs over the probe key's
+// fields; int32 two's complement, / and % truncate; a division by zero (or
+// INT32_MIN / -1) fails the row.
+enum BcOp : int8_t { BC_FIELD = 0, BC_CONST = 1, BC_ADD, BC_SUB, BC_MUL, BC_DIV, BC_MOD, BC_NEG };
+constexpr int MAXBC = 16, MAXBH = 4, MAXBF = 2;
+struct BcIns {
+  int8_t op;
+  uint8_t shift, bits;  // BC_FIELD: value = (key >> shift & mask(bits)) + v
+  int32_t v;
+};
+struct Bc {
+  int n;
+  BcIns ins[MAXBC];
+};
+struct BcHead {        // computed head column: (value - base) << dshift, dead if outside [0, 2^bits)
+  Bc e;
+  uint8_t dshift, bits;
+  int32_t base;
+};
+struct BcFilter {
+  Bc lhs, rhs;
+  int8_t rel;
 };
 
 // A join step: probe rows (sorted packed keys) x a sorted build index whose key
@@ -148,6 +174,10 @@ struct ProjectPlan {
   uint32_t* dirty;
   int aggregate;
   MxEnc mx;
+  // arithmetic: computed head columns and expression filters (bytecode)
+  int nbh, nbf;
+  BcHead bh[MAXBH];
+  BcFilter bf[MAXBF];
 };
 
 // Lookup chain: probe rows whose variables cover the whole rule; every other

@@ -47,15 +47,16 @@ class Lexer {
       if (std::isalpha(c) || c == '_') {
         while (i < s_.size() && (std::isalnum((unsigned char)s_[i]) || s_[i] == '_')) step();
         toks.push_back({TK::Ident, s_.substr(st, i - st), L, C});
-      } else if (std::isdigit(c) || (c == '-' && i + 1 < s_.size() && std::isdigit((unsigned char)s_[i + 1]))) {
+      } else if (std::isdigit(c)) {
         step();
         while (i < s_.size() && std::isdigit((unsigned char)s_[i])) step();
         toks.push_back({TK::Int, s_.substr(st, i - st), L, C});
       } else if (i + 1 < s_.size() && (s_.compare(i, 2, ":-") == 0 || s_.compare(i, 2, "!=") == 0 ||
-                                       s_.compare(i, 2, "==") == 0)) {
+                                       s_.compare(i, 2, "==") == 0 || s_.compare(i, 2, "<=") == 0 ||
+                                       s_.compare(i, 2, ">=") == 0)) {
         step(); step();
         toks.push_back({TK::Sym, s_.substr(st, 2), L, C});
-      } else if (std::strchr("(),.:=", c) && c) {
+      } else if (std::strchr("(),.:=<>+-*/%", c) && c) {
         step();
         toks.push_back({TK::Sym, s_.substr(st, 1), L, C});
       } else {
@@ -68,9 +69,15 @@ class Lexer {
 };
 
 // Surface forms before variable numbering.
-struct STerm { bool var; std::string name; int32_t val; };
+struct SExpr {
+  char op = '#';  // '#' constant, 'v' variable, '+', '-', '*', '/', '%', 'n'
+  std::string name;
+  int32_t val = 0;
+  std::vector<SExpr> kids;
+};
+struct STerm { bool var; std::string name; int32_t val; bool is_expr = false; SExpr ex; };
 struct SAtom { std::string rel; std::vector<STerm> args; int line, col; };
-struct SCmp { STerm a, b; bool neq; };
+struct SCmp { SExpr a, b; int8_t rel; };
 struct SConj { std::vector<SAtom> atoms; std::vector<SCmp> cmps; };
 struct SRule { SAtom head; SConj body; };
 
@@ -127,13 +134,115 @@ class Parser {
     if (peek().k != TK::Ident) error("expected identifier");
     return t_[p_++].text;
   }
+  int32_t integer(bool neg) {
+    long long v = std::stoll(t_[p_++].text);
+    if (neg) v = -v;
+    if (v < INT32_MIN || v > INT32_MAX) error("integer constant out of int32 range");
+    return (int32_t)v;
+  }
   STerm term() {
-    if (peek().k == TK::Int) {
-      long long v = std::stoll(t_[p_++].text);
-      if (v < INT32_MIN || v > INT32_MAX) error("integer constant out of int32 range");
-      return {false, "", (int32_t)v};
+    if (sym("-") && peek(1).k == TK::Int) {
+      ++p_;
+      return {false, "", integer(true)};
     }
+    if (peek().k == TK::Int) return {false, "", integer(false)};
     return {true, ident(), 0};
+  }
+  // expr := mul (('+'|'-') mul)* ; mul := un (('*'|'/'|'%') un)* ; un := '-' un | prim ;
+  // prim := integer | variable | '(' expr ')'
+  SExpr prim() {
+    SExpr e;
+    if (sym("(")) {
+      ++p_;
+      e = expr();
+      need(")");
+      return e;
+    }
+    if (peek().k == TK::Int) {
+      e.val = integer(false);
+      return e;
+    }
+    e.op = 'v';
+    e.name = ident();
+    return e;
+  }
+  SExpr unary() {
+    if (sym("-")) {
+      ++p_;
+      if (peek().k == TK::Int) {
+        SExpr e;
+        e.val = integer(true);
+        return e;
+      }
+      SExpr e;
+      e.op = 'n';
+      e.kids.push_back(unary());
+      return e;
+    }
+    return prim();
+  }
+  SExpr mul() {
+    SExpr e = unary();
+    while (sym("*") || sym("/") || sym("%")) {
+      SExpr b;
+      b.op = peek().text[0];
+      ++p_;
+      b.kids = {e, unary()};
+      e = b;
+    }
+    return e;
+  }
+  SExpr expr() {
+    SExpr e = mul();
+    while (sym("+") || sym("-")) {
+      SExpr b;
+      b.op = peek().text[0];
+      ++p_;
+      b.kids = {e, mul()};
+      e = b;
+    }
+    return e;
+  }
+  STerm head_term() {
+    SExpr e = expr();
+    if (e.op == 'v') return {true, e.name, 0};
+    if (e.op == '#') return {false, "", e.val};
+    STerm t{false, "", 0};
+    t.is_expr = true;
+    t.ex = e;
+    return t;
+  }
+  SAtom head_atom() {
+    SAtom a;
+    a.line = peek().line;
+    a.col = peek().col;
+    a.rel = ident();
+    need("(");
+    if (!sym(")")) {
+      for (;;) {
+        a.args.push_back(head_term());
+        if (sym(",")) { ++p_; continue; }
+        break;
+      }
+    }
+    need(")");
+    return a;
+  }
+  // '(' opens a group, unless the token after its matching ')' continues an
+  // expression: then it starts a comparison such as (x - y) % 3 == 0
+  bool paren_is_expr() const {
+    int depth = 0;
+    for (size_t q = p_; q < t_.size(); ++q) {
+      if (t_[q].k == TK::Sym && t_[q].text == "(") ++depth;
+      if (t_[q].k == TK::Sym && t_[q].text == ")" && --depth == 0) {
+        const Token& n = t_[std::min(q + 1, t_.size() - 1)];
+        if (n.k != TK::Sym) return false;
+        for (const char* o : {"+", "-", "*", "/", "%", "<", "<=", ">", ">=", "==", "!="})
+          if (n.text == o) return true;
+        return false;
+      }
+    }
+    return false;
   }
   SAtom atom() {
     SAtom a;
@@ -169,7 +278,7 @@ class Parser {
     decls.push_back({name, {arity, shared}});
   }
   void rule() {
-    SAtom head = atom();
+    SAtom head = head_atom();
     need(":-");
     std::vector<SConj> dnf = disjunction();
     if (sym(".")) ++p_;
@@ -203,9 +312,9 @@ class Parser {
     }
     return acc;
   }
-  // factor := '(' disjunction ')' | atom | term ('!=' | '==') term
+  // factor := '(' disjunction ')' | atom | expr relop expr
   std::vector<SConj> factor() {
-    if (sym("(")) {
+    if (sym("(") && !paren_is_expr()) {
       ++p_;
       std::vector<SConj> d = disjunction();
       need(")");
@@ -216,15 +325,19 @@ class Parser {
       c.atoms.push_back(atom());
       return {c};
     }
-    STerm a = term();
-    bool neq;
-    if (sym("!=")) neq = true;
-    else if (sym("==")) neq = false;
+    SExpr a = expr();
+    int8_t rel;
+    if (sym("!=")) rel = REL_NE;
+    else if (sym("==")) rel = REL_EQ;
+    else if (sym("<")) rel = REL_LT;
+    else if (sym("<=")) rel = REL_LE;
+    else if (sym(">")) rel = REL_GT;
+    else if (sym(">=")) rel = REL_GE;
     else error("expected an atom or a comparison");
     ++p_;
-    STerm b = term();
+    SExpr b = expr();
     SConj c;
-    c.cmps.push_back({a, b, neq});
+    c.cmps.push_back({a, b, rel});
     return {c};
   }
 };
@@ -242,9 +355,89 @@ struct UnionFind {
 
 }  // namespace
 
+// Rules with arithmetic (P:707-712 eval) are split in two: the body is
+// evaluated into __eval<k>(its variables, first-appearance order) with the
+// plain comparisons, and the head expressions / expression comparisons become
+// a single-atom rule over it — the projection kernel evaluates them by
+// bytecode.  Non-recursive rules only (a recursive one would change the round
+// structure; its computed column could also feed its own domain).
+static bool leaf(const SExpr& e) { return e.op == '#' || e.op == 'v'; }
+static void rewrite_arith(std::vector<SRule>& rules) {
+  // SCCs over rule heads (by name)
+  std::map<std::string, int> id;
+  for (auto& r : rules) id.emplace(r.head.rel, (int)id.size());
+  const int n = (int)id.size();
+  std::vector<std::vector<int>> g(n);
+  for (auto& r : rules)
+    for (auto& a : r.body.atoms) {
+      auto it = id.find(a.rel);
+      if (it != id.end()) g[id[r.head.rel]].push_back(it->second);
+    }
+  std::vector<int> idx(n, -1), low(n, 0), comp(n, -1), stk;
+  std::vector<char> on(n, 0);
+  int cnt = 0, nc = 0;
+  std::function<void(int)> dfs = [&](int v) {
+    idx[v] = low[v] = cnt++;
+    stk.push_back(v);
+    on[v] = 1;
+    for (int w : g[v]) {
+      if (idx[w] < 0) { dfs(w); low[v] = std::min(low[v], low[w]); }
+      else if (on[w]) low[v] = std::min(low[v], idx[w]);
+    }
+    if (low[v] == idx[v]) {
+      for (;;) {
+        int w = stk.back();
+        stk.pop_back();
+        on[w] = 0;
+        comp[w] = nc;
+        if (w == v) break;
+      }
+      ++nc;
+    }
+  };
+  for (int v = 0; v < n; ++v)
+    if (idx[v] < 0) dfs(v);
+  std::vector<SRule> out;
+  int k = 0;
+  for (auto& r : rules) {
+    bool arith = false;
+    for (auto& t : r.head.args) arith |= t.is_expr;
+    for (auto& c : r.body.cmps) arith |= !leaf(c.a) || !leaf(c.b);
+    if (!arith) {
+      out.push_back(r);
+      continue;
+    }
+    for (auto& a : r.body.atoms) {
+      auto it = id.find(a.rel);
+      if (it != id.end() && comp[it->second] == comp[id[r.head.rel]])
+        fail_at(r.head, "arithmetic in a recursive rule for " + r.head.rel + " is not supported");
+    }
+    SAtom ev;
+    ev.rel = "__eval" + std::to_string(k++);
+    ev.line = r.head.line;
+    ev.col = r.head.col;
+    std::set<std::string> seen;
+    for (auto& a : r.body.atoms)
+      for (auto& t : a.args)
+        if (t.var && seen.insert(t.name).second) ev.args.push_back({true, t.name, 0});
+    if (ev.args.size() > 8) fail_at(r.head, "a rule with arithmetic binds more than 8 variables");
+    SRule body_rule;
+    body_rule.head = ev;
+    body_rule.body.atoms = r.body.atoms;
+    SRule proj;
+    proj.head = r.head;
+    proj.body.atoms = {ev};
+    for (auto& c : r.body.cmps) (leaf(c.a) && leaf(c.b) ? body_rule : proj).body.cmps.push_back(c);
+    out.push_back(body_rule);
+    out.push_back(proj);
+  }
+  rules.swap(out);
+}
+
 Program parse_program(const std::string& text) {
   Parser ps(text);
   ps.parse();
+  rewrite_arith(ps.rules);
   Program P;
   auto add_rel = [&](const std::string& name, int arity) -> int {
     auto it = P.rel_id.find(name);
@@ -329,9 +522,24 @@ Program parse_program(const std::string& text) {
       R.body.push_back(a);
     }
     if (!any_batched) fail_at(sr.head, "rule for " + sr.head.rel + " needs at least one batched (non-shared) body atom");
+    std::function<Expr(const SExpr&)> conv = [&](const SExpr& e) -> Expr {
+      Expr x;
+      x.op = e.op;
+      x.cst = e.val;
+      if (e.op == 'v') {
+        auto it = vid.find(e.name);
+        if (it == vid.end()) fail_at(sr.head, "unbound variable " + e.name + " in an expression");
+        x.var = it->second;
+      }
+      for (auto& k : e.kids) x.kids.push_back(conv(k));
+      return x;
+    };
+    R.head_expr.assign(sr.head.args.size(), Expr{});
     for (size_t c = 0; c < sr.head.args.size(); ++c) {
       Term t;
-      if (sr.head.args[c].var) {
+      if (sr.head.args[c].is_expr) {
+        R.head_expr[c] = conv(sr.head.args[c].ex);  // computed column: its own domain class
+      } else if (sr.head.args[c].var) {
         auto it = vid.find(sr.head.args[c].name);
         if (it == vid.end()) fail_at(sr.head, "unbound head variable " + sr.head.args[c].name);
         t.var = it->second;
@@ -343,18 +551,25 @@ Program parse_program(const std::string& text) {
     }
     for (auto& sc : sr.body.cmps) {
       Compare cm;
-      cm.neq = sc.neq;
-      for (int side = 0; side < 2; ++side) {
-        const STerm& st = side ? sc.b : sc.a;
-        Term t;
-        if (st.var) {
-          auto it = vid.find(st.name);
-          if (it == vid.end()) fail_at(sr.head, "unbound variable " + st.name + " in comparison");
-          t.var = it->second;
-        } else {
-          t.cst = st.val;
+      cm.rel = sc.rel;
+      cm.neq = sc.rel == REL_NE;
+      if (leaf(sc.a) && leaf(sc.b)) {
+        for (int side = 0; side < 2; ++side) {
+          const SExpr& st = side ? sc.b : sc.a;
+          Term t;
+          if (st.op == 'v') {
+            auto it = vid.find(st.name);
+            if (it == vid.end()) fail_at(sr.head, "unbound variable " + st.name + " in comparison");
+            t.var = it->second;
+          } else {
+            t.cst = st.val;
+          }
+          (side ? cm.b : cm.a) = t;
         }
-        (side ? cm.b : cm.a) = t;
+      } else {
+        cm.is_expr = true;
+        cm.ea = conv(sc.a);
+        cm.eb = conv(sc.b);
       }
       R.cmps.push_back(cm);
     }
@@ -398,8 +613,9 @@ Program parse_program(const std::string& text) {
       for (size_t c = 0; c < a.args.size(); ++c)
         if (!a.args[c].is_var()) note_const(P.rels[a.rel].col_class[c], a.args[c].cst);
     for (size_t c = 0; c < R.head.size(); ++c)
-      if (!R.head[c].is_var()) note_const(P.rels[R.head_rel].col_class[c], R.head[c].cst);
+      if (!R.head[c].is_var() && !R.head_expr[c].op) note_const(P.rels[R.head_rel].col_class[c], R.head[c].cst);
   }
+  for (auto& r : P.rels) r.internal = r.name.compare(0, 6, "__eval") == 0;
 
   // Stratification: Tarjan SCC over IDB relations, edges head -> body IDB.
   const int nr = (int)P.rels.size();

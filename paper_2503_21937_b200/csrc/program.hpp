@@ -30,9 +30,25 @@ struct BodyAtom {
   std::vector<Term> args;
 };
 
+// Integer expression (§5.2 eval): int32 two's-complement + - * and
+// unary -, / and % truncating toward zero; / or % by zero (or INT32_MIN / -1)
+// fails the candidate.
+struct Expr {
+  char op = 0;       // 0 none, '#' constant, 'v' variable, '+', '-', '*', '/', '%', 'n' (negation)
+  int var = -1;
+  int32_t cst = 0;
+  std::vector<Expr> kids;
+};
+
+// Relational operators of comparisons (the encoding of kernels.cuh Cmp::neq).
+enum RelOp : int8_t { REL_EQ = 0, REL_NE = 1, REL_LT = 2, REL_LE = 3, REL_GT = 4, REL_GE = 5 };
+
 struct Compare {
-  Term a, b;
-  bool neq = true;  // true: a != b, false: a == b
+  Term a, b;          // operands when both sides are a variable or a constant
+  bool neq = true;    // rel == REL_NE (kept for the equality-only planners)
+  int8_t rel = REL_NE;
+  bool is_expr = false;  // a side is an arithmetic expression: ea / eb (single-atom rules only)
+  Expr ea, eb;
 };
 
 struct Rule {
@@ -42,7 +58,9 @@ struct Rule {
   std::vector<Compare> cmps;
   std::vector<std::string> var_names;  // var id -> name; ids in order of first appearance in the body
   std::vector<int> var_class;          // var id -> domain class
-  std::vector<int> nonhead;            // non-head var ids, order of first appearance (witness order)
+  std::vector<int> nonhead;            // non-head var ids, order of first appearance (witness order);
+                                       // variables used only inside head expressions are non-head
+  std::vector<Expr> head_expr;         // per head column: op != 0 -> computed by this expression
   int global_index = 0;                // position in program order (after `or` splitting)
   int local_index = 0;                 // position among rules with the same head
 };
@@ -53,6 +71,7 @@ struct Relation {
   bool shared = false;   // no sample column (SURVEY §8(c) point 12)
   bool input = false;    // EDB: declared with `type`
   bool output = false;   // gradients are produced for it
+  bool internal = false;  // __eval<k>: body of a rule with expressions (not counted in stats)
   int stratum = -1;      // IDB only
   std::vector<int> col_class;  // per column domain class
   int nrules = 0;        // IDB: rules with this head

@@ -115,8 +115,11 @@ __device__ __forceinline__ bool cmps_ok(const TileRule& R, int level, unsigned l
   for (int i = 0; i < R.ncmp; ++i) {
     const TileCmp& c = R.cmp[i];
     if (c.level != level) continue;
-    const bool eq = cmp_value(c.va, c.ca, R, vals) == cmp_value(c.vb, c.cb, R, vals);
-    if (c.neq ? eq : !eq) return false;
+    const int32_t a = cmp_value(c.va, c.ca, R, vals), b = cmp_value(c.vb, c.cb, R, vals);
+    // c.neq: relation 0 ==, 1 !=, 2 <, 3 <=, 4 >, 5 >=
+    const bool ok = c.neq == 0 ? a == b : c.neq == 1 ? a != b : c.neq == 2 ? a < b : c.neq == 3 ? a <= b
+                  : c.neq == 4 ? a > b : a >= b;
+    if (!ok) return false;
   }
   return true;
 }

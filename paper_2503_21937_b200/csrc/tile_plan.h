@@ -55,7 +55,7 @@ struct TileAtom {
 struct TileCmp {
   int8_t va, vb;                // variable ids, -1: constant value
   int32_t ca, cb;               // constant values (value space)
-  int8_t neq;
+  int8_t neq;                   // relation: 0 ==, 1 !=, 2 <, 3 <=, 4 >, 5 >=
   int8_t level;                 // -1: head variables / constants only
 };
 struct TileRule {
