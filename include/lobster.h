@@ -108,7 +108,7 @@ typedef struct {
                            them to global ids).  The fixpoint has no collective.       */
   int32_t world_size;   /* number of ranks sharing the batch (0 or 1 = unsharded)          */
   void* nccl_comm;      /* unused: batch-sharded collectives run above the ABI (dist.py);
-                           key-partitioned runs take a lobster_group (below)            */
+                           key-partitioned runs use lobster_partition                       */
 } lobster_options;
 
 /* Create a context on options->device.  options may be NULL (device 0, default
