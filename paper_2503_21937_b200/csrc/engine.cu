@@ -349,6 +349,7 @@ struct Ctx {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (hbuf) cudaFreeHost(hbuf);
     if (hx) cudaFreeHost(hx);
+    if (hplan) cudaFreeHost(hplan);
     if (hring) cudaFreeHost(hring);
   }
 
@@ -1500,7 +1501,7 @@ struct Ctx {
   }
 
   // dense F -> sorted list (key, p, w) for later strata, outputs and the walk
-  void dense_to_sorted(RelState& S) {
+  void dense_to_sorted(RelState& S, int64_t known_n = -1) {
     const int64_t ns = S.nslots;
     uint32_t* fl = arena.get<uint32_t>(ns);
     uint32_t* pos = arena.get<uint32_t>(ns);
@@ -1509,7 +1510,7 @@ struct Ctx {
     else launch_dense_present(S.dfp.ptr(), S.dfbits.ptr(), ns, semi, fl, st);
     exclusive_scan<uint32_t>(fl, pos, ns, tot, arena.alloc(scan_tmp_bytes<uint32_t>(ns)), st);
     kcheck("dense present");
-    const int64_t n = read_dev(tot);
+    const int64_t n = known_n >= 0 ? known_n : (int64_t)read_dev(tot);  // (the tile kernel counts its tuples)
     S.key.reserve(n);
     if (semi != S_UNIT) S.p.reserve(n);
     if (semi == S_MAXMULT) S.w.reserve(n);
@@ -1871,9 +1872,14 @@ struct Ctx {
     }
     batch_cur = B;
     if (micro) finalize_collected();
-    stats.fj_timed_candidates = (int64_t)read_dev(d_ncand + 2);
-    stats.fj_candidates = (int64_t)read_dev(d_ncand + 1) + stats.fj_timed_candidates;
-    stats.candidates += (int64_t)read_dev(d_ncand) + stats.fj_candidates;
+    {  // the three device counters in one read
+      cuda_check(cudaMemcpyAsync(hbuf, d_ncand, 24, cudaMemcpyDeviceToHost, st), "D2H");
+      sync();
+      const unsigned long long* c = reinterpret_cast<const unsigned long long*>(hbuf);
+      stats.fj_timed_candidates = (int64_t)c[2];
+      stats.fj_candidates = (int64_t)c[1] + stats.fj_timed_candidates;
+      stats.candidates += (int64_t)c[0] + stats.fj_candidates;
+    }
     stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
     finish_run(t0, round_cap_hit, out);
   }
@@ -2508,6 +2514,7 @@ struct Ctx {
   // stratum's S / Δ / U arrays plus fibers fit one CTA's shared memory.
   bool no_tile = getenv("LOBSTER_NO_TILE") != nullptr;  // A/B: the per-round path
   int64_t tile_max_slots = getenv("LOBSTER_TILE") ? INT64_MAX : 65536;
+  TilePlan* hplan = nullptr;  // pinned
   int64_t class_dom(int cl) const { return class_max[cl] - class_min[cl] + 1; }
 
   bool tile_plan(const std::vector<int>& strat, TilePlan& P, std::vector<int>& prel) {
@@ -2745,8 +2752,10 @@ struct Ctx {
       launch_tile_scatter(sc, st);
       stats.bytes_algorithmic += S.n * (8 + (semi == S_UNIT ? 0 : 4));
     }
-    int* d = arena.get<int>(B + 2);  // [max rounds, cap hit, rounds per sample...]
-    cuda_check(cudaMemsetAsync(d, 0, 8, st), "memset");
+    // [max rounds, cap hit, tuples of each local relation (u64), rounds per sample...]
+    int* d = arena.get<int>(B + 2 + 2 * TILE_MAXREL);
+    cuda_check(cudaMemsetAsync(d, 0, 8 + 8 * TILE_MAXREL, st), "memset");
+    P.counts = reinterpret_cast<unsigned long long*>(d + 2);
     std::vector<uint32_t> htr;
     if (getenv("LOBSTER_TILE_TRACE")) {  // debug: per (sample, round) candidates and |Δ'|
       P.trace = arena.get<uint32_t>((int64_t)B * 128);
@@ -2754,7 +2763,10 @@ struct Ctx {
     }
     {
       Phase ph(this, 0);
-      launch_tile_fixpoint(P, reinterpret_cast<TilePlan*>(arena.alloc(sizeof(TilePlan))), d + 2, d_ncand, d + 1, st);
+      if (!hplan) cuda_check(cudaMallocHost(&hplan, sizeof(TilePlan)), "cudaMallocHost");
+      *hplan = P;  // pinned staging: the plan's H2D copy stays asynchronous (the previous one completed at its sync)
+      launch_tile_fixpoint(*hplan, reinterpret_cast<TilePlan*>(arena.alloc(sizeof(TilePlan))),
+                           d + 2 + 2 * TILE_MAXREL, d_ncand, d + 1, st);
       kcheck("tile fixpoint");
     }
     if (P.trace) {
@@ -2768,10 +2780,14 @@ struct Ctx {
         fprintf(stderr, "\n");
       }
     }
-    launch_max_i32(d + 2, B, d, st);
-    const int64_t both = read_dev(reinterpret_cast<const int64_t*>(d));
-    cap = (both >> 32) != 0;
-    return (int)(both & 0xffffffff);
+    launch_max_i32(d + 2 + 2 * TILE_MAXREL, B, d, st);
+    cuda_check(cudaMemcpyAsync(hbuf, d, 8 + 8 * TILE_MAXREL, cudaMemcpyDeviceToHost, st), "D2H");
+    sync();
+    const int* h = reinterpret_cast<const int*>(hbuf);
+    cap = h[1] != 0;
+    for (int li = 0; li < P.nlocal; ++li)  // exact tuple counts: compaction needs no second read
+      rels[prel[P.local_rel[li]]]->n = (int64_t)reinterpret_cast<const unsigned long long*>(h + 2)[li];
+    return h[0];
   }
 
   int64_t run_strata() {
@@ -2924,7 +2940,7 @@ struct Ctx {
           S.n = (int64_t)read_dev(c);
           S.lazy = true;
         } else {
-          dense_to_sorted(S);
+          dense_to_sorted(S, tiled ? S.n : -1);
         }
       }
       mark("dense->sorted");

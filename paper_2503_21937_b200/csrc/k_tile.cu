@@ -29,6 +29,8 @@
 // per-sample arrays built once per stratum by tile_scatter_k.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "devmem.hpp"
 #include "device_util.cuh"
@@ -97,15 +99,31 @@ void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, un
                    cudaStream_t st) {
   static int configured_bytes = -1;  // per template: opt in to > 48 KB of dynamic shared memory once
   if (configured_bytes < P.smem_bytes) {
-    const int dyn = 227 * 1024 - (int)sizeof(TilePlan);  // static plan copy + dynamic relations <= 227 KB
+    const int dyn = 227 * 1024 - (int)((sizeof(TilePlan) + 255) & ~size_t(255));  // static plan copy + dynamic <= 227 KB
     cuda_check(cudaFuncSetAttribute(tile_fixpoint_k<SEMI>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn),
                "tile smem attribute");
     configured_bytes = dyn;
   }
-  int per_sm = 1, dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_fixpoint_k<SEMI>, TILE_THREADS, P.smem_bytes);
+  // occupancy per shared-memory size, SM count: host queries cached (microseconds each)
+  static std::mutex mu;
+  static std::map<int, int> occ;
+  static int sms = 0;
+  int per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto it = occ.find(P.smem_bytes);
+    if (it == occ.end()) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_fixpoint_k<SEMI>, TILE_THREADS, P.smem_bytes);
+      occ[P.smem_bytes] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
   int threads = TILE_THREADS;
   if (const char* e = getenv("LOBSTER_TILE_THREADS")) threads = std::max(32, std::min(TILE_THREADS, atoi(e)));
   int grid = std::max(1, std::min(P.nsamples, std::max(1, per_sm) * sms));
@@ -118,6 +136,7 @@ void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, un
 void launch_tile_fixpoint(const TilePlan& P, TilePlan* dplan, int* rounds_out, unsigned long long* ncand,
                           int* cap_hit, cudaStream_t st) {
   if (P.nsamples <= 0) return;
+  // P should live in pinned host memory (the engine's staging copy): an async copy
   cuda_check(cudaMemcpyAsync(dplan, &P, sizeof(TilePlan), cudaMemcpyHostToDevice, st), "tile plan");
   note_launch();
   switch (P.semi) {

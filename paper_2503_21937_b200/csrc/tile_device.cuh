@@ -379,8 +379,10 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
       const uint32_t* Sb = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[0]);
       const uint32_t* Db = reinterpret_cast<const uint32_t*>(sm + H.sm_bits[1]);
       const float* St = reinterpret_cast<const float*>(sm + H.sm_tag[0]);
+      uint32_t cnt = 0;
       for (int h = threadIdx.x; h < H.D; h += blockDim.x) {
         if (!tbit(Sb, h)) continue;  // Δ' was empty: S holds every tuple
+        ++cnt;
         (void)Db;
         uint64_t pk = (uint64_t)s << H.psshift;
         int x = h;
@@ -391,6 +393,8 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
         if constexpr (SEMI == TILE_S_UNIT) atomicOr(HQ.dfbits + (pk >> 5), 1u << (pk & 31u));
         else HQ.dfp[pk] = St[h];
       }
+      cnt = __reduce_add_sync(~0u, cnt);
+      if (lane == 0 && cnt) atomicAdd(Q.counts + li, (unsigned long long)cnt);
     }
     __syncthreads();
   }

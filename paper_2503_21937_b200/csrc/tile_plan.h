@@ -85,6 +85,7 @@ struct TilePlan {
   int32_t smem_bytes;
   int32_t clear_words;           // leading u32 words of shared memory zeroed per sample (bits + fibers)
   uint32_t* trace;               // debug (LOBSTER_TILE_TRACE): per (sample, round < 64) candidates, |Δ'|
+  unsigned long long* counts;    // per local relation (local_rel order): tuples at the fixpoint
 };
 
 }  // namespace lob
