@@ -47,6 +47,26 @@ __device__ __forceinline__ int64_t operand_value(const Operand& o, uint64_t a, u
   return (int64_t)((s >> o.shift) & bmask(o.bits)) + (int64_t)o.base;
 }
 
+// Stale reads of slot words that other threads of the same launch update with
+// atomics: relaxed loads at GPU scope, so the read and the atomics are morally
+// strong and the race is defined behaviour (PTX memory model).  The value is
+// any version of the word between the launch start and now — a lower bound of
+// the final value, which is all the fused ⊕ needs (kernels.cuh Direct).
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+#ifndef PEEK_SLOT
+#define PEEK_SLOT ld_relaxed  // A/B: -DPEEK_SLOT=__ldca (plain L1 read, formally racy)
+#endif
+
 // relation encoded as Cmp::neq: 0 ==, 1 !=, 2 <, 3 <=, 4 >, 5 >=
 __device__ __forceinline__ bool cmp_holds(int rel, int64_t a, int64_t b) {
   switch (rel) {
@@ -188,9 +208,9 @@ __device__ __forceinline__ unsigned long long direct_pack(int semi, uint32_t slo
 __device__ __forceinline__ unsigned long long direct_peek(int semi, const void* f, uint32_t slot) {
   // through L1 (ld.ca): L1 holds no line from before this launch, so a hit is
   // still a lower bound of the slot's round-start value
-  if (semi == S_UNIT) return __ldca(reinterpret_cast<const uint32_t*>(f) + (slot >> 5));
-  if (semi == S_MAXMIN) return __ldca(reinterpret_cast<const uint32_t*>(f) + slot);
-  return __ldca(reinterpret_cast<const unsigned long long*>(f) + slot);
+  if (semi == S_UNIT) return PEEK_SLOT(reinterpret_cast<const uint32_t*>(f) + (slot >> 5));
+  if (semi == S_MAXMIN) return PEEK_SLOT(reinterpret_cast<const uint32_t*>(f) + slot);
+  return PEEK_SLOT(reinterpret_cast<const unsigned long long*>(f) + slot);
 }
 
 template <int N>

@@ -345,12 +345,11 @@ __device__ __forceinline__ uint64_t moves_n(const Move* mv, int n, uint64_t a, u
 #ifndef FJ_MINB_MX
 #define FJ_MINB_MX 5
 #endif
-// The stale read may come from L1 (ld.ca): L1 holds no lines from before this
-// launch, and slots only grow, so any value it returns is still a lower bound
-// of the slot and >= its round-start value (measured: -1% vs an L2 read).
-#ifndef PEEK
-#define PEEK __ldca
-#endif
+// The stale read is a relaxed GPU-scope load (device_util.cuh ld_relaxed):
+// slots only grow, so any value it returns is a lower bound of the slot and
+// >= its round-start value.  (A plain ld.ca through L1 was 1% faster but
+// formally a data race with the other threads' atomics.)
+#define PEEK PEEK_SLOT
 template <typename PK, int MAXDEG, int SEMI, int NM, bool REC>
 __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_MINB_MX : FJ_MINB) : 4)
     join_rows_direct_k(const JoinPlan jp,

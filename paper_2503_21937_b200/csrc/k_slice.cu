@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) slice_expand_k(const uint32_t* __restrict
       mycand += (unsigned long long)__popc(bits);
       const uint32_t nb = bits & ~Rb[idx];
       if (!nb) continue;
-      if (!(nb & ~__ldcg(Nb + idx))) continue;
+      if (!(nb & ~PEEK_SLOT(Nb + idx))) continue;  // stale lower bound (relaxed load; Nb only gains bits)
       atomicOr(Nb + idx, nb);
       atomicOr(dirty + (idx >> 5), 1u << (idx & 31));
     }
