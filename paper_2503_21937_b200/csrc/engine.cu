@@ -2631,6 +2631,24 @@ struct Ctx {
             T.ver[j][lpos[q]] = q == j ? TV_DELTA : (q < j ? TV_NEW : TV_OLD);
         }
       }
+      // the composition shape (tile_device.cuh compose_head): H(a,x,z) :- H(b,x,y), H(c,y,z), T(b,c,a)
+      T.shape = 0;
+      if (R.body.size() == 3 && R.cmps.empty() && lpos.size() == 2 && lpos[0] == 0 && lpos[1] == 1 &&
+          R.body[0].rel == R.head_rel && R.body[1].rel == R.head_rel && !local.count(R.body[2].rel) &&
+          prog.rels[R.head_rel].arity == 3 && prog.rels[R.body[2].rel].arity == 3) {
+        bool ok = true;
+        for (auto& a : R.body)
+          for (auto& t : a.args) ok &= t.is_var();
+        for (auto& t : R.head) ok &= t.is_var();
+        if (ok) {
+          const int b = R.body[0].args[0].var, x = R.body[0].args[1].var, y = R.body[0].args[2].var;
+          const int c = R.body[1].args[0].var, z = R.body[1].args[2].var, av = R.body[2].args[2].var;
+          const std::set<int> distinct{b, x, y, c, z, av};
+          ok = distinct.size() == 6 && R.body[1].args[1].var == y && R.body[2].args[0].var == b &&
+               R.body[2].args[1].var == c && R.head[0].var == av && R.head[1].var == x && R.head[2].var == z;
+        }
+        if (ok) T.shape = 1;
+      }
       T.ncmp = (int8_t)R.cmps.size();
       for (size_t i = 0; i < R.cmps.size(); ++i) {
         const Compare& c = R.cmps[i];
@@ -2693,7 +2711,9 @@ struct Ctx {
     int64_t slots = 0;
     for (int i = 0; i < P.nrel; ++i)
       if (P.rel[i].local) slots += (int64_t)P.rel[i].D * batch_cur;
-    if (slots > tile_max_slots) return false;
+    bool spelled = true;  // every recursive rule has a spelled-out shape (no interpretation)
+    for (int i = 0; i < P.nrule; ++i) spelled &= P.rule[i].seed || P.rule[i].shape != 0;
+    if (slots > tile_max_slots && !spelled) return false;
     P.smem_bytes = (int32_t)std::max<int64_t>(off, 16);
     return true;
   }

@@ -39,7 +39,7 @@
 namespace lob {
 namespace {
 
-constexpr int TILE_THREADS = 512;
+constexpr int TILE_THREADS = TILE_THREADS_N;
 
 template <int SEMI>
 __global__ void __launch_bounds__(TILE_THREADS, 1) tile_fixpoint_k(const TilePlan* __restrict__ Pg, int* rounds_out,
@@ -124,8 +124,7 @@ void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, un
       per_sm = it->second;
     }
   }
-  int threads = TILE_THREADS;
-  if (const char* e = getenv("LOBSTER_TILE_THREADS")) threads = std::max(32, std::min(TILE_THREADS, atoi(e)));
+  const int threads = TILE_THREADS;
   int grid = std::max(1, std::min(P.nsamples, std::max(1, per_sm) * sms));
   if (const char* e = getenv("LOBSTER_TILE_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
   tile_fixpoint_k<SEMI><<<grid, threads, P.smem_bytes, st>>>(dplan, rounds_out, ncand, cap_hit);

@@ -19,6 +19,7 @@ constexpr int TILE_S_UNIT = 0, TILE_S_MAXMIN = 1, TILE_S_ADDMULT = 2;  // == Sem
 // of the atoms its variable closes, so add-mult sums are formed in exactly the
 // oracle's fp64 order.
 constexpr int TILE_MAXREL = 6, TILE_MAXRULE = 8, TILE_MAXLEV = 5, TILE_MAXVAR = 4, TILE_MAXCOL = 4, TILE_MAXV = 10;
+constexpr int TILE_THREADS_N = 512;
 enum TileVer : int8_t { TV_EXT = 0, TV_NEW = 1, TV_OLD = 2, TV_DELTA = 3 };
 struct TileRel {
   int8_t ncols;
@@ -71,6 +72,7 @@ struct TileRule {
   int8_t nvariant;              // 1 for a seed rule
   int8_t ver[TILE_MAXVAR][TILE_MAXT];
   int8_t seed;                  // all-external rule: round 1 only
+  int8_t shape;                 // 1: composition H(a,x,z) :- K(b,x,y), K(c,y,z), T(b,c,a) (K local = H, T external)
   int8_t ncmp;
   TileCmp cmp[TILE_MAXC];
 };
