@@ -295,10 +295,18 @@ def main():
     cfg = CONFIGS[args.config]
     per_gpu = cfg["per_gpu"]
     ws, rank, local = dist_env()
+    # LOBSTER_BENCH_BACKEND=gloo + LOBSTER_BENCH_ONE_DEVICE=1: every rank on cuda:0 with
+    # gloo collectives — exercises the multi-rank path on a one-GPU box (not a measurement)
+    if os.environ.get("LOBSTER_BENCH_ONE_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("LOBSTER_BENCH_BACKEND", "nccl")
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        else:
+            dist.init_process_group(backend, init_method="env://")
     L = _lib.load()
     part = bool(cfg.get("partition"))  # key-partitioned: every rank holds the whole input
     gbatch = per_gpu if part else per_gpu * ws
@@ -430,7 +438,7 @@ def main():
             total_ms += e0.elapsed_time(e1)
             stats_all.append(st)
         launches = L.lobster_kernel_launches() - l0
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         per_rank = [total_ms]
         if ws > 1:
             allt = [torch.zeros_like(t) for _ in range(ws)]
@@ -461,7 +469,7 @@ def main():
     tuples_step = sum(s["tuples_derived"] for s in stats_all[-1])
     cands_step = sum(s["candidates"] for s in stats_all[-1])
     if part and ws > 1:  # each rank holds its owned tuples: the job's total is their sum
-        tt = torch.tensor([tuples_step, cands_step], dtype=torch.float64, device=dev)
+        tt = torch.tensor([tuples_step, cands_step], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt)
         tuples_step, cands_step = int(tt[0].item()), int(tt[1].item())
     mult = 1 if part else ws  # weak scaling: every rank did per-GPU work of the same size
@@ -485,7 +493,8 @@ def main():
         achieved = fj_b / fj_l / (fj_ms / fj_l / 1000.0) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr.get("dram_bytes_per_launch"),
-                    "kernel": "join_rows_direct_k (fused count-free join + ⊗ + direct ⊕ into the dense store)",
+                    "kernel": "join_rows_rec32_k / join_rows_direct_k (fused count-free join + ⊗ + direct ⊕ into the "
+                              "dense store; the 32-bit fast path takes every C2 launch)",
                     "launches_per_step": fj_all / len(rf_stats), "timed_launches_per_step": fj_l / len(rf_stats),
                     "timing": "CUDA events on the engine stream around every 4th launch (systematic sample); "
                               "bytes and time are those of the timed launches" +

@@ -79,6 +79,8 @@ def _counts_matrix(local_counts: List[int], group=None, device=None) -> np.ndarr
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    if dist.get_backend(group) != "nccl":
+        device = "cpu"
     t = torch.tensor(local_counts, dtype=torch.int64, device=device)
     allt = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(allt, t, group=group)
@@ -141,12 +143,12 @@ def all_gather_records(rec, group=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     out = torch.empty(world * rec.numel(), dtype=rec.dtype, device=rec.device)
-    if rec.device.type == "cuda":
+    if rec.device.type == "cuda" and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, rec.contiguous(), group=group)
-    else:  # gloo
-        parts = [torch.empty_like(rec) for _ in range(world)]
-        dist.all_gather(parts, rec.contiguous(), group=group)
-        out.copy_(torch.cat(parts))
+    else:  # gloo (host-staged)
+        parts = [torch.empty_like(rec, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, rec.contiguous().cpu(), group=group)
+        out.copy_(torch.cat(parts).to(out.device))
     return out
 
 
@@ -165,6 +167,11 @@ def records_global(gathered, batch: int, world: int):
 def all_reduce_grad(grad, group=None):
     """Sum the dense input-fact gradient across ranks (in place)."""
     import torch.distributed as dist
+    if grad.device.type == "cuda" and dist.get_backend(group) != "nccl":  # gloo: host-staged
+        h = grad.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        grad.copy_(h)
+        return grad
     dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
     return grad
 
