@@ -1,0 +1,18 @@
+# Round-2 (session 3) GPU pass: C3 compaction A/B, C1 timeline, tile tests.
+# usage: bash scripts/gpu_r02b.sh [what...]
+set -x
+mkdir -p gpurun_out
+for what in "$@"; do
+case $what in
+tile) timeout 900 python -m pytest tests/test_gpu_tile.py -x -q > gpurun_out/tile.log 2>&1; tail -5 gpurun_out/tile.log ;;
+c3ab) for v in 0 1; do
+        if [ $v = 1 ]; then export LOBSTER_NO_TILE_COMPACT=1; fi
+        timeout 600 python bench.py --config C3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3_nc$v.json 2> gpurun_out/bench_C3_nc$v.err
+        tail -2 gpurun_out/bench_C3_nc$v.err; cut -c1-200 gpurun_out/bench_C3_nc$v.json
+      done; unset LOBSTER_NO_TILE_COMPACT ;;
+c1log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 5 > gpurun_out/c1log.txt 2>&1; tail -30 gpurun_out/c1log.txt ;;
+c3log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C3 3 > gpurun_out/c3log.txt 2>&1; tail -12 gpurun_out/c3log.txt ;;
+c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 1 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
+configs) for c in C1 C2 C3 C4 C5 C2P SG; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -2 gpurun_out/bench_$c.err; cut -c1-300 gpurun_out/bench_$c.json; done ;;
+esac
+done
