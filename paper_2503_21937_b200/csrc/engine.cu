@@ -2513,6 +2513,7 @@ struct Ctx {
   // that closes an atom appears once in it and has a domain <= 64; and the
   // stratum's S / Δ / U arrays plus fibers fit one CTA's shared memory.
   bool no_tile = getenv("LOBSTER_NO_TILE") != nullptr;  // A/B: the per-round path
+  bool no_tile_compact = getenv("LOBSTER_NO_TILE_COMPACT") != nullptr;  // A/B: every head slot every round
   int64_t tile_max_slots = getenv("LOBSTER_TILE") ? INT64_MAX : 65536;
   TilePlan* hplan = nullptr;  // pinned
   int64_t class_dom(int cl) const { return class_max[cl] - class_min[cl] + 1; }
@@ -2662,6 +2663,22 @@ struct Ctx {
       }
     }
     P.nrel = (int)prel.size();
+    // compacted composition rounds (tile_device.cuh compose_rounds): one local
+    // relation whose only recursive rule is the composition shape.  (Fibers
+    // along its middle column, to cut each lane's y walk to the y with a
+    // candidate, measured slower: 13.8 vs 8.7 ms on C3 — the walk was uniform
+    // across a warp's lanes, the cut one diverges.)
+    P.cm_rule = -1;
+    P.cm_off = 0;
+    if (P.nlocal == 1 && !no_tile_compact) {
+      int cm = -1, nrec = 0;
+      for (int i = 0; i < P.nrule; ++i) {
+        if (P.rule[i].seed) continue;
+        ++nrec;
+        if (P.rule[i].shape == 1 && P.rule[i].head == P.local_rel[0]) cm = i;
+      }
+      if (nrec == 1 && cm >= 0) P.cm_rule = cm;
+    }
     // fiber strides (row-major over the other columns) and the shared-memory layout:
     // [fibers S, Δ | bits S, Δ] (zeroed per sample) then [bits U | tags S, Δ, U]
     int64_t off = 0;
@@ -2701,6 +2718,12 @@ struct Ctx {
           T.sm_tag[k] = (int32_t)off;
           off += (int64_t)T.D * 4;
         }
+    }
+    if (P.cm_rule >= 0) {  // compacted composition rounds: masks + pair list
+      const TileRel& H = P.rel[P.local_rel[0]];
+      off = (off + 15) & ~int64_t(15);
+      P.cm_off = (int32_t)off;
+      off += 320 * 8 + 64 + (int64_t)H.dom[1] * H.dom[2] * 6;
     }
     if (off > 200 * 1024) return false;
     // Each round pulls every head slot of every sample through an interpreted

@@ -41,9 +41,9 @@ namespace {
 
 constexpr int TILE_THREADS = TILE_THREADS_N;
 
-template <int SEMI>
-__global__ void __launch_bounds__(TILE_THREADS, 1) tile_fixpoint_k(const TilePlan* __restrict__ Pg, int* rounds_out,
-                                                                   unsigned long long* ncand, int* cap_hit) {
+template <int SEMI, int NT>
+__global__ void __launch_bounds__(NT, 1) tile_fixpoint_k(const TilePlan* __restrict__ Pg, int* rounds_out,
+                                                         unsigned long long* ncand, int* cap_hit) {
   extern __shared__ __align__(16) uint8_t sm[];
   // The plan (~5.5 KB) is copied to shared memory: every enumeration step
   // indexes it.  (Reading it through a pointer to a > 4 KB __grid_constant__
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 1) tile_fixpoint_k(const TilePla
   for (int i = threadIdx.x; i < (int)(sizeof(TilePlan) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(&Q)[i] = reinterpret_cast<const uint32_t*>(Pg)[i];
   __syncthreads();
-  tile_body<SEMI>(Q, sm, rounds_out, ncand, cap_hit);
+  tile_body<SEMI, (NT > 512 ? 2 : TILE_MAXLEV)>(Q, sm, rounds_out, ncand, cap_hit);
 }
 
 __global__ void tile_scatter_k(const __grid_constant__ TileScatter S) {
@@ -94,13 +94,13 @@ __global__ void max_i32_k(const int* __restrict__ a, int n, int* __restrict__ ou
   }
 }
 
-template <int SEMI>
+template <int SEMI, int NT>
 void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, unsigned long long* ncand, int* cap_hit,
                    cudaStream_t st) {
   static int configured_bytes = -1;  // per template: opt in to > 48 KB of dynamic shared memory once
   if (configured_bytes < P.smem_bytes) {
     const int dyn = 227 * 1024 - (int)((sizeof(TilePlan) + 255) & ~size_t(255));  // static plan copy + dynamic <= 227 KB
-    cuda_check(cudaFuncSetAttribute(tile_fixpoint_k<SEMI>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn),
+    cuda_check(cudaFuncSetAttribute(tile_fixpoint_k<SEMI, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn),
                "tile smem attribute");
     configured_bytes = dyn;
   }
@@ -118,16 +118,16 @@ void launch_tile_t(const TilePlan& P, const TilePlan* dplan, int* rounds_out, un
     }
     auto it = occ.find(P.smem_bytes);
     if (it == occ.end()) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_fixpoint_k<SEMI>, TILE_THREADS, P.smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_fixpoint_k<SEMI, NT>, NT, P.smem_bytes);
       occ[P.smem_bytes] = per_sm;
     } else {
       per_sm = it->second;
     }
   }
-  const int threads = TILE_THREADS;
+  const int threads = NT;
   int grid = std::max(1, std::min(P.nsamples, std::max(1, per_sm) * sms));
   if (const char* e = getenv("LOBSTER_TILE_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
-  tile_fixpoint_k<SEMI><<<grid, threads, P.smem_bytes, st>>>(dplan, rounds_out, ncand, cap_hit);
+  tile_fixpoint_k<SEMI, NT><<<grid, threads, P.smem_bytes, st>>>(dplan, rounds_out, ncand, cap_hit);
 }
 
 }  // namespace
@@ -138,10 +138,25 @@ void launch_tile_fixpoint(const TilePlan& P, TilePlan* dplan, int* rounds_out, u
   // P should live in pinned host memory (the engine's staging copy): an async copy
   cuda_check(cudaMemcpyAsync(dplan, &P, sizeof(TilePlan), cudaMemcpyHostToDevice, st), "tile plan");
   note_launch();
+  // compacted composition plans: the recursive rounds need few registers, so
+  // a 1024-thread CTA (64 registers) doubles the warps hiding shared-memory
+  // latency (LOBSTER_TILE_THREADS=512 for A/B)
+  static const int nt_env = getenv("LOBSTER_TILE_THREADS") ? atoi(getenv("LOBSTER_TILE_THREADS")) : 1024;
+  bool wide = P.cm_rule >= 0 && nt_env >= 1024;
+  for (int i = 0; i < P.nrule && wide; ++i) wide = i == P.cm_rule || P.rule[i].nlev <= 2;
   switch (P.semi) {
-    case S_UNIT: launch_tile_t<S_UNIT>(P, dplan, rounds_out, ncand, cap_hit, st); break;
-    case S_MAXMIN: launch_tile_t<S_MAXMIN>(P, dplan, rounds_out, ncand, cap_hit, st); break;
-    default: launch_tile_t<S_ADDMULT>(P, dplan, rounds_out, ncand, cap_hit, st); break;
+    case S_UNIT:
+      if (wide) launch_tile_t<S_UNIT, 1024>(P, dplan, rounds_out, ncand, cap_hit, st);
+      else launch_tile_t<S_UNIT, TILE_THREADS>(P, dplan, rounds_out, ncand, cap_hit, st);
+      break;
+    case S_MAXMIN:
+      if (wide) launch_tile_t<S_MAXMIN, 1024>(P, dplan, rounds_out, ncand, cap_hit, st);
+      else launch_tile_t<S_MAXMIN, TILE_THREADS>(P, dplan, rounds_out, ncand, cap_hit, st);
+      break;
+    default:
+      if (wide) launch_tile_t<S_ADDMULT, 1024>(P, dplan, rounds_out, ncand, cap_hit, st);
+      else launch_tile_t<S_ADDMULT, TILE_THREADS>(P, dplan, rounds_out, ncand, cap_hit, st);
+      break;
   }
 }
 

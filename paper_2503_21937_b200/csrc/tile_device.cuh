@@ -195,15 +195,24 @@ __device__ __forceinline__ void level(Frame& F, const TileRule& R, uint32_t aliv
   }
 }
 
-template <int SEMI>
+// MAXL: deepest enumeration compiled in (the 1024-thread variant keeps only
+// shallow seed rules, the host checks R.nlev <= MAXL)
+template <int SEMI, int MAXL>
 __device__ __forceinline__ void enumerate(Frame& F, const TileRule& R, uint32_t alive) {
   switch (R.nlev) {
     case 0: level<SEMI, 0, 0>(F, R, alive); break;
     case 1: level<SEMI, 0, 1>(F, R, alive); break;
-    case 2: level<SEMI, 0, 2>(F, R, alive); break;
-    case 3: level<SEMI, 0, 3>(F, R, alive); break;
-    case 4: level<SEMI, 0, 4>(F, R, alive); break;
-    default: level<SEMI, 0, 5>(F, R, alive); break;
+    default:
+      if constexpr (MAXL <= 2) {
+        level<SEMI, 0, 2>(F, R, alive);
+      } else {
+        switch (R.nlev) {
+          case 2: level<SEMI, 0, 2>(F, R, alive); break;
+          case 3: level<SEMI, 0, 3>(F, R, alive); break;
+          case 4: level<SEMI, 0, 4>(F, R, alive); break;
+          default: level<SEMI, 0, 5>(F, R, alive); break;
+        }
+      }
   }
 }
 
@@ -214,12 +223,18 @@ __device__ __forceinline__ void enumerate(Frame& F, const TileRule& R, uint32_t 
 // interpreting the plan (the generic path spent ~200 instructions per
 // candidate on plan reads and atom loops).  Variant 0 reads Δ(b,x,y),
 // OLD(c,y,z); variant 1 NEW(b,x,y), Δ(c,y,z).
+//
+// ys_s / ys_d: the y values z can be reached from through OLD(·, y, z) /
+// Δ(·, y, z) (all ones when unknown).  A y outside (Δ(b,x,·) ∩ ys_s) ∪
+// (NEW(b,x,·) ∩ ys_d) has no candidate in either variant, so skipping it
+// leaves the candidates and their order unchanged.
 template <int SEMI>
-__device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
+__device__ __forceinline__ void compose_core(Frame& F, const TileRule& R, int a, int x, int z,
+                                             unsigned long long ys_s, unsigned long long ys_d,
+                                             unsigned long long bs) {
   const TileRel& K = TP(F).rel[R.atom[0].rel];
   const TileRel& T = TP(F).rel[R.atom[2].rel];
   const TileRel& TQ = F.Q->rel[R.atom[2].rel];
-  const int a = getv(F.vals, R.atom[2].var[2]), x = getv(F.vals, R.atom[0].var[1]), z = getv(F.vals, R.atom[1].var[2]);
   const int RB = K.dom[0];
   const unsigned long long* Sf2 = reinterpret_cast<const unsigned long long*>(F.sm + K.sm_fib[0][2]);
   const unsigned long long* Df2 = reinterpret_cast<const unsigned long long*>(F.sm + K.sm_fib[1][2]);
@@ -230,12 +245,16 @@ __device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
   const uint32_t* Sb = reinterpret_cast<const uint32_t*>(F.sm + K.sm_bits[0]);
   const unsigned long long* Tf = TQ.fib[1] + (T.shared ? 0 : (int64_t)F.s * T.nfib[1]);
   const float* Tt = TQ.tag ? TQ.tag + (T.shared ? 0 : (int64_t)F.s * T.D) : nullptr;
-  for (int b = 0; b < RB; ++b) {
-    const unsigned long long tf = __ldg(Tf + b * T.fstride[1][0] + a * T.fstride[1][2]);  // c with T(b, c, a)
-    if (!tf) continue;
+  (void)RB;
+  while (bs) {  // b with NEW(b, x, ·) non-empty (a superset: all ones when unknown)
+    const int b = __ffsll((long long)bs) - 1;
+    bs &= bs - 1;
     const int fbx = b * K.fstride[2][0] + x * K.fstride[2][1];
     const unsigned long long d0 = Df2[fbx], n0 = Sf2[fbx] | d0;  // y with Δ / NEW (b, x, y)
-    unsigned long long ys = n0;
+    unsigned long long ys = (d0 & ys_s) | (n0 & ys_d);
+    if (!ys) continue;
+    const unsigned long long tf = __ldg(Tf + b * T.fstride[1][0] + a * T.fstride[1][2]);  // c with T(b, c, a)
+    if (!tf) continue;
     while (ys) {
       const int y = __ffsll((long long)ys) - 1;
       ys &= ys - 1;
@@ -279,8 +298,212 @@ __device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
   }
 }
 
-// U of head slot h of local relation `hr` (one round; seed = round 1)
+// compose_core with 32-bit masks (relation-type and entity domains <= 32, the
+// low words of the 64-bit fibers), the T tag row and the (y, z) slot part
+// hoisted out of the candidate loop: the same candidates in the same order.
 template <int SEMI>
+__device__ __forceinline__ void compose_core32(Frame& F, const TileRule& R, int a, int x, int z, uint32_t ys_s,
+                                               uint32_t ys_d, uint32_t bs) {
+  const TileRel& K = TP(F).rel[R.atom[0].rel];
+  const TileRel& T = TP(F).rel[R.atom[2].rel];
+  const TileRel& TQ = F.Q->rel[R.atom[2].rel];
+  const uint32_t* Sf2 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[0][2]);  // low words: [2 f]
+  const uint32_t* Df2 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[1][2]);
+  const uint32_t* Sf0 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[0][0]);
+  const uint32_t* Df0 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[1][0]);
+  const float* St = reinterpret_cast<const float*>(F.sm + K.sm_tag[0]);
+  const float* Dt = reinterpret_cast<const float*>(F.sm + K.sm_tag[1]);
+  const uint32_t* Sb = reinterpret_cast<const uint32_t*>(F.sm + K.sm_bits[0]);
+  const uint32_t* Tf = reinterpret_cast<const uint32_t*>(TQ.fib[1] + (T.shared ? 0 : (int64_t)F.s * T.nfib[1]));
+  const float* Tt = TQ.tag ? TQ.tag + (T.shared ? 0 : (int64_t)F.s * T.D) : nullptr;
+  const int ks0 = K.stride[0], zs = z * K.stride[2], xs = x * K.stride[1];
+  const int f2x = x * K.fstride[2][1], f2b = K.fstride[2][0], f0y = K.fstride[0][1], f0z = z * K.fstride[0][2];
+  const int tfb = T.fstride[1][0], tfa = a * T.fstride[1][2], ts0 = T.stride[0], ts1 = T.stride[1];
+  const int ta = a * T.stride[2];
+  double acc = F.acc;
+  float mx = F.mx;
+  uint32_t nc = F.ncand;
+  while (bs) {
+    const int b = __ffs(bs) - 1;
+    bs &= bs - 1;
+    const int fbx = b * f2b + f2x;
+    const uint32_t d0 = Df2[2 * fbx], n0 = Sf2[2 * fbx] | d0;
+    uint32_t ys = (d0 & ys_s) | (n0 & ys_d);
+    if (!ys) continue;
+    const uint32_t tf = __ldg(Tf + 2 * (b * tfb + tfa));
+    if (!tf) continue;
+    const float* Ttb = Tt ? Tt + b * ts0 + ta : nullptr;
+    const int bx = b * ks0 + xs;
+    while (ys) {
+      const int y = __ffs(ys) - 1;
+      ys &= ys - 1;
+      const int fyz = y * f0y + f0z;
+      const uint32_t dy = (d0 >> y) & 1u;
+      const uint32_t m0 = dy ? (Sf0[2 * fyz] & tf) : 0u;  // v0: Δ(b,x,y) OLD(c,y,z)
+      const uint32_t m1 = Df0[2 * fyz] & tf;              // v1: NEW(b,x,y) Δ(c,y,z)
+      uint32_t cs = m0 | m1;
+      if (!cs) continue;
+      float nbxy = 0.0f, dbxy = 0.0f;
+      if constexpr (SEMI != TILE_S_UNIT) {
+        const int sbxy = bx + y * K.stride[2];
+        dbxy = Dt[sbxy];
+        const bool sp = tbit(Sb, sbxy);
+        nbxy = sp ? (dy ? oplus_state<SEMI>(St[sbxy], dbxy) : St[sbxy]) : dbxy;
+      }
+      const int yz = y * K.stride[1] + zs;
+      while (cs) {
+        const int c = __ffs(cs) - 1;
+        cs &= cs - 1;
+        const int scyz = c * ks0 + yz;
+        const float tc = (SEMI != TILE_S_UNIT && Ttb) ? __ldg(Ttb + c * ts1) : 1.0f;
+        if ((m0 >> c) & 1u) {
+          ++nc;
+          if constexpr (SEMI != TILE_S_UNIT) {
+            const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(dbxy, St[scyz]), tc);
+            if constexpr (SEMI == TILE_S_ADDMULT) acc = __dadd_rn(acc, (double)t);
+            else mx = (nc == 1 || t > mx) ? t : mx;
+          }
+        }
+        if ((m1 >> c) & 1u) {
+          ++nc;
+          if constexpr (SEMI != TILE_S_UNIT) {
+            const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(nbxy, Dt[scyz]), tc);
+            if constexpr (SEMI == TILE_S_ADDMULT) acc = __dadd_rn(acc, (double)t);
+            else mx = (nc == 1 || t > mx) ? t : mx;
+          }
+        }
+      }
+    }
+  }
+  F.acc = acc;
+  F.mx = mx;
+  F.any = F.any || nc != F.ncand;
+  F.ncand = nc;
+}
+
+template <int SEMI>
+__device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
+  compose_core<SEMI>(F, R, getv(F.vals, R.atom[2].var[2]), getv(F.vals, R.atom[0].var[1]),
+                     getv(F.vals, R.atom[1].var[2]), ~0ull, ~0ull,
+                     TP(F).rel[R.atom[0].rel].dom[0] >= 64 ? ~0ull : (1ull << TP(F).rel[R.atom[0].rel].dom[0]) - 1ull);
+}
+
+// One recursive round of a stratum whose only recursive rule is the
+// composition shape (TilePlan::cm_rule): U of every head slot, evaluating
+// only the slots (a, x, z) whose pair (x, z) can receive a candidate:
+//   (Δ(·, x, ·) ∩ OLD(·, ·, z)-sources) ∪ (NEW(·, x, ·) ∩ Δ(·, ·, z)-sources) ≠ ∅
+// over y (a superset of the slots with candidates; the others get no U, as
+// before).  Active pairs are listed in shared memory and handed out with a
+// fastest across lanes, so a warp's lanes share the (b, y) walk and differ
+// only in the T fiber.  Per slot the enumeration is compose_core's: same
+// candidates, same canonical order, bit-identical U.
+template <int SEMI>
+__device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint8_t* sm, uint64_t& my_cand) {
+  const TileRule& R = TP(F).rule[Q.cm_rule];
+  const TileRel& H = TP(F).rel[R.head];
+  const int A = H.dom[0], X = H.dom[1], Z = H.dom[2];
+  unsigned long long* AX = reinterpret_cast<unsigned long long*>(sm + Q.cm_off);  // y: Δ(b, x, y) for some b
+  unsigned long long* NX = AX + 64;                                              // y: NEW(b, x, y)
+  unsigned long long* SY = AX + 128;                                             // y: OLD(c, y, z) for some c
+  unsigned long long* DY = AX + 192;                                             // y: Δ(c, y, z)
+  unsigned long long* BX = AX + 256;                                             // b: NEW(b, x, ·) non-empty
+  uint32_t* npairs = reinterpret_cast<uint32_t*>(AX + 320);
+  // npairs: [0] active pairs, [1] work counter, [2..5] pairs per cost class, [6..9] class offsets
+  uint32_t* slotof = npairs + 16;                                                // per pair: class << 16 | rank
+  uint16_t* pairs = reinterpret_cast<uint16_t*>(slotof + X * Z);
+  const unsigned long long* Sf2 = reinterpret_cast<const unsigned long long*>(sm + H.sm_fib[0][2]);
+  const unsigned long long* Df2 = reinterpret_cast<const unsigned long long*>(sm + H.sm_fib[1][2]);
+  const unsigned long long* Sf0 = reinterpret_cast<const unsigned long long*>(sm + H.sm_fib[0][0]);
+  const unsigned long long* Df0 = reinterpret_cast<const unsigned long long*>(sm + H.sm_fib[1][0]);
+  uint32_t* Ub = reinterpret_cast<uint32_t*>(sm + H.sm_bits[2]);
+  float* Ut = reinterpret_cast<float*>(sm + H.sm_tag[2]);
+  const int t = threadIdx.x;
+  if (t < X) {
+    unsigned long long ax = 0, nx = 0, bx = 0;
+    for (int b = 0; b < A; ++b) {
+      const int f = b * H.fstride[2][0] + t * H.fstride[2][1];
+      const unsigned long long n = Sf2[f] | Df2[f];
+      ax |= Df2[f];
+      nx |= n;
+      bx |= (unsigned long long)(n != 0ull) << b;
+    }
+    AX[t] = ax;
+    NX[t] = nx;
+    BX[t] = bx;
+  } else if (t >= 64 && t < 64 + Z) {
+    const int z = t - 64;
+    unsigned long long sy = 0, dy = 0;
+    for (int y = 0; y < H.dom[1]; ++y) {
+      const int f = y * H.fstride[0][1] + z * H.fstride[0][2];
+      sy |= (unsigned long long)(Sf0[f] != 0ull) << y;
+      dy |= (unsigned long long)(Df0[f] != 0ull) << y;
+    }
+    SY[z] = sy;
+    DY[z] = dy;
+  } else if (t == 128) {
+    for (int k = 0; k < 10; ++k) npairs[k] = 0;
+  }
+  const int nw = (H.D + 31) >> 5;
+  for (int w = t; w < nw; w += blockDim.x) Ub[w] = 0u;
+  __syncthreads();
+  for (int p = t; p < X * Z; p += blockDim.x) {
+    const int x = p / Z, z = p - x * Z;
+    const unsigned long long ys = (AX[x] & SY[z]) | (NX[x] & DY[z]);
+    if (!ys) continue;
+    // longest first (a round ends at its slowest warp): class by the size of
+    // the pair's (b, y) walk, heaviest class first
+    const int cost = __popcll(BX[x]) * __popcll(ys);
+    const int k = cost >= 96 ? 0 : cost >= 32 ? 1 : cost >= 8 ? 2 : 3;
+    slotof[p] = ((uint32_t)k << 16) | atomicAdd(npairs + 2 + k, 1u);
+  }
+  __syncthreads();
+  if (t == 0) {
+    uint32_t o = 0;
+    for (int k = 0; k < 4; ++k) {
+      npairs[6 + k] = o;
+      o += npairs[2 + k];
+    }
+    npairs[0] = o;
+  }
+  __syncthreads();
+  for (int p = t; p < X * Z; p += blockDim.x) {
+    const int x = p / Z, z = p - x * Z;
+    if ((AX[x] & SY[z]) | (NX[x] & DY[z])) pairs[npairs[6 + (slotof[p] >> 16)] + (slotof[p] & 0xffffu)] = (uint16_t)p;
+  }
+  __syncthreads();
+  const int items = (int)npairs[0] * A;
+  const bool narrow = A <= 32 && H.dom[1] <= 32 && H.dom[2] <= 32;  // 32-bit masks (K == H)
+  // warps claim 32 items at a time (items differ a lot in cost; a static
+  // stride left warps waiting at the round's barrier)
+  const int lane = t & 31;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = (int)atomicAdd(npairs + 1, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= items) break;
+    const int i = base + lane;
+    if (i >= items) continue;
+    const int p = pairs[i / A], a = i - (i / A) * A;
+    const int x = p / Z, z = p - x * Z;
+    F.acc = 0.0;
+    F.mx = 0.0f;
+    F.any = false;
+    F.ncand = 0;
+    if (narrow)
+      compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
+    else
+      compose_core<SEMI>(F, R, a, x, z, SY[z], DY[z], BX[x]);
+    my_cand += F.ncand;
+    if (F.any) {
+      const int h = a * H.stride[0] + x * H.stride[1] + z * H.stride[2];
+      atomicOr(Ub + (h >> 5), 1u << (h & 31));
+      if constexpr (SEMI != TILE_S_UNIT) Ut[h] = SEMI == TILE_S_ADDMULT ? (float)F.acc : F.mx;
+    }
+  }
+}
+
+// U of head slot h of local relation `hr` (one round; seed = round 1)
+template <int SEMI, int MAXL>
 __device__ __forceinline__ void eval_head(Frame& F, int hr, int h, bool seed) {
   const TileRel& H = TP(F).rel[hr];
   TILE_UNROLL
@@ -319,13 +542,13 @@ __device__ __forceinline__ void eval_head(Frame& F, int hr, int h, bool seed) {
       continue;
     }
     if (alive) alive = prune(F, R, -1, alive);
-    if (alive) enumerate<SEMI>(F, R, alive);
+    if (alive) enumerate<SEMI, MAXL>(F, R, alive);
   }
 }
 
 // The fixpoint of one stratum; Q: the launched plan, copied into shared
 // memory by the caller (sm: the dynamic shared memory of the relations).
-template <int SEMI>
+template <int SEMI, int MAXL = TILE_MAXLEV>
 __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* rounds_out, unsigned long long* ncand,
                                           int* cap_hit) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -344,6 +567,8 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
       // (i) + (iii): U per head slot (staged in shared memory; keeping the u
       // values in registers instead, with eval_head out of line, measured
       // 23.2 ms vs 17.5 ms on C3 — and 19.3 ms at 64 registers / 2 CTAs per SM)
+      if (!seed && Q.cm_rule >= 0) compose_rounds<SEMI>(F, Q, sm, my_cand);
+      else
       TILE_UNROLL
       for (int li = 0; li < TP(F).nlocal; ++li) {
         const int hr = TP(F).local_rel[li];
@@ -357,7 +582,7 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
           F.mx = 0.0f;
           F.any = false;
           F.ncand = 0;
-          if (h < H.D) eval_head<SEMI>(F, hr, h, seed);
+          if (h < H.D) eval_head<SEMI, MAXL>(F, hr, h, seed);
           my_cand += F.ncand;
           if (Q.trace && F.ncand) atomicAdd(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 2, F.ncand);
           const uint32_t word = __ballot_sync(~0u, F.any);

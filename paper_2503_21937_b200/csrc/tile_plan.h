@@ -86,6 +86,15 @@ struct TilePlan {
   TileRule rule[TILE_MAXRULE];
   int32_t smem_bytes;
   int32_t clear_words;           // leading u32 words of shared memory zeroed per sample (bits + fibers)
+  // Compacted composition rounds (tile_device.cuh compose_rounds): the
+  // stratum is one local relation whose only recursive rule is the
+  // composition shape.  Rounds >= 2 evaluate only the head slots (a, x, z)
+  // whose (x, z) pair can receive a candidate this round, a fastest across
+  // lanes.  cm_rule: that rule's index, -1 off; cm_off: shared-memory bytes of
+  // the per-x / per-z masks (5 × 64 u64), counters, per-pair cost class
+  // and rank (u32) and the pair list (u16, heaviest cost class first).
+  int32_t cm_rule;
+  int32_t cm_off;
   uint32_t* trace;               // debug (LOBSTER_TILE_TRACE): per (sample, round < 64) candidates, |Δ'|
   unsigned long long* counts;    // per local relation (local_rel order): tuples at the fixpoint
 };

@@ -10,9 +10,13 @@ c3ab) for v in 0 1; do
         timeout 600 python bench.py --config C3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3_nc$v.json 2> gpurun_out/bench_C3_nc$v.err
         tail -2 gpurun_out/bench_C3_nc$v.err; cut -c1-200 gpurun_out/bench_C3_nc$v.json
       done; unset LOBSTER_NO_TILE_COMPACT ;;
+c3nt) for nt in 1024 512; do
+        LOBSTER_TILE_THREADS=$nt timeout 600 python bench.py --config C3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3_nt$nt.json 2> gpurun_out/bench_C3_nt$nt.err
+        tail -2 gpurun_out/bench_C3_nt$nt.err; cut -c1-200 gpurun_out/bench_C3_nt$nt.json
+      done ;;
 c1log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 5 > gpurun_out/c1log.txt 2>&1; tail -30 gpurun_out/c1log.txt ;;
 c3log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C3 3 > gpurun_out/c3log.txt 2>&1; tail -12 gpurun_out/c3log.txt ;;
-c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 1 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
+c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 2 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
 configs) for c in C1 C2 C3 C4 C5 C2P SG; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -2 gpurun_out/bench_$c.err; cut -c1-300 gpurun_out/bench_$c.json; done ;;
 esac
 done

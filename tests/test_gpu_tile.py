@@ -206,3 +206,21 @@ def test_determinism():
         outs.append((o.cols.tobytes(), o.probs.tobytes()))
         eng.close()
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2])
+def test_compacted_composition_rounds_identical(monkeypatch, sr):
+    """Rounds >= 2 of the composition stratum evaluate only the head slots whose
+    (x, z) pair can receive a candidate (compose_rounds): the same candidates
+    in the same canonical order as evaluating every slot, so tuples, tags,
+    candidate and round counts are identical — and bit-exact with the oracle."""
+    w = W.c3_workload(semiring=sr, batch=12, entities=16, rtypes=10, skips=8, ncomp=60)
+    eng, st, _ = _check(w, ["kinship", "answer"], tiles=2)
+    a = eng.output("kinship")
+    monkeypatch.setenv("LOBSTER_NO_TILE_COMPACT", "1")
+    eng2, st2, _ = engine_run(w)
+    b = eng2.output("kinship")
+    assert np.array_equal(a.sample_ids, b.sample_ids) and np.array_equal(a.cols, b.cols)
+    if sr != 0:
+        assert np.array_equal(a.probs.view(np.uint32), b.probs.view(np.uint32))
+    assert st["candidates"] == st2["candidates"] and st["rounds_total"] == st2["rounds_total"]
