@@ -2670,6 +2670,8 @@ struct Ctx {
     // across a warp's lanes, the cut one diverges.)
     P.cm_rule = -1;
     P.cm_off = 0;
+    P.cm_nocert = getenv("LOBSTER_TILE_NO_CERT") ? 1 : 0;
+    P.cm_nosplit = getenv("LOBSTER_TILE_NO_SPLIT") ? 1 : 0;
     if (P.nlocal == 1 && !no_tile_compact) {
       int cm = -1, nrec = 0;
       for (int i = 0; i < P.nrule; ++i) {
@@ -2723,7 +2725,7 @@ struct Ctx {
       const TileRel& H = P.rel[P.local_rel[0]];
       off = (off + 15) & ~int64_t(15);
       P.cm_off = (int32_t)off;
-      off += 320 * 8 + 64 + (int64_t)H.dom[1] * H.dom[2] * 6;
+      off += 320 * 8 + 64 + (int64_t)H.dom[1] * H.dom[2] * 6 + 8 + (int64_t)TILE_CM_PARTS * 20;
     }
     if (off > 200 * 1024) return false;
     // Each round pulls every head slot of every sample through an interpreted
@@ -2801,8 +2803,8 @@ struct Ctx {
     P.counts = reinterpret_cast<unsigned long long*>(d + 2);
     std::vector<uint32_t> htr;
     if (getenv("LOBSTER_TILE_TRACE")) {  // debug: per (sample, round) candidates and |Δ'|
-      P.trace = arena.get<uint32_t>((int64_t)B * 128);
-      cuda_check(cudaMemsetAsync(P.trace, 0, (size_t)B * 128 * 4, st), "memset");
+      P.trace = arena.get<uint32_t>((int64_t)B * 256);
+      cuda_check(cudaMemsetAsync(P.trace, 0, (size_t)B * 256 * 4, st), "memset");
     }
     {
       Phase ph(this, 0);
@@ -2813,13 +2815,16 @@ struct Ctx {
       kcheck("tile fixpoint");
     }
     if (P.trace) {
-      htr.resize((size_t)B * 128);
+      htr.resize((size_t)B * 256);
       cuda_check(cudaMemcpyAsync(htr.data(), P.trace, htr.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
       sync();
       for (int s = 0; s < B; ++s) {
         fprintf(stderr, "[tile] sample %d:", s);
-        for (int r = 1; r < 64 && (htr[(s * 64 + r) * 2] || htr[(s * 64 + r) * 2 + 1]); ++r)
-          fprintf(stderr, " r%d c%u d%u", r, htr[(s * 64 + r) * 2], htr[(s * 64 + r) * 2 + 1]);
+        for (int r = 1; r < 64 && (htr[(s * 64 + r) * 4] || htr[(s * 64 + r) * 4 + 1]); ++r)
+          fprintf(stderr, " r%d c%u d%u", r, htr[(s * 64 + r) * 4], htr[(s * 64 + r) * 4 + 1]);
+        fprintf(stderr, "\n[tile] sample %d U phase / longest item (x16 cycles):", s);
+        for (int r = 1; r < 64 && htr[(s * 64 + r) * 4 + 3]; ++r)
+          fprintf(stderr, " r%d %u/%u", r, htr[(s * 64 + r) * 4 + 3], htr[(s * 64 + r) * 4 + 2]);
         fprintf(stderr, "\n");
       }
     }

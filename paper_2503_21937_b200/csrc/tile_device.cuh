@@ -43,6 +43,7 @@ struct Frame {
   int s;
   unsigned long long vals;
   double acc;
+  double aabs;  // Σ|t| of add-mult terms (split composition items: the rounding certificate)
   float mx;
   bool any;
   uint32_t ncand;
@@ -301,7 +302,7 @@ __device__ __forceinline__ void compose_core(Frame& F, const TileRule& R, int a,
 // compose_core with 32-bit masks (relation-type and entity domains <= 32, the
 // low words of the 64-bit fibers), the T tag row and the (y, z) slot part
 // hoisted out of the candidate loop: the same candidates in the same order.
-template <int SEMI>
+template <int SEMI, bool ABS = false>
 __device__ __forceinline__ void compose_core32(Frame& F, const TileRule& R, int a, int x, int z, uint32_t ys_s,
                                                uint32_t ys_d, uint32_t bs) {
   const TileRel& K = TP(F).rel[R.atom[0].rel];
@@ -320,7 +321,7 @@ __device__ __forceinline__ void compose_core32(Frame& F, const TileRule& R, int 
   const int f2x = x * K.fstride[2][1], f2b = K.fstride[2][0], f0y = K.fstride[0][1], f0z = z * K.fstride[0][2];
   const int tfb = T.fstride[1][0], tfa = a * T.fstride[1][2], ts0 = T.stride[0], ts1 = T.stride[1];
   const int ta = a * T.stride[2];
-  double acc = F.acc;
+  double acc = F.acc, aabs = F.aabs;
   float mx = F.mx;
   uint32_t nc = F.ncand;
   while (bs) {
@@ -360,22 +361,31 @@ __device__ __forceinline__ void compose_core32(Frame& F, const TileRule& R, int 
           ++nc;
           if constexpr (SEMI != TILE_S_UNIT) {
             const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(dbxy, St[scyz]), tc);
-            if constexpr (SEMI == TILE_S_ADDMULT) acc = __dadd_rn(acc, (double)t);
-            else mx = (nc == 1 || t > mx) ? t : mx;
+            if constexpr (SEMI == TILE_S_ADDMULT) {
+              acc = __dadd_rn(acc, (double)t);
+              if constexpr (ABS) aabs = __dadd_rn(aabs, fabs((double)t));
+            } else {
+              mx = (nc == 1 || t > mx) ? t : mx;
+            }
           }
         }
         if ((m1 >> c) & 1u) {
           ++nc;
           if constexpr (SEMI != TILE_S_UNIT) {
             const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(nbxy, Dt[scyz]), tc);
-            if constexpr (SEMI == TILE_S_ADDMULT) acc = __dadd_rn(acc, (double)t);
-            else mx = (nc == 1 || t > mx) ? t : mx;
+            if constexpr (SEMI == TILE_S_ADDMULT) {
+              acc = __dadd_rn(acc, (double)t);
+              if constexpr (ABS) aabs = __dadd_rn(aabs, fabs((double)t));
+            } else {
+              mx = (nc == 1 || t > mx) ? t : mx;
+            }
           }
         }
       }
     }
   }
   F.acc = acc;
+  F.aabs = aabs;
   F.mx = mx;
   F.any = F.any || nc != F.ncand;
   F.ncand = nc;
@@ -388,6 +398,137 @@ __device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
                      TP(F).rel[R.atom[0].rel].dom[0] >= 64 ? ~0ull : (1ull << TP(F).rel[R.atom[0].rel].dom[0]) - 1ull);
 }
 
+// A round ends at its longest head item (C3: from round ~6 on, one item's
+// (b, y) walk IS the round).  The items of the heaviest pairs (all of them
+// when the round has fewer items than threads) are split into P parts by b
+// (ranks ≡ part mod P), the parts run in parallel and their partial results
+// are combined per head:
+//   unit: any part;  max-min: the max (exact, order-free);
+//   add-mult: the fp64 sum of the parts.  The sequential fp64 sum S_seq of
+//   the oracle's canonical order and this S_par both lie within
+//   (n + P)·2^-53·Σ|t| of the exact sum (n terms; every term takes at most
+//   n + P roundings), so when every value in S_par ± d, d = (2(n + P) + 4)·
+//   2^-53·Σ|t|·1.01, rounds to the same fp32 value, that value IS
+//   fl32(S_seq) (rounding is monotone).  Otherwise (rare: S within d of an
+//   fp32 rounding boundary) the head is recomputed sequentially in canonical
+//   order.  Either way U is bit-identical to the sequential walk.
+template <int SEMI>
+__device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const TileRel& H, int items, uint8_t* pb,
+                                           uint32_t* npairs, const uint16_t* pairs, const unsigned long long* AX,
+                                           uint64_t& my_cand, uint32_t* tr) {
+  const unsigned long long* SY = AX + 128;
+  const unsigned long long* DY = AX + 192;
+  const unsigned long long* BX = AX + 256;
+  const int A = H.dom[0], Z = H.dom[2];
+  pb = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pb) + 7) & ~uintptr_t(7));
+  double* pacc = reinterpret_cast<double*>(pb);
+  double* pabs = pacc + TILE_CM_PARTS;
+  uint32_t* pcnt = reinterpret_cast<uint32_t*>(pabs + TILE_CM_PARTS);
+  uint32_t* Ub = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(F.sm) + H.sm_bits[2]);
+  float* Ut = reinterpret_cast<float*>(const_cast<uint8_t*>(F.sm) + H.sm_tag[2]);
+  // split every pair's items when the round has fewer items than threads
+  // (splitting only the heaviest classes of the larger rounds measured slower:
+  // 6.42 vs 6.21 ms on C3 — those rounds are throughput-, not path-bound)
+  const int npr = items / A;
+  int ns = items < (int)blockDim.x ? npr : 0;
+  int P = 1;
+  while (P < 8 && ns * A * P * 2 <= TILE_CM_PARTS && (ns * A * P < (int)blockDim.x || ns < npr)) P <<= 1;
+  if (P == 1) ns = 0;
+  const int nsub = ns * A * P, total = nsub + (npr - ns) * A;
+  const int t = threadIdx.x, lane = t & 31;
+  for (;;) {  // (pair, part, a): a fastest, so a warp's lanes share the b subset
+    int base = 0;
+    if (lane == 0) base = (int)atomicAdd(npairs + 1, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= total) break;
+    const int i = base + lane;
+    if (i >= total) continue;
+    F.acc = 0.0;
+    F.aabs = 0.0;
+    F.mx = 0.0f;
+    F.any = false;
+    F.ncand = 0;
+    const long long c0 = tr ? clock64() : 0;
+    if (i >= nsub) {  // a whole item: U directly
+      const int w = i - nsub + ns * A, pi = w / A, a = w - pi * A;
+      const int p = pairs[pi], x = p / Z, z = p - x * Z;
+      compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
+      my_cand += F.ncand;
+      if (tr) {
+        atomicAdd(tr, F.ncand);
+        atomicMax(tr + 2, (uint32_t)((clock64() - c0) >> 4));
+      }
+      if (F.any) {
+        const int h = a * H.stride[0] + x * H.stride[1] + z * H.stride[2];
+        atomicOr(Ub + (h >> 5), 1u << (h & 31));
+        if constexpr (SEMI != TILE_S_UNIT) Ut[h] = SEMI == TILE_S_ADDMULT ? (float)F.acc : F.mx;
+      }
+      continue;
+    }
+    const int pi = i / (A * P), rem = i - pi * (A * P), part = rem / A, a = rem - part * A;
+    const int p = pairs[pi], x = p / Z, z = p - x * Z;
+    uint32_t bm = (uint32_t)BX[x], bs = 0;
+    for (int r = 0; bm; ++r) {
+      const uint32_t lo = bm & (0u - bm);
+      bm ^= lo;
+      if ((r & (P - 1)) == part) bs |= lo;
+    }
+    compose_core32<SEMI, true>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], bs);
+    my_cand += F.ncand;
+    if (tr) {
+      atomicAdd(tr, F.ncand);
+      atomicMax(tr + 2, (uint32_t)((clock64() - c0) >> 4));
+    }
+    const int j = (pi * A + a) * P + part;
+    pacc[j] = SEMI == TILE_S_ADDMULT ? F.acc : (double)F.mx;
+    pabs[j] = F.aabs;
+    pcnt[j] = F.ncand;
+  }
+  if (!ns) return;
+  __syncthreads();
+  for (int it = t; it < ns * A; it += blockDim.x) {
+    const int pi = it / A, a = it - pi * A;
+    const int p = pairs[pi], x = p / Z, z = p - x * Z;
+    double s = 0.0, ab = 0.0;
+    float mx = 0.0f;
+    uint32_t n = 0;
+    for (int part = 0; part < P; ++part) {
+      const int j = it * P + part;
+      const uint32_t c = pcnt[j];
+      if (!c) continue;
+      if constexpr (SEMI == TILE_S_ADDMULT) {
+        s = __dadd_rn(s, pacc[j]);
+        ab = __dadd_rn(ab, pabs[j]);
+      } else if constexpr (SEMI == TILE_S_MAXMIN) {
+        const float v = (float)pacc[j];
+        mx = (n == 0 || v > mx) ? v : mx;
+      }
+      n += c;
+    }
+    if (!n) continue;
+    float u = mx;
+    if constexpr (SEMI == TILE_S_ADDMULT) {
+      const double d = (2.0 * (double)(n + P) + 4.0) * 0x1p-53 * ab * 1.01;
+      const float lo = __double2float_rn(__dsub_rn(s, d)), hi = __double2float_rn(__dadd_rn(s, d));
+      if (lo == hi && !F.Q->cm_nocert) {
+        u = lo;
+      } else {  // uncertified: the canonical sequential walk
+        F.acc = 0.0;
+        F.aabs = 0.0;
+        F.mx = 0.0f;
+        F.any = false;
+        F.ncand = 0;
+        compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
+        u = (float)F.acc;
+        if (tr) atomicAdd(tr + 1, 1u << 16);  // debug: fallbacks in the |Δ'| word's high half
+      }
+    }
+    const int h = a * H.stride[0] + x * H.stride[1] + z * H.stride[2];
+    atomicOr(Ub + (h >> 5), 1u << (h & 31));
+    if constexpr (SEMI != TILE_S_UNIT) Ut[h] = u;
+  }
+}
+
 // One recursive round of a stratum whose only recursive rule is the
 // composition shape (TilePlan::cm_rule): U of every head slot, evaluating
 // only the slots (a, x, z) whose pair (x, z) can receive a candidate:
@@ -398,7 +539,8 @@ __device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
 // only in the T fiber.  Per slot the enumeration is compose_core's: same
 // candidates, same canonical order, bit-identical U.
 template <int SEMI>
-__device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint8_t* sm, uint64_t& my_cand) {
+__device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint8_t* sm, uint64_t& my_cand,
+                                               uint32_t* tr) {
   const TileRule& R = TP(F).rule[Q.cm_rule];
   const TileRel& H = TP(F).rel[R.head];
   const int A = H.dom[0], X = H.dom[1], Z = H.dom[2];
@@ -473,9 +615,13 @@ __device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint
   __syncthreads();
   const int items = (int)npairs[0] * A;
   const bool narrow = A <= 32 && H.dom[1] <= 32 && H.dom[2] <= 32;  // 32-bit masks (K == H)
+  const int lane = t & 31;
+  if (narrow && !F.Q->cm_nosplit) {
+    compose_split<SEMI>(F, R, H, items, (uint8_t*)(pairs + X * Z), npairs, pairs, AX, my_cand, tr);
+    return;
+  }
   // warps claim 32 items at a time (items differ a lot in cost; a static
   // stride left warps waiting at the round's barrier)
-  const int lane = t & 31;
   for (;;) {
     int base = 0;
     if (lane == 0) base = (int)atomicAdd(npairs + 1, 32u);
@@ -489,11 +635,16 @@ __device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint
     F.mx = 0.0f;
     F.any = false;
     F.ncand = 0;
+    const long long c0 = tr ? clock64() : 0;
     if (narrow)
       compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
     else
       compose_core<SEMI>(F, R, a, x, z, SY[z], DY[z], BX[x]);
     my_cand += F.ncand;
+    if (tr) {  // debug (LOBSTER_TILE_TRACE): candidates, longest item (cycles / 16)
+      atomicAdd(tr, F.ncand);
+      atomicMax(tr + 2, (uint32_t)((clock64() - c0) >> 4));
+    }
     if (F.any) {
       const int h = a * H.stride[0] + x * H.stride[1] + z * H.stride[2];
       atomicOr(Ub + (h >> 5), 1u << (h & 31));
@@ -567,7 +718,9 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
       // (i) + (iii): U per head slot (staged in shared memory; keeping the u
       // values in registers instead, with eval_head out of line, measured
       // 23.2 ms vs 17.5 ms on C3 — and 19.3 ms at 64 registers / 2 CTAs per SM)
-      if (!seed && Q.cm_rule >= 0) compose_rounds<SEMI>(F, Q, sm, my_cand);
+      const long long ph0 = clock64();
+      if (!seed && Q.cm_rule >= 0)
+        compose_rounds<SEMI>(F, Q, sm, my_cand, Q.trace ? Q.trace + ((int64_t)s * 64 + min(round, 63)) * 4 : nullptr);
       else
       TILE_UNROLL
       for (int li = 0; li < TP(F).nlocal; ++li) {
@@ -584,7 +737,7 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
           F.ncand = 0;
           if (h < H.D) eval_head<SEMI, MAXL>(F, hr, h, seed);
           my_cand += F.ncand;
-          if (Q.trace && F.ncand) atomicAdd(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 2, F.ncand);
+          if (Q.trace && F.ncand) atomicAdd(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 4, F.ncand);
           const uint32_t word = __ballot_sync(~0u, F.any);
           if (lane == 0) Ub[w] = word;
           if constexpr (SEMI != TILE_S_UNIT) {
@@ -593,6 +746,8 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
         }
       }
       __syncthreads();
+      if (Q.trace && threadIdx.x == 0)  // debug: the U phase (cycles / 16)
+        atomicMax(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 4 + 3, (uint32_t)((clock64() - ph0) >> 4));
       // (ii) S <- S ⊕ Δ; (iv) Δ' = changed or new U
       int grew = 0;
       TILE_UNROLL
@@ -632,7 +787,7 @@ __device__ __forceinline__ void tile_body(const TilePlan& Q, uint8_t* sm, int* r
             Db[w] = dword;
           }
           grew |= nd;
-          if (Q.trace && nd) atomicAdd(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 2 + 1, 1u);
+          if (Q.trace && nd) atomicAdd(Q.trace + ((int64_t)s * 64 + min(round, 63)) * 4 + 1, 1u);
         }
       }
       __syncthreads();

@@ -224,3 +224,19 @@ def test_compacted_composition_rounds_identical(monkeypatch, sr):
     if sr != 0:
         assert np.array_equal(a.probs.view(np.uint32), b.probs.view(np.uint32))
     assert st["candidates"] == st2["candidates"] and st["rounds_total"] == st2["rounds_total"]
+
+
+def test_split_items_certified_rounding_equals_sequential(monkeypatch):
+    """Late composition rounds split each head item by b across threads and
+    combine the fp64 partial sums; the fp32 result is taken only when the
+    rounding is certified, else recomputed in canonical order.  Forcing the
+    sequential fallback for every split head gives bit-identical tags (and
+    both equal the oracle)."""
+    w = W.c3_workload(batch=24, samples=list(range(24)))
+    eng, st, _ = _check(w, ["kinship", "answer"], tiles=2, samples=[0, 7, 23])
+    a = eng.output("kinship")
+    monkeypatch.setenv("LOBSTER_TILE_NO_CERT", "1")
+    eng2, st2, _ = engine_run(w)
+    b = eng2.output("kinship")
+    assert np.array_equal(a.cols, b.cols) and np.array_equal(a.probs.view(np.uint32), b.probs.view(np.uint32))
+    assert st["candidates"] == st2["candidates"]
