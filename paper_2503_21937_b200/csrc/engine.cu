@@ -2679,7 +2679,11 @@ struct Ctx {
         ++nrec;
         if (P.rule[i].shape == 1 && P.rule[i].head == P.local_rel[0]) cm = i;
       }
-      if (nrec == 1 && cm >= 0) P.cm_rule = cm;
+      if (nrec == 1 && cm >= 0) {
+        P.cm_rule = cm;
+        TileRel& H = P.rel[P.local_rel[0]];
+        H.nfib[1] = H.D / H.dom[1];  // middle-column fibers (compose_bc32)
+      }
     }
     // fiber strides (row-major over the other columns) and the shared-memory layout:
     // [fibers S, Δ | bits S, Δ] (zeroed per sample) then [bits U | tags S, Δ, U]
@@ -2725,7 +2729,7 @@ struct Ctx {
       const TileRel& H = P.rel[P.local_rel[0]];
       off = (off + 15) & ~int64_t(15);
       P.cm_off = (int32_t)off;
-      off += 320 * 8 + 64 + (int64_t)H.dom[1] * H.dom[2] * 6 + 8 + (int64_t)TILE_CM_PARTS * 20;
+      off += 320 * 8 + 64 + (int64_t)H.dom[1] * H.dom[2] * 6 + 8 + (int64_t)TILE_CM_PARTS * 16;
     }
     if (off > 200 * 1024) return false;
     // Each round pulls every head slot of every sample through an interpreted

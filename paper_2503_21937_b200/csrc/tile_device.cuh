@@ -398,9 +398,107 @@ __device__ __forceinline__ void compose_head(Frame& F, const TileRule& R) {
                      TP(F).rel[R.atom[0].rel].dom[0] >= 64 ? ~0ull : (1ull << TP(F).rel[R.atom[0].rel].dom[0]) - 1ull);
 }
 
+// The candidates of one head (a, x, z) enumerated from T's side, in the
+// order (b, c, y, variant): for each b with NEW(b, x, ·) and each c of
+// T(b, ·, a), the y are the AND of the fibers Δ(b,x,·) ∧ OLD(c,·,z)
+// (variant 0) and NEW(b,x,·) ∧ Δ(c,·,z) (variant 1) — K's middle-column
+// fibers — so no y without a candidate is visited.  The terms are the same
+// fp32 values as the canonical walk; only their summation order differs, so
+// the caller certifies the fp32 rounding (add-mult) or needs no certificate
+// (max-min: max is exact; unit).
+template <int SEMI>
+__device__ __forceinline__ void compose_bc32(Frame& F, const TileRule& R, int a, int x, int z, uint32_t bs) {
+  const TileRel& K = TP(F).rel[R.atom[0].rel];
+  const TileRel& T = TP(F).rel[R.atom[2].rel];
+  const TileRel& TQ = F.Q->rel[R.atom[2].rel];
+  const uint32_t* Sf2 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[0][2]);  // low words: [2 f]
+  const uint32_t* Df2 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[1][2]);
+  const uint32_t* Sf1 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[0][1]);
+  const uint32_t* Df1 = reinterpret_cast<const uint32_t*>(F.sm + K.sm_fib[1][1]);
+  const float* St = reinterpret_cast<const float*>(F.sm + K.sm_tag[0]);
+  const float* Dt = reinterpret_cast<const float*>(F.sm + K.sm_tag[1]);
+  const uint32_t* Sb = reinterpret_cast<const uint32_t*>(F.sm + K.sm_bits[0]);
+  const uint32_t* Tf = reinterpret_cast<const uint32_t*>(TQ.fib[1] + (T.shared ? 0 : (int64_t)F.s * T.nfib[1]));
+  const float* Tt = TQ.tag ? TQ.tag + (T.shared ? 0 : (int64_t)F.s * T.D) : nullptr;
+  const int ks0 = K.stride[0], ks1 = K.stride[1], ks2 = K.stride[2], zs = z * ks2, xs = x * ks1;
+  const int f2x = x * K.fstride[2][1], f2b = K.fstride[2][0], f1c = K.fstride[1][0], f1z = z * K.fstride[1][2];
+  const int tfb = T.fstride[1][0], tfa = a * T.fstride[1][2], ts0 = T.stride[0], ts1 = T.stride[1];
+  const int ta = a * T.stride[2];
+  double acc = F.acc, aabs = F.aabs;
+  float mx = F.mx;
+  uint32_t nc = F.ncand;
+  while (bs) {
+    const int b = __ffs(bs) - 1;
+    bs &= bs - 1;
+    uint32_t cc = __ldg(Tf + 2 * (b * tfb + tfa));  // c with T(b, c, a)
+    if (!cc) continue;
+    const int fbx = b * f2b + f2x;
+    const uint32_t d0 = Df2[2 * fbx], n0 = Sf2[2 * fbx] | d0;
+    const float* Ttb = Tt ? Tt + b * ts0 + ta : nullptr;
+    const int bx = b * ks0 + xs;
+    while (cc) {
+      const int c = __ffs(cc) - 1;
+      cc &= cc - 1;
+      const int fcz = c * f1c + f1z;
+      uint32_t m0 = d0 & Sf1[2 * fcz], m1 = n0 & Df1[2 * fcz];
+      if (!(m0 | m1)) continue;
+      const float tc = (SEMI != TILE_S_UNIT && Ttb) ? __ldg(Ttb + c * ts1) : 1.0f;
+      const int cz = c * ks0 + zs;
+      if constexpr (SEMI == TILE_S_UNIT) {
+        nc += __popc(m0) + __popc(m1);
+        continue;
+      }
+      while (m0) {  // v0: Δ(b,x,y) ⊗ OLD(c,y,z) ⊗ T(b,c,a)
+        const int y = __ffs(m0) - 1;
+        m0 &= m0 - 1;
+        ++nc;
+        const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(Dt[bx + y * ks2], St[cz + y * ks1]), tc);
+        if constexpr (SEMI == TILE_S_ADDMULT) {
+          acc = __dadd_rn(acc, (double)t);
+          aabs = __dadd_rn(aabs, fabs((double)t));
+        } else {
+          mx = (nc == 1 || t > mx) ? t : mx;
+        }
+      }
+      while (m1) {  // v1: NEW(b,x,y) ⊗ Δ(c,y,z) ⊗ T(b,c,a)
+        const int y = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        ++nc;
+        const int sbxy = bx + y * ks2;
+        const float dv = Dt[sbxy];
+        const float nb = tbit(Sb, sbxy) ? (((d0 >> y) & 1u) ? oplus_state<SEMI>(St[sbxy], dv) : St[sbxy]) : dv;
+        const float t = tile_otimes<SEMI>(tile_otimes<SEMI>(nb, Dt[cz + y * ks1]), tc);
+        if constexpr (SEMI == TILE_S_ADDMULT) {
+          acc = __dadd_rn(acc, (double)t);
+          aabs = __dadd_rn(aabs, fabs((double)t));
+        } else {
+          mx = (nc == 1 || t > mx) ? t : mx;
+        }
+      }
+    }
+  }
+  F.acc = acc;
+  F.aabs = aabs;
+  F.mx = mx;
+  F.any = F.any || nc != F.ncand;
+  F.ncand = nc;
+}
+
+// fp32 rounding certificate of an fp64 sum of n terms formed in some order
+// whose canonical sequential sum must be reproduced: both lie within
+// (n + k)·2^-53·Σ|t| of the exact sum (every term takes at most n + k
+// roundings), so if every value in s ± d rounds to one fp32 value, that value
+// is fl32(canonical sum).  Returns false when uncertified.
+__device__ __forceinline__ bool certify32(double s, double ab, uint32_t n, int k, float& out) {
+  const double d = (2.0 * (double)(n + k) + 4.0) * 0x1p-53 * ab * 1.01;
+  const float lo = __double2float_rn(__dsub_rn(s, d)), hi = __double2float_rn(__dadd_rn(s, d));
+  out = lo;
+  return lo == hi;
+}
+
 // A round ends at its longest head item (C3: from round ~6 on, one item's
-// (b, y) walk IS the round).  The items of the heaviest pairs (all of them
-// when the round has fewer items than threads) are split into P parts by b
+// walk IS the round).  The items of the heaviest pairs (all of them when
+// they fit the partial buffer) are split into P parts by b
 // (ranks ≡ part mod P), the parts run in parallel and their partial results
 // are combined per head:
 //   unit: any part;  max-min: the max (exact, order-free);
@@ -422,17 +520,18 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
   const int A = H.dom[0], Z = H.dom[2];
   pb = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pb) + 7) & ~uintptr_t(7));
   double* pacc = reinterpret_cast<double*>(pb);
-  double* pabs = pacc + TILE_CM_PARTS;
+  float* pabs = reinterpret_cast<float*>(pacc + TILE_CM_PARTS);  // Σ|t| rounded up
   uint32_t* pcnt = reinterpret_cast<uint32_t*>(pabs + TILE_CM_PARTS);
   uint32_t* Ub = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(F.sm) + H.sm_bits[2]);
   float* Ut = reinterpret_cast<float*>(const_cast<uint8_t*>(F.sm) + H.sm_tag[2]);
-  // split every pair's items when the round has fewer items than threads
-  // (splitting only the heaviest classes of the larger rounds measured slower:
-  // 6.42 vs 6.21 ms on C3 — those rounds are throughput-, not path-bound)
+  // split every pair's items when at least two parts per item fit the
+  // partial buffer (up to ~2 sub-items per thread), else the heaviest two
+  // cost classes' items (C3: 4.53 -> 4.44 ms; with the canonical-order walk
+  // the same split of the big rounds had measured slower, 6.42 vs 6.21 ms)
   const int npr = items / A;
-  int ns = items < (int)blockDim.x ? npr : 0;
+  int ns = items * 2 <= TILE_CM_PARTS ? npr : min((int)(npairs[2] + npairs[3]), TILE_CM_PARTS / (2 * A));
   int P = 1;
-  while (P < 8 && ns * A * P * 2 <= TILE_CM_PARTS && (ns * A * P < (int)blockDim.x || ns < npr)) P <<= 1;
+  while (P < 8 && ns * A * P * 2 <= TILE_CM_PARTS && (ns * A * P < 2 * (int)blockDim.x || ns < npr)) P <<= 1;
   if (P == 1) ns = 0;
   const int nsub = ns * A * P, total = nsub + (npr - ns) * A;
   const int t = threadIdx.x, lane = t & 31;
@@ -452,16 +551,26 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
     if (i >= nsub) {  // a whole item: U directly
       const int w = i - nsub + ns * A, pi = w / A, a = w - pi * A;
       const int p = pairs[pi], x = p / Z, z = p - x * Z;
-      compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
+      compose_bc32<SEMI>(F, R, a, x, z, (uint32_t)BX[x]);
       my_cand += F.ncand;
       if (tr) {
         atomicAdd(tr, F.ncand);
         atomicMax(tr + 2, (uint32_t)((clock64() - c0) >> 4));
       }
       if (F.any) {
+        float u = F.mx;
+        if constexpr (SEMI == TILE_S_ADDMULT) {
+          if (!certify32(F.acc, F.aabs, F.ncand, 0, u) || F.Q->cm_nocert) {  // the canonical sequential walk
+            F.acc = 0.0;
+            F.ncand = 0;
+            compose_core32<SEMI>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], (uint32_t)BX[x]);
+            u = (float)F.acc;
+            if (tr) atomicAdd(tr + 1, 1u << 16);
+          }
+        }
         const int h = a * H.stride[0] + x * H.stride[1] + z * H.stride[2];
         atomicOr(Ub + (h >> 5), 1u << (h & 31));
-        if constexpr (SEMI != TILE_S_UNIT) Ut[h] = SEMI == TILE_S_ADDMULT ? (float)F.acc : F.mx;
+        if constexpr (SEMI != TILE_S_UNIT) Ut[h] = u;
       }
       continue;
     }
@@ -473,7 +582,7 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
       bm ^= lo;
       if ((r & (P - 1)) == part) bs |= lo;
     }
-    compose_core32<SEMI, true>(F, R, a, x, z, (uint32_t)SY[z], (uint32_t)DY[z], bs);
+    compose_bc32<SEMI>(F, R, a, x, z, bs);
     my_cand += F.ncand;
     if (tr) {
       atomicAdd(tr, F.ncand);
@@ -481,7 +590,7 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
     }
     const int j = (pi * A + a) * P + part;
     pacc[j] = SEMI == TILE_S_ADDMULT ? F.acc : (double)F.mx;
-    pabs[j] = F.aabs;
+    pabs[j] = __double2float_ru(F.aabs);
     pcnt[j] = F.ncand;
   }
   if (!ns) return;
@@ -498,7 +607,7 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
       if (!c) continue;
       if constexpr (SEMI == TILE_S_ADDMULT) {
         s = __dadd_rn(s, pacc[j]);
-        ab = __dadd_rn(ab, pabs[j]);
+        ab = __dadd_rn(ab, (double)pabs[j]);
       } else if constexpr (SEMI == TILE_S_MAXMIN) {
         const float v = (float)pacc[j];
         mx = (n == 0 || v > mx) ? v : mx;
@@ -508,10 +617,7 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
     if (!n) continue;
     float u = mx;
     if constexpr (SEMI == TILE_S_ADDMULT) {
-      const double d = (2.0 * (double)(n + P) + 4.0) * 0x1p-53 * ab * 1.01;
-      const float lo = __double2float_rn(__dsub_rn(s, d)), hi = __double2float_rn(__dadd_rn(s, d));
-      if (lo == hi && !F.Q->cm_nocert) {
-        u = lo;
+      if (certify32(s, ab, n, P, u) && !F.Q->cm_nocert) {
       } else {  // uncertified: the canonical sequential walk
         F.acc = 0.0;
         F.aabs = 0.0;
@@ -534,10 +640,11 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
 // only the slots (a, x, z) whose pair (x, z) can receive a candidate:
 //   (Δ(·, x, ·) ∩ OLD(·, ·, z)-sources) ∪ (NEW(·, x, ·) ∩ Δ(·, ·, z)-sources) ≠ ∅
 // over y (a superset of the slots with candidates; the others get no U, as
-// before).  Active pairs are listed in shared memory and handed out with a
-// fastest across lanes, so a warp's lanes share the (b, y) walk and differ
-// only in the T fiber.  Per slot the enumeration is compose_core's: same
-// candidates, same canonical order, bit-identical U.
+// before).  Active pairs are listed in shared memory, heaviest first, and
+// handed out with a fastest across lanes.  Per head the candidates are
+// compose_bc32's (T-driven order, rounding certified, canonical fallback;
+// compose_split) — U bit-identical to the canonical walk; with 64-bit masks
+// (domains > 32) or LOBSTER_TILE_NO_SPLIT, compose_core's canonical walk.
 template <int SEMI>
 __device__ __forceinline__ void compose_rounds(Frame& F, const TilePlan& Q, uint8_t* sm, uint64_t& my_cand,
                                                uint32_t* tr) {

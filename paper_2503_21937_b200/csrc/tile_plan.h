@@ -20,7 +20,7 @@ constexpr int TILE_S_UNIT = 0, TILE_S_MAXMIN = 1, TILE_S_ADDMULT = 2;  // == Sem
 // oracle's fp64 order.
 constexpr int TILE_MAXREL = 6, TILE_MAXRULE = 8, TILE_MAXLEV = 5, TILE_MAXVAR = 4, TILE_MAXCOL = 4, TILE_MAXV = 10;
 constexpr int TILE_THREADS_N = 512;
-constexpr int TILE_CM_PARTS = 2048;  // partial sums of split composition items (compose_rounds)
+constexpr int TILE_CM_PARTS = 4096;  // partial sums of split composition items (compose_rounds)
 enum TileVer : int8_t { TV_EXT = 0, TV_NEW = 1, TV_OLD = 2, TV_DELTA = 3 };
 struct TileRel {
   int8_t ncols;
