@@ -13,6 +13,7 @@
 // Probe / output keys are u32 or u64 (template PK / OK): relations whose
 // packed key fits 31 bits move half the key bytes.
 #include <algorithm>
+#include <cstring>
 #include <type_traits>
 
 #include "device_util.cuh"
@@ -802,6 +803,162 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
   if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
 }
 
+// 32-bit fast path of an aggregating lookup chain over a direct store (C2 /
+// C5 `endpoints_connected() :- is_endpoint(x), is_endpoint(y), path(x, y),
+// x != y`: every path slot probes two point lookups into a narrow head).  The
+// generic row (64-bit operands, move-list loops, run-time ⊗ order, a binary
+// search compiled in) spent ~500 thread instructions per probe row; here the
+// plan is pre-split on the host into 32-bit single-source move pairs, field
+// comparisons and a fixed ⊗ order.  Same filters, lookups, ⊗ order, witness
+// and head key as lookup_row.
+struct LOpnd32 {
+  uint32_t shift, mask;  // field = (pk >> shift) & mask (mask 0: constant)
+  int64_t base;          // field min or the constant
+};
+struct LFast32 {
+  int nlk, ncmp, ntag;
+  Mv32 pre[MAXL];
+  uint32_t cprefix[MAXL], nprefix[MAXL];
+  LOpnd32 ca[MAXC], cb[MAXC];
+  int8_t neq[MAXC];
+  int8_t tag_order[MAXT];
+  Mv32 out, wm;
+  uint32_t cout, wconst;
+};
+
+__device__ __forceinline__ int64_t lopnd(const LOpnd32& o, uint32_t pk) {
+  return (int64_t)((pk >> o.shift) & o.mask) + o.base;
+}
+
+template <int SEMI>
+__global__ void __launch_bounds__(256) lookup_agg32_k(const LookupPlan lp, const LFast32 f,
+                                                      unsigned long long* __restrict__ ncand) {
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t chunk = ((lp.np + nwarps - 1) / nwarps + 31) & ~(int64_t)31;
+  const int64_t r0 = wid * chunk, r1 = r0 + chunk < lp.np ? r0 + chunk : lp.np;
+  uint32_t mycount = 0, cur = 0xffffffffu;
+  unsigned long long run = 0;
+  for (int64_t base = r0; base < r1; base += 32) {
+    const int64_t i = base + (threadIdx.x & 31);
+    const uint32_t pk = (uint32_t)i;
+    bool ok = i < r1;
+    float tags[MAXL + 1];
+    tags[0] = 1.0f;
+    if (ok) {
+      if (SEMI == S_UNIT) {
+        ok = (reinterpret_cast<const uint32_t*>(lp.pdir)[i >> 5] >> (i & 31)) & 1u;
+      } else if (SEMI == S_MAXMIN) {
+        const uint32_t v = reinterpret_cast<const uint32_t*>(lp.pdir)[i];
+        ok = v != 0u;
+        tags[0] = mm_p(v);
+      } else {
+        const unsigned long long v = reinterpret_cast<const unsigned long long*>(lp.pdir)[i];
+        ok = v != 0ull;
+        tags[0] = mx_p(v);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < f.ncmp) ok = ok && cmp_holds(f.neq[c], lopnd(f.ca[c], pk), lopnd(f.cb[c], pk));
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) {
+      tags[l + 1] = 1.0f;
+      if (l >= f.nlk || !ok) continue;
+      const uint32_t pre = f.cprefix[l] | mv32(f.pre[l], pk);
+      if (pre >= f.nprefix[l]) {
+        ok = false;
+        continue;
+      }
+      const int64_t b0 = __ldg(lp.lk[l].boff + pre), b1 = __ldg(lp.lk[l].boff + pre + 1);
+      ok = b1 > b0;
+      if (ok && SEMI != S_UNIT && lp.lk[l].btag) tags[l + 1] = __ldg(lp.lk[l].btag + b0);
+    }
+    float t = 1.0f;
+    uint32_t w = 0;
+    if (ok && SEMI != S_UNIT) {
+      auto pick = [&](int idx) {
+        float r = tags[0];
+#pragma unroll
+        for (int k = 1; k <= MAXL; ++k)
+          if (k == idx) r = tags[k];
+        return r;
+      };
+      t = pick(f.tag_order[0]);
+#pragma unroll
+      for (int k = 1; k < MAXT; ++k)
+        if (k < f.ntag) t = otimes(lp.omin ? S_MAXMIN : SEMI, t, pick(f.tag_order[k]));
+      if (SEMI == S_MAXMULT) w = f.wconst | mv32(f.wm, pk);
+    }
+    if (ok) ++mycount;
+    const uint32_t slot = f.cout | mv32(f.out, pk);
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (!act) continue;
+    const uint32_t s0 = __shfl_sync(0xffffffffu, slot, __ffs(act) - 1);
+    const bool uniform = __all_sync(0xffffffffu, !ok || slot == s0);
+    if (uniform && s0 == cur) {
+      const unsigned long long v = ok ? agg_pack<SEMI>(t, w, lp.mx) : 0ull;
+      run = v > run ? v : run;
+      continue;
+    }
+    if (cur != 0xffffffffu) agg_flush<SEMI>(lp.fdir, lp.dirty, cur, run);
+    run = 0;
+    cur = 0xffffffffu;
+    if (uniform) {
+      cur = s0;
+      run = ok ? agg_pack<SEMI>(t, w, lp.mx) : 0ull;
+    } else if (ok) {
+      direct_oplus(SEMI, lp.fdir, slot, t, w, lp.dirty, 1, lp.mx);
+    }
+  }
+  if (cur != 0xffffffffu) agg_flush<SEMI>(lp.fdir, lp.dirty, cur, run);
+  mycount = __reduce_add_sync(0xffffffffu, mycount);
+  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+}
+
+// host: the 32-bit plan, or false (then the generic kernel runs)
+static bool split_src0_32(const Move* mv, int n, Mv32& a) {
+  Mv32 b;
+  for (int i = 0; i < n; ++i)
+    if (mv[i].src != 0) return false;
+  return split_moves32(mv, n, a, b);
+}
+static bool lookup_fast32_plan(const LookupPlan& lp, LFast32& f) {
+  if (!lp.pdir || !lp.direct || !lp.aggregate || lp.np > 0xffffffffll || lp.cout >> 32) return false;
+  if (lp.nlk > MAXL || lp.ncmp > MAXC || lp.ntag > MAXT || lp.ntag < 1) return false;
+  std::memset(&f, 0, sizeof(f));
+  f.nlk = lp.nlk;
+  f.ncmp = lp.ncmp;
+  f.ntag = lp.ntag;
+  for (int l = 0; l < lp.nlk; ++l) {
+    const Lookup& L = lp.lk[l];
+    if (!L.boff || L.cprefix >> 32 || L.nprefix > 0xffffffffll || !split_src0_32(L.prem, L.nprem, f.pre[l]))
+      return false;
+    f.cprefix[l] = (uint32_t)L.cprefix;
+    f.nprefix[l] = (uint32_t)L.nprefix;
+  }
+  for (int c = 0; c < lp.ncmp; ++c) {
+    const Operand* o[2] = {&lp.cmp[c].a, &lp.cmp[c].b};
+    LOpnd32* d[2] = {&f.ca[c], &f.cb[c]};
+    for (int k = 0; k < 2; ++k) {
+      if (o[k]->src == 1) return false;
+      if (o[k]->src == 2) {
+        *d[k] = LOpnd32{0, 0, (int64_t)o[k]->base};
+      } else {
+        if (o[k]->shift + o[k]->bits > 32) return false;
+        *d[k] = LOpnd32{o[k]->shift, o[k]->bits >= 32 ? 0xffffffffu : ((1u << o[k]->bits) - 1u), (int64_t)o[k]->base};
+      }
+    }
+    f.neq[c] = lp.cmp[c].neq;
+  }
+  for (int k = 0; k < lp.ntag; ++k) f.tag_order[k] = lp.tag_order[k];
+  if (!split_src0_32(lp.om, lp.nom, f.out)) return false;
+  f.cout = (uint32_t)lp.cout;
+  if (lp.semi == S_MAXMULT && !split_src0_32(lp.wm, lp.nwm, f.wm)) return false;
+  f.wconst = lp.wconst;
+  return true;
+}
+
 struct MoveList {
   Move m[MAXM];
   int n;
@@ -926,6 +1083,16 @@ void launch_lookup_chain(const LookupPlan& lp, unsigned long long* ncand, cudaSt
   if (lp.np <= 0) return;
   const int g = grid_for(lp.np, 256);
   note_launch();
+  static const bool fast_off = getenv("LOBSTER_LOOKUP_FAST32") && atoi(getenv("LOBSTER_LOOKUP_FAST32")) == 0;
+  LFast32 f;
+  if (!fast_off && lookup_fast32_plan(lp, f)) {
+    switch (lp.semi) {
+      case S_UNIT: lookup_agg32_k<S_UNIT><<<g, 256, 0, st>>>(lp, f, ncand); break;
+      case S_MAXMIN: lookup_agg32_k<S_MAXMIN><<<g, 256, 0, st>>>(lp, f, ncand); break;
+      default: lookup_agg32_k<S_MAXMULT><<<g, 256, 0, st>>>(lp, f, ncand); break;
+    }
+    return;
+  }
   if (lp.pk32 && lp.ok32) launch_lookup_chain_t<uint32_t, uint32_t>(lp, ncand, g, st);
   else if (lp.pk32) launch_lookup_chain_t<uint32_t, uint64_t>(lp, ncand, g, st);
   else if (lp.ok32) launch_lookup_chain_t<uint64_t, uint32_t>(lp, ncand, g, st);
