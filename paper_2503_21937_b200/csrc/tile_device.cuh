@@ -589,6 +589,7 @@ __device__ __forceinline__ void compose_split(Frame& F, const TileRule& R, const
       atomicMax(tr + 2, (uint32_t)((clock64() - c0) >> 4));
     }
     const int j = (pi * A + a) * P + part;
+    if (j >= TILE_CM_PARTS) __trap();  // bounds guard (compute-sanitizer is unavailable on the GPU pool)
     pacc[j] = SEMI == TILE_S_ADDMULT ? F.acc : (double)F.mx;
     pabs[j] = __double2float_ru(F.aabs);
     pcnt[j] = F.ncand;

@@ -240,3 +240,11 @@ def test_split_items_certified_rounding_equals_sequential(monkeypatch):
     b = eng2.output("kinship")
     assert np.array_equal(a.cols, b.cols) and np.array_equal(a.probs.view(np.uint32), b.probs.view(np.uint32))
     assert st["candidates"] == st2["candidates"]
+
+
+@pytest.mark.parametrize("entities,rtypes", [(36, 4), (6, 40)])
+def test_composition_rounds_wide_domains(entities, rtypes):
+    """Entity or relation-type domains above 32: the composition rounds take
+    the 64-bit canonical walk (no 32-bit masks, no split); still bit-exact."""
+    w = W.c3_workload(batch=3, entities=entities, rtypes=rtypes, skips=6, ncomp=min(rtypes * rtypes, 60))
+    _check(w, ["kinship", "answer"], tiles=2)
