@@ -109,40 +109,64 @@ __global__ void slice_to_bitmap_k(const uint32_t* __restrict__ Rb, int tbits, in
   }
 }
 
-// Δ' extraction: one warp per dirty-bitmap word, one lane per word slot.
-// d = Nb & ~Rb; Rb |= d; Nb = 0; nonzero d -> Δ' entry (t, wi, d).
-__global__ void slice_extract_k(uint32_t* __restrict__ dirty, int64_t ndw, uint32_t* __restrict__ Nb,
-                                uint32_t* __restrict__ Rb, int W, uint32_t* __restrict__ dt, uint32_t* __restrict__ dwi,
-                                uint32_t* __restrict__ dbits, uint32_t* __restrict__ count,
-                                unsigned long long* __restrict__ tuples) {
-  const int lane = threadIdx.x & 31;
+// Δ' extraction: a CTA takes 32 dirty-bitmap words per step (4 per warp, one
+// lane per word slot).  d = Nb & ~Rb; Rb |= d; Nb = 0; nonzero d -> Δ' entry
+// (t, wi, d).  Positions come from ONE global atomic per CTA step (a per-warp
+// atomic on the single counter serialised in L2: 81 µs per C4 round).
+constexpr int SX_WPW = 4;  // dirty words per warp per step
+__global__ void __launch_bounds__(256) slice_extract_k(uint32_t* __restrict__ dirty, int64_t ndw,
+                                                       uint32_t* __restrict__ Nb, uint32_t* __restrict__ Rb, int W,
+                                                       uint32_t* __restrict__ dt, uint32_t* __restrict__ dwi,
+                                                       uint32_t* __restrict__ dbits, uint32_t* __restrict__ count,
+                                                       unsigned long long* __restrict__ tuples) {
+  __shared__ uint32_t wcnt[8], wpre[8], cbase;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long mytup = 0;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ndw;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const uint32_t m = dirty[q];
-    if (!m) continue;
-    const int64_t idx = q * 32 + lane;
-    uint32_t d = 0;
-    if ((m >> lane) & 1u) {
-      const uint32_t r = Rb[idx];
-      d = Nb[idx] & ~r;
-      Nb[idx] = 0;
-      if (d) Rb[idx] = r | d;
+  const int64_t per = (int64_t)(blockDim.x >> 5) * SX_WPW;
+  for (int64_t q0 = (int64_t)blockIdx.x * per; q0 < ndw; q0 += (int64_t)gridDim.x * per) {
+    uint32_t d[SX_WPW], act[SX_WPW];
+    int64_t idxv[SX_WPW];
+    uint32_t n = 0;
+#pragma unroll
+    for (int j = 0; j < SX_WPW; ++j) {
+      const int64_t q = q0 + (int64_t)warp * SX_WPW + j;
+      const uint32_t m = q < ndw ? dirty[q] : 0u;
+      idxv[j] = q * 32 + lane;
+      d[j] = 0;
+      if ((m >> lane) & 1u) {
+        const uint32_t r = Rb[idxv[j]];
+        d[j] = Nb[idxv[j]] & ~r;
+        Nb[idxv[j]] = 0;
+        if (d[j]) Rb[idxv[j]] = r | d[j];
+      }
+      act[j] = __ballot_sync(0xffffffffu, d[j] != 0);
+      if (lane == 0 && m) dirty[q] = 0;
+      n += __popc(act[j]);
     }
-    const uint32_t act = __ballot_sync(0xffffffffu, d != 0);
-    uint32_t base = 0;
-    if (lane == 0) {
-      dirty[q] = 0;
-      if (act) base = atomicAdd(count, (uint32_t)__popc(act));
+    if (lane == 0) wcnt[warp] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        wpre[w] = t;
+        t += wcnt[w];
+      }
+      cbase = t ? atomicAdd(count, t) : 0u;
     }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (d) {
-      const uint32_t pos = base + __popc(act & ((1u << lane) - 1u));
-      dt[pos] = (uint32_t)(idx / W);
-      dwi[pos] = (uint32_t)(idx % W);
-      dbits[pos] = d;
-      mytup += (unsigned long long)__popc(d);
+    __syncthreads();
+    uint32_t base = cbase + wpre[warp];
+#pragma unroll
+    for (int j = 0; j < SX_WPW; ++j) {
+      if (d[j]) {
+        const uint32_t pos = base + __popc(act[j] & ((1u << lane) - 1u));
+        dt[pos] = (uint32_t)(idxv[j] / W);
+        dwi[pos] = (uint32_t)(idxv[j] % W);
+        dbits[pos] = d[j];
+        mytup += (unsigned long long)__popc(d[j]);
+      }
+      base += __popc(act[j]);
     }
+    __syncthreads();  // wcnt / wpre / cbase are rewritten by the next step
   }
   mytup = __reduce_add_sync(0xffffffffu, (uint32_t)mytup);
   if (lane == 0 && mytup) atomicAdd(tuples, mytup);
@@ -248,7 +272,7 @@ void launch_slice_to_bitmap(const uint32_t* Rb, int tbits, int B, int64_t T, int
 void launch_slice_extract(uint32_t* dirty, int64_t ndw, uint32_t* Nb, uint32_t* Rb, int W, uint32_t* dt, uint32_t* dwi,
                           uint32_t* dbits, uint32_t* count, unsigned long long* tuples, cudaStream_t st) {
   note_launch();
-  slice_extract_k<<<grid_for(ndw * 32, 256), 256, 0, st>>>(dirty, ndw, Nb, Rb, W, dt, dwi, dbits, count, tuples);
+  slice_extract_k<<<grid_for(ndw, 8 * SX_WPW, 148 * 16), 256, 0, st>>>(dirty, ndw, Nb, Rb, W, dt, dwi, dbits, count, tuples);
 }
 
 void launch_slice_deg(const uint32_t* dt, int64_t nd, const uint32_t* off, uint32_t* deg, cudaStream_t st) {
