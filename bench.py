@@ -529,6 +529,14 @@ def main():
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": None, "kernel": "fixpoint phases (SURVEY §8(d) B_alg / summed phase time)",
                     "peak_source": peak_src}
+        # the same phases under SURVEY §8(d)'s per-candidate model (|Δ|·r + 2|C|·r): what a
+        # candidate-materialising join would have to move; the bit-sliced (C4) and tile (C1, C3)
+        # kernels process many candidates per word / in shared memory, so this can exceed 1
+        b8 = sum(s["tuples_derived"] * s["fj_row_bytes"] + 2 * s["candidates"] * s["fj_row_bytes"]
+                 for s in rf_stats[-1])
+        roofline["per_candidate_model"] = {"achieved": b8 / t_alg / 1e9, "frac": b8 / t_alg / 1e9 / peak,
+                                           "def": "(Σ tuples·r + 2·candidates·r) / summed phase time, "
+                                                  "r = 4 B key + tag bytes"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if part else "weak",
