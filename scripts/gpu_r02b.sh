@@ -23,6 +23,8 @@ c2plog) LOBSTER_LOG=1 timeout 600 python scripts/profile_cfg.py C2P 2 > gpurun_o
 c4) timeout 900 python -m pytest tests/test_gpu_slice.py -x -q > gpurun_out/slice.log 2>&1; tail -2 gpurun_out/slice.log
     timeout 600 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; tail -1 gpurun_out/bench_C4.err; cut -c1-200 gpurun_out/bench_C4.json
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C4.csv python scripts/profile_cfg.py C4 1 > /dev/null 2>&1; python scripts/launches.py gpurun_out/launches_C4.csv 6 ;;
+l2w) for v in 1 0 1 0; do LOBSTER_L2_WINDOW=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C2_l2w$v.json 2> gpurun_out/bench_C2_l2w$v.err; echo "l2w=$v $(cut -c1-140 gpurun_out/bench_C2_l2w$v.json)"; done
+     for v in 1 0; do LOBSTER_L2_WINDOW=$v timeout 600 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5_l2w$v.json 2>/dev/null; echo "C5 l2w=$v $(cut -c1-140 gpurun_out/bench_C5_l2w$v.json)"; done ;;
 c1log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 5 > gpurun_out/c1log.txt 2>&1; tail -30 gpurun_out/c1log.txt ;;
 c3log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C3 3 > gpurun_out/c3log.txt 2>&1; tail -12 gpurun_out/c3log.txt ;;
 c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 2 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
