@@ -524,7 +524,12 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   __shared__ uint32_t wpre[8];
   __shared__ uint32_t s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tile = blockIdx.x;
+  // ATOMIC: grid-stride over tiles (the launcher caps the grid) with ONE
+  // claim atomic per CTA tile and one completion atomic per CTA: per-warp
+  // claims plus a completion atomic from each of C2's 4096 CTAs serialised on
+  // the two counters (a ~12 µs floor per round even when Δ' is tiny)
+  const int64_t ntiles = ATOMIC ? (nw + 256 * WPT - 1) / (256 * WPT) : (int64_t)gridDim.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   const int64_t w0 = tile * (256 * WPT) + (int64_t)warp * (32 * WPT);
   uint32_t m[WPT];
   uint32_t c = 0;
@@ -537,27 +542,18 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   const uint32_t wsum = __reduce_add_sync(0xffffffffu, c);
   uint32_t base;
   if constexpr (ATOMIC) {
-    uint32_t wb = 0;
-    if (lane == 0 && wsum) wb = atomicAdd(ctr, wsum);
-    base = __shfl_sync(0xffffffffu, wb, 0);
-    // |Δ'| is final once every CTA has claimed (writes may still be in flight:
-    // the next kernel is stream-ordered after them), so the last CTA to claim
-    // publishes it and resets the counters — no barrier at the end of the work
+    if (lane == 0) wtot[warp] = wsum;
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
-        __threadfence();
-        const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctr);
-        *total = n;
-        ctr[0] = 0u;
-        ctr[1] = 0u;
-        if (ring) {  // zero-copy report to the host (async rounds)
-          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | n;
-          __threadfence_system();
-        }
+      uint32_t t = 0;
+      for (int k = 0; k < 8; ++k) {
+        wpre[k] = t;
+        t += wtot[k];
       }
+      s_base = t ? atomicAdd(ctr, t) : 0u;
     }
+    __syncthreads();
+    base = s_base + wpre[warp];
   } else {
   // tile base: groups before this tile's group + this group's earlier tiles
   const int64_t grp = tile / LB_GROUP;
@@ -663,6 +659,27 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
       }
     }
     base += tot;
+  }
+  __syncthreads();  // wtot / wpre / s_base are rewritten by the next tile
+  }
+  if constexpr (ATOMIC) {
+    // |Δ'| is final once every CTA has claimed (writes may still be in flight:
+    // the next kernel is stream-ordered after them), so the last CTA to finish
+    // claiming publishes it and resets the counters
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const uint32_t n = *reinterpret_cast<volatile uint32_t*>(ctr);
+        *total = n;
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+        if (ring) {  // zero-copy report to the host (async rounds)
+          *reinterpret_cast<volatile unsigned long long*>(ring) = ((unsigned long long)seq << 32) | n;
+          __threadfence_system();
+        }
+      }
+    }
   }
 }
 
@@ -878,6 +895,16 @@ int64_t direct_extract2_scratch(int64_t nwords) {
   const int64_t nt = (nwords + LB_TILE - 1) / LB_TILE;
   return nt + (nt + LB_GROUP - 1) / LB_GROUP;
 }
+// LOBSTER_EX_CTAS: CTAs per SM of the atomic extraction's grid (A/B; default 8)
+static int ex_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("LOBSTER_EX_CTAS");
+    const int x = e ? atoi(e) : 8;
+    return x < 1 ? 1 : (x > 64 ? 64 : x);
+  }();
+  return v;
+}
+
 void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, uint32_t* dkey, float* dp,
                             uint32_t* dw, uint32_t* scratch, uint32_t* total, unsigned long long restamp,
                             unsigned long long wmask, unsigned long long* ring, uint32_t seq, uint32_t* ctr,
@@ -902,7 +929,11 @@ void launch_direct_extract2(void* f, uint32_t* dirty, int64_t nwords, int semi, 
     const char* e = getenv("LOBSTER_EX_WPT");
     return (e && atoi(e) == 4) ? 4 : 2;
   }();
-  const unsigned g = (unsigned)(small ? (nwords + 256 * swpt - 1) / (256 * swpt) : nt);
+  // ATOMIC on C2-sized bitmaps: a grid-stride grid of at most 148 x 8 CTAs (one
+  // completion atomic each; C2 23.9 -> 23.1 ms).  Larger bitmaps keep one CTA
+  // per tile of 8 words per lane: capping C5's 16k tiles measured +9%.
+  const int64_t tiles = small ? (nwords + 256 * swpt - 1) / (256 * swpt) : nt;
+  const unsigned g = (unsigned)(small ? std::min<int64_t>(tiles, 148 * ex_ctas_per_sm()) : tiles);
 #define LOB_EX(S, A, W) direct_extract2_k<S, A, W><<<g, 256, 0, st>>>(f, dirty, nwords, dkey, dp, dw, tcnt, gsum, \
                                                                   total, restamp, wmask, ring, seq, ctr)
 #define LOB_EXS(S) if (!ctr) LOB_EX(S, false, LB_WPT); else if (small && swpt == 2) LOB_EX(S, true, 2); \

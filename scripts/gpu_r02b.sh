@@ -25,6 +25,13 @@ c4) timeout 900 python -m pytest tests/test_gpu_slice.py -x -q > gpurun_out/slic
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C4.csv python scripts/profile_cfg.py C4 1 > /dev/null 2>&1; python scripts/launches.py gpurun_out/launches_C4.csv 6 ;;
 l2w) for v in 1 0 1 0; do LOBSTER_L2_WINDOW=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C2_l2w$v.json 2> gpurun_out/bench_C2_l2w$v.err; echo "l2w=$v $(cut -c1-140 gpurun_out/bench_C2_l2w$v.json)"; done
      for v in 1 0; do LOBSTER_L2_WINDOW=$v timeout 600 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5_l2w$v.json 2>/dev/null; echo "C5 l2w=$v $(cut -c1-140 gpurun_out/bench_C5_l2w$v.json)"; done ;;
+ex) timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_deep.py tests/test_gpu_slice.py tests/test_gpu_microbatch.py -x -q > gpurun_out/ex_tests.log 2>&1; tail -2 gpurun_out/ex_tests.log
+    for v in 8 4 16; do LOBSTER_EX_CTAS=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C2_ex$v.json 2>/dev/null; echo "ex=$v $(cut -c1-140 gpurun_out/bench_C2_ex$v.json)"; done
+    LOBSTER_EX_CTAS=8 timeout 600 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5_ex.json 2>/dev/null; echo "C5 $(cut -c1-140 gpurun_out/bench_C5_ex.json)"
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2e.csv python scripts/profile_c2.py 1,3 > /dev/null 2>&1; python scripts/launches.py gpurun_out/launches_c2e.csv 6 ;;
+ex2) for v in 8 64 8 64; do LOBSTER_EX_CTAS=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C2_ex$v.json 2>/dev/null; echo "ex=$v $(cut -c1-140 gpurun_out/bench_C2_ex$v.json)"; done
+    timeout 600 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5_ex.json 2>/dev/null; echo "C5 $(cut -c1-140 gpurun_out/bench_C5_ex.json)"
+    timeout 600 python bench.py --config SG --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_SG_ex.json 2>/dev/null; echo "SG $(cut -c1-140 gpurun_out/bench_SG_ex.json)" ;;
 c1log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 5 > gpurun_out/c1log.txt 2>&1; tail -30 gpurun_out/c1log.txt ;;
 c3log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C3 3 > gpurun_out/c3log.txt 2>&1; tail -12 gpurun_out/c3log.txt ;;
 c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 2 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
