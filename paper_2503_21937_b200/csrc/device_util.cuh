@@ -238,6 +238,21 @@ __device__ __forceinline__ void direct_commit(int semi, void* f, uint32_t* dirty
   }
 }
 
+// Per-CTA candidate count -> one global atomic per CTA (blockDim <= 1024, every
+// thread of the CTA calls it at the end of the kernel).  Per-warp atomics on
+// the single counter (~6k per fused-join launch) serialised in L2 at the tail.
+__device__ __forceinline__ void cta_count_add(unsigned long long* ctr, uint32_t mine) {
+  __shared__ uint32_t s_cnt[32];
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_cnt[w];
+    if (t) atomicAdd(ctr, t);
+  }
+}
+
 inline int grid_for(int64_t n, int threads, int cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;

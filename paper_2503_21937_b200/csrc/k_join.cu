@@ -466,8 +466,7 @@ __global__ void __launch_bounds__(256, (MAXDEG <= 4) ? (SEMI == S_MAXMULT ? FJ_M
       atomicOr(jp.dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
     }
   }
-  mycount = __reduce_add_sync(0xffffffffu, mycount);
-  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+  cta_count_add(ncand, mycount);
 }
 
 // 32-bit fast path of the fused join (the C2 / C5 hot kernel): probe keys,
@@ -570,8 +569,7 @@ __global__ void __launch_bounds__(256, SEMI == S_MAXMULT ? FJ_MINB_MX : FJ_MINB)
       atomicOr(dirty + (slotv[d] >> 5), 1u << (slotv[d] & 31u));
     }
   }
-  mycount = __reduce_add_sync(0xffffffffu, mycount);
-  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+  cta_count_add(ncand, mycount);
 }
 
 // host: split a move list by source into two 32-bit move pairs; false when a
@@ -799,8 +797,7 @@ __global__ void __launch_bounds__(256) lookup_chain_k(const LookupPlan lp, unsig
       }
     }
   }
-  mycount = __reduce_add_sync(0xffffffffu, mycount);
-  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+  cta_count_add(ncand, mycount);
 }
 
 // (ncu of this kernel on C2: 0.57 ms per fixpoint, issue-bound — 71% issue
@@ -915,8 +912,7 @@ __global__ void __launch_bounds__(256) lookup_agg32_k(const LookupPlan lp, const
     }
   }
   if (cur != 0xffffffffu) agg_flush<SEMI>(lp.fdir, lp.dirty, cur, run);
-  mycount = __reduce_add_sync(0xffffffffu, mycount);
-  if ((threadIdx.x & 31) == 0 && mycount) atomicAdd(ncand, (unsigned long long)mycount);
+  cta_count_add(ncand, mycount);
 }
 
 // host: the 32-bit plan, or false (then the generic kernel runs)

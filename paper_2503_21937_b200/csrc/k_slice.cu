@@ -168,8 +168,7 @@ __global__ void __launch_bounds__(256) slice_extract_k(uint32_t* __restrict__ di
     }
     __syncthreads();  // wcnt / wpre / cbase are rewritten by the next step
   }
-  mytup = __reduce_add_sync(0xffffffffu, (uint32_t)mytup);
-  if (lane == 0 && mytup) atomicAdd(tuples, mytup);
+  cta_count_add(tuples, (uint32_t)mytup);
 }
 
 __global__ void slice_deg_k(const uint32_t* __restrict__ dt, int64_t nd, const uint32_t* __restrict__ off,
@@ -225,8 +224,7 @@ __global__ void __launch_bounds__(256) slice_expand_k(const uint32_t* __restrict
       atomicOr(dirty + (idx >> 5), 1u << (idx & 31));
     }
   }
-  mycand = __reduce_add_sync(0xffffffffu, (uint32_t)mycand);
-  if ((threadIdx.x & 31) == 0 && mycand) atomicAdd(cands, mycand);
+  cta_count_add(cands, (uint32_t)mycand);
 }
 
 __global__ void add_u32_dev_k(uint32_t* dst, const uint32_t* src, int assign) {
