@@ -1872,16 +1872,10 @@ struct Ctx {
     }
     batch_cur = B;
     if (micro) finalize_collected();
-    {  // the three device counters in one read
-      cuda_check(cudaMemcpyAsync(hbuf, d_ncand, 24, cudaMemcpyDeviceToHost, st), "D2H");
-      sync();
-      const unsigned long long* c = reinterpret_cast<const unsigned long long*>(hbuf);
-      stats.fj_timed_candidates = (int64_t)c[2];
-      stats.fj_candidates = (int64_t)c[1] + stats.fj_timed_candidates;
-      stats.candidates += (int64_t)c[0] + stats.fj_candidates;
-    }
+    // the three device counters in one read, landing with finish_run's sync
+    cuda_check(cudaMemcpyAsync(hbuf, d_ncand, 24, cudaMemcpyDeviceToHost, st), "D2H");
     stats.fj_row_bytes = 4 + (semi == S_UNIT ? 0 : (semi == S_MAXMULT ? 8 : 4));
-    finish_run(t0, round_cap_hit, out);
+    finish_run(t0, round_cap_hit, out, true);
   }
 
   // largest power-of-two sample range whose dense-eligible relations fit 30 bits
@@ -3008,10 +3002,16 @@ struct Ctx {
     return round_cap_hit;
   }
 
-  void finish_run(cudaEvent_t t0, int64_t round_cap_hit, lobster_run_stats* out) {
+  void finish_run(cudaEvent_t t0, int64_t round_cap_hit, lobster_run_stats* out, bool counters = false) {
     cudaEvent_t t1 = get_event();
     cudaEventRecord(t1, st);
     sync();
+    if (counters) {  // run(): d_ncand was copied to hbuf before t1
+      const unsigned long long* c = reinterpret_cast<const unsigned long long*>(hbuf);
+      stats.fj_timed_candidates = (int64_t)c[2];
+      stats.fj_candidates = (int64_t)c[1] + stats.fj_timed_candidates;
+      stats.candidates += (int64_t)c[0] + stats.fj_candidates;
+    }
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
     stats.ms_total = ms;

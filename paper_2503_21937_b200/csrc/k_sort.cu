@@ -98,9 +98,39 @@ __global__ void __launch_bounds__(NT) radix_scatter_k(const K* __restrict__ kin,
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Tiny inputs (C1-sized relations): one CTA ranks every key against all others
+// on the same low bits the LSD passes would sort, ties by index — the same
+// stable permutation as the passes, in one launch instead of ~5 per 8-bit
+// pass (hist, scan, scatter).
+constexpr int SMALL_SORT = 256;
+template <typename K, typename V, bool HASV>
+__global__ void __launch_bounds__(SMALL_SORT) radix_small_k(const K* __restrict__ ki, const V* __restrict__ vi,
+                                                            K* __restrict__ ko, V* __restrict__ vo, int n, K mask) {
+  __shared__ K sk[SMALL_SORT];
+  const int i = threadIdx.x;
+  if (i < n) sk[i] = ki[i] & mask;
+  __syncthreads();
+  if (i >= n) return;
+  const K x = sk[i];
+  int r = 0;
+  for (int j = 0; j < n; ++j) {
+    const K y = sk[j];
+    r += (y < x) || (y == x && j < i);
+  }
+  ko[r] = ki[i];
+  if (HASV) vo[r] = vi[i];
+}
+
 template <typename K, typename V, bool HASV>
 int radix_sort_impl(K* k0, V* v0, K* k1, V* v1, int64_t n, int bits, void* tmp, cudaStream_t st) {
   if (n <= 1 || bits <= 0) return 0;
+  if (n <= SMALL_SORT) {
+    const int sb = ((bits + 7) / 8) * 8;  // the bits the passes would sort
+    const K mask = sb >= (int)(8 * sizeof(K)) ? ~K(0) : (K)((K(1) << sb) - 1);
+    note_launch();
+    radix_small_k<K, V, HASV><<<1, SMALL_SORT, 0, st>>>(k0, v0, k1, v1, (int)n, mask);
+    return 1;
+  }
   const int64_t ntiles = (n + TILE - 1) / TILE;
   uint32_t* hist = reinterpret_cast<uint32_t*>(tmp);
   void* stmp = reinterpret_cast<char*>(tmp) + align_up((size_t)ntiles * 256 * sizeof(uint32_t));
