@@ -342,7 +342,9 @@ __device__ __forceinline__ uint64_t moves_n(const Move* mv, int n, uint64_t a, u
 }
 
 // resident CTAs per SM: 6 (40 registers) except max-mult, whose 64-bit words
-// need 48 registers to stay out of local memory (5)
+// need 48 registers to stay out of local memory (5).  Re-measured after the
+// per-CTA candidate counters (scripts/ab.sh, same box): 7 or 8 / 6 CTAs per SM
+// spill 24-32 B and run 4-6% slower on C2 (23.1-23.5 vs 22.0-22.3 ms), 2-3% on C5.
 #ifndef FJ_MINB_MX
 #define FJ_MINB_MX 5
 #endif
