@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(256) direct_extract2_k(void* __restrict__ f, u
   base = s_base + wtot[warp];
   }
 #pragma unroll 1
-  for (int j = 0; j < WPT; ++j) {
+  for (int j = 0; j < (wsum ? WPT : 0); ++j) {  // a warp whose words are all clean has nothing to do
     const uint32_t mm = m[j];
     const uint32_t cnt = __popc(mm);
     uint32_t inc = cnt;

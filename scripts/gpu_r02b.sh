@@ -42,6 +42,8 @@ sync1) timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_til
     for c in C1 C1 C2; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_sync1_$c.json 2>/dev/null; echo "$c $(cut -c1-140 gpurun_out/bench_sync1_$c.json)"; done
     LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 4 2>&1 | tail -3 ;;
 extune) for rep in 1 2; do for cfg in "2 8" "4 8" "2 12" "4 4"; do set -- $cfg; LOBSTER_EX_WPT=$1 LOBSTER_EX_CTAS=$2 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_extune.json 2>/dev/null; echo "wpt=$1 ctas=$2 $(cut -c100-140 gpurun_out/bench_extune.json)"; done; done ;;
+skip) timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_deep.py tests/test_gpu_dmaxmin.py -x -q > gpurun_out/skip_tests.log 2>&1; tail -2 gpurun_out/skip_tests.log
+    for c in C2 C2 C2 C5 SG; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_skip.json 2>/dev/null; echo "$c $(cut -c100-140 gpurun_out/bench_skip.json)"; done ;;
 c1log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C1 5 > gpurun_out/c1log.txt 2>&1; tail -30 gpurun_out/c1log.txt ;;
 c3log) LOBSTER_LOG=1 timeout 300 python scripts/profile_cfg.py C3 3 > gpurun_out/c3log.txt 2>&1; tail -12 gpurun_out/c3log.txt ;;
 c3full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_fixpoint -s 2 -c 1 -o gpurun_out/prof_tile python scripts/profile_cfg.py C3 2 > gpurun_out/ncu_tile.log 2>&1; tail -2 gpurun_out/ncu_tile.log ;;
